@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 scoring path.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C4]
+
+One step = one pass of the whole hot path over one batch: score_batch (decode + mask + simulator
++ GP posterior + EI + CTA top-k + pool merge) of the workload's candidate batch, then topk
+(FP64 refine, certification, D2H).  Workload (N=1): C4 -- the Llama-3 70B fine-tuning space on
+256 simulated A100s, 10^8 candidates sampled from its 3.57e8 valid-structure positions, 256
+observed points, EI, k = 32 (BASELINE.json configs[3]; the largest single-GPU configuration).
+N > 1 (torchrun, one process per GPU, NCCL): the same 10^8 candidates are split across ranks
+(strong scaling) and the per-GPU pools are merged with one all-gather.
+
+Timing: W warm-up steps; K timed steps, each bracketed by CUDA events on the launching stream
+after an L2 flush (256 MiB write, untimed); barrier + synchronize around the timed region; the
+max over ranks is reported.  nvidia-smi clocks are sampled during the timed region.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidate configs scored/s (mask+sim+EI+top-k)"
+WORKLOAD = {
+    "C4": "C4: Llama-3 70B fine-tuning space on 256xA100 (16 knobs, 1.18e11 raw / 3.57e8 valid-structure "
+          "positions), 1e8 sampled candidates, M=256 observed, EI, top-32",
+    "C5": "C5: Mixtral 8x7B space on 512xA100 (1.27e9 raw index range), all 5.55e6 positions, M=128, EI, top-32",
+    "C2": "C2: Llama-3 8B on 64xA100, all 73,176 positions, M=64, EI, top-32",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample for cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def load_doc(cfg):
+    with open(os.path.join(ROOT, "spaces", f"{cfg}.json")) as fh:
+        return json.load(fh)
+
+
+def flops_per_valid(M, d):
+    """Algorithmic FP32 flops per valid candidate of the GP path:
+    cross-covariance M(3d+10), mu 2M, v = L^-1 k: M(M+1), ||v||^2 2M."""
+    if M == 0:
+        return 0
+    return M * (3 * d + 10) + 2 * M + M * (M + 1) + 2 * M
+
+
+def fp32_peak_tflops(sm_mhz, n_sm=148):
+    """FP32 SIMT peak: 148 SMs x 128 FP32 lanes x 2 flops/FMA x clock."""
+    return n_sm * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.p = None
+        self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
+        try:
+            self.fh = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-i", str(gpu_index), "-lms", "200"], stdout=self.fh,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def observed_with_library(sp, M, seed=0):
+    """The seeded observed set (synthgen recipe) drawn with the LIBRARY's decode/mask/simulator."""
+    import synthgen
+    sizes = [len(f["domain"]) for f in sp.doc["features"]]
+
+    def unrank(p):
+        raw = sp.cvi_to_raw(p)
+        return raw, sp.decode(raw)[0]
+
+    return synthgen.observed_set(M, seed, sp.n_cvi, sizes, unrank, lambda r: sp.simulate(r)[2],
+                                 lambda r: sp.simulate(r)[0])
+
+
+def cpu_baseline(cfg, raws, costs, seconds, seed=0):
+    """The oracle as it stands, on a bounded sample of the same workload (BLAS pinned to 1 thread)."""
+    from threadpoolctl import threadpool_limits
+    from oracle import run, space as S
+    doc = load_doc(cfg)
+    b = doc["bench"]
+    with threadpool_limits(1):
+        o = S.load_space(os.path.join(ROOT, "spaces", f"{cfg}.json"))
+        fit = run.observed_fit(o, raws, costs)
+        t0 = time.perf_counter()
+        done = 0
+        chunk = 2048
+        while time.perf_counter() - t0 < seconds:
+            run.score_batch(o, fit, b["mode"], done, chunk, seed, acq=b["acq"])
+            done += chunk
+        dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": "candidates/s", "cores": 1, "kind": "oracle",
+            "sample": f"{cfg} {b['mode']} ordinals [0,{done}) of the bench batch (seed {seed}), "
+                      f"{dt:.1f} s, numpy/BLAS 1 thread; top-k sort excluded (bounded sample)"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle, timed on bounded samples of the same workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from threadpoolctl import threadpool_limits
+    from oracle import run, space as S
+    import synthgen
+    from oracle import sim
+    cfg = args.config
+    doc = load_doc(cfg)
+    b = doc["bench"]
+    o = S.load_space(os.path.join(ROOT, "spaces", f"{cfg}.json"))
+
+    def unrank(p):
+        dg = o.cvi_unrank(p)
+        return o.encode_raw(dg), dg
+
+    raws, costs = synthgen.observed_set(b["M"], 0, o.n_cvi(), [f.n for f in o.features], unrank,
+                                        lambda r: bool(sim.simulate(o, [o.decode_raw(r)])[1][0]),
+                                        lambda r: float(sim.simulate(o, [o.decode_raw(r)])[0][0]))
+    chunk = 1024
+    with threadpool_limits(1):
+        fit = run.observed_fit(o, raws, costs)
+        times = []
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            rec = run.score_batch(o, fit, b["mode"], i * chunk, chunk, 0, acq=b["acq"])
+            run.topk(rec, b["k"])
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+    ms = 1e3 * sum(times) / len(times)
+    v = chunk / (ms / 1e3)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "candidates/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD.get(cfg, cfg), "candidates_per_step": chunk,
+                       "note": "oracle/ (plain numpy FP64) on a bounded sample of the workload per step"},
+            "cpu_baseline": {"value": v, "unit": "candidates/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{chunk} candidates per step, sample ordinals [{args.warmup * chunk},"
+                                       f"{(args.warmup + args.steps) * chunk})"},
+            "e2e": {"value": v, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2603_11603_b200.autoscout import Space
+    from paper_2603_11603_b200.shard import gather_merge, shard_range
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    cfg = args.config
+    doc = load_doc(cfg)
+    b = doc["bench"]
+    sp = Space(os.path.join(ROOT, "spaces", f"{cfg}.json"), local)
+    M, k, acq, mode = b["M"], b["k"], b["acq"], b["mode"]
+    raws, costs = observed_with_library(sp, M, 0)
+    sp.observe(raws, costs)
+    count = int(b.get("count", sp.n_cvi))
+    lo, n = shard_range(0, count, rank, world)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    vc = torch.zeros(1, dtype=torch.int64, device=dev)
+    cap = k + max(k, 64)
+
+    def step(valid_counter=None):
+        sp.score_batch(mode=mode, begin=lo, count=n, seed=0, acq=acq, k=k, d_valid_count=valid_counter,
+                       stream=stream)
+        if world == 1:
+            return sp.topk(k, stream=stream)
+        pool, npool, cut = sp.topk_pool(k, cap, stream=stream)
+        return gather_merge(pool, npool, cut, k, device=dev)[0]
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    sp.set_timing(True)
+    launches0 = sp.n_launches()
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kern_ms = []
+    vc.zero_()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)                     # untimed L2 flush (256 MiB > 126 MB L2)
+        ev[i][0].record(stream)
+        top = step(vc)
+        ev[i][1].record(stream)
+        kern_ms.append(sp.last_kernel_ms())
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = sp.n_launches() - launches0
+    step_ms = [a.elapsed_time(b_) for a, b_ in ev]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    valid_per_step = int(vc.item()) / args.steps
+    vtot = torch.tensor([valid_per_step], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vtot)
+    valid_per_step_all = float(vtot.item())
+
+    # ---- end to end through the public API with host buffers (observe from pinned host arrays)
+    import numpy as np
+    h_raw = torch.tensor(np.asarray(raws, dtype=np.int64)).pin_memory()
+    h_cost = torch.tensor(np.asarray(costs, dtype=np.float64)).pin_memory()
+    e2e_ms = []
+    for i in range(max(3, args.steps // 2)):
+        flush.fill_(i & 0xFF)
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sp.observe_clear()
+        sp.observe(h_raw.numpy().view(np.uint64), h_cost.numpy(), stream=stream)
+        step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms.append(e0.elapsed_time(e1))
+    te = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_step_ms = float(te.item())
+    d = len(doc["features"])
+    Mp = ((M + 3) // 4) * 4
+    DP = ((d + 3) // 4) * 4
+    nb = Mp // 4
+    h2d = 4 * Mp * DP + 8 * Mp + 64 * nb * (nb + 1) // 2 + 8 * M * d + 8 * M + 8 * M * M
+    d2h = 4 + 8 + 16 * cap
+
+    if rank == 0:
+        score_ms = statistics.mean(x[0] for x in kern_ms)
+        merge_ms = statistics.mean(x[1] for x in kern_ms)
+        fl = flops_per_valid(M, d) * valid_per_step
+        sm_max = (clk or {}).get("sm_max_mhz") or 1965.0
+        peak = fp32_peak_tflops(sm_max)
+        achieved = fl / (score_ms * 1e-3) / 1e12 if score_ms > 0 else 0.0
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "score_kernel_traffic.json")
+        if os.path.exists(prof):
+            with open(prof) as fh:
+                traffic = json.load(fh).get("dram_bytes_per_launch")
+        line = {
+            "metric": METRIC, "value": count / (ms_per_step / 1e3), "unit": "candidates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD.get(cfg, cfg), "space": f"spaces/{cfg}.json", "mode": mode,
+                       "candidates_per_step": count, "observed_M": M, "acq": acq, "k": k,
+                       "valid_per_step": valid_per_step_all, "l2": "flushed (256 MiB write) before every timed step",
+                       "parallelism": f"dp{world} (candidate-range shards, one all-gather)",
+                       "arith": "decode int; simulator + resource check + acquisition FP64; GP FP32; refine FP64"},
+            "valid_per_s": valid_per_step_all / (ms_per_step / 1e3),
+            "roofline": {"bound": "alu", "kernel": "score_kernel", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": traffic,
+                         "kernel_ms": score_ms, "merge_ms": merge_ms, "kernel_share": score_ms / ms_per_step,
+                         "flops_per_valid": flops_per_valid(M, d),
+                         "peak_source": f"FP32 SIMT 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz (guide unit counts)"},
+            "e2e": {"value": count / (e2e_step_ms / 1e3), "unit": "candidates/s", "ms_per_step": e2e_step_ms,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "path": "observe(host arrays) + score_batch + topk(host outputs) via the C ABI"},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "top1": {"raw": top[0][0], "score": top[0][1]} if top else None,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg, raws, costs, args.cpu_seconds)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,157 @@
+/*
+ * autoscout.h -- C ABI of the B200-native AutoScout candidate-scoring library (libautoscout.so).
+ *
+ * What it computes.  AutoScout (arXiv 2603.11603) searches a hierarchical configuration space
+ * of sparse structural knobs and dense execution knobs "valid only under specific upstream
+ * decisions" (masking function M(s), :171).  The data-parallel hot path
+ * built here scores MANY candidate configurations at once (BASELINE.json north_star): for each
+ * candidate index it decodes the configuration, applies conditional validity, runs the
+ * analytical iteration-time/memory simulator, evaluates a GP posterior and an acquisition
+ * against the profiled set, and keeps a top-k ("the top-K configurations ... are prioritized
+ * for re-evaluation").  All readings of ambiguous passages are listed in
+ * DESIGN.md §3; formulas in SURVEY.md Appendix A.
+ *
+ * Conventions.
+ *  - Every call returns as_status; nothing throws across the ABI.  On error the thread-local
+ *    message is available from autoscout_last_error().
+ *  - "host" pointers are caller-owned CPU memory read/written during the call only.
+ *    "device" pointers are caller-owned CUDA memory on the handle's device (typically PyTorch
+ *    tensors) that must stay alive until the enqueued work on `cuda_stream` completes.
+ *  - cuda_stream is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - A handle is bound to one CUDA device (or to none: cuda_device = -1 gives a host-only
+ *    handle that supports parsing and the host introspection calls, never scoring).  Handles
+ *    are not thread-safe; use one per thread/rank.
+ *  - Index spaces (R2-R4): the RAW index is the mixed-radix number of the digit
+ *    tuple, first-declared feature most significant.  A CVI position p in [0, n_cvi) is the
+ *    p-th raw index, ascending, that satisfies the canonical-inactive rule and every structural
+ *    (non-resource) constraint of the space.  n_cvi must be < 2^32.
+ *  - Scores: higher is better.  EI is reported as log EI; LCB as kappa*sigma - mu; SIM as
+ *    -ln(cost_sim).  Ties are broken by the smaller raw index.
+ */
+#ifndef AUTOSCOUT_H
+#define AUTOSCOUT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct as_space as_space; /* opaque */
+
+typedef enum {
+  AS_OK = 0,
+  AS_ERR_INVALID_ARG = 1,    /* null pointer, bad enum, k out of range, non-finite/<=0 cost */
+  AS_ERR_SPACE_SCHEMA = 2,   /* malformed JSON, unknown key/type, default not in domain */
+  AS_ERR_SPACE_CYCLE = 3,    /* cyclic activation dependency */
+  AS_ERR_SPACE_ORDER = 4,    /* forward gate reference, or a tail gating group not contiguous (R4) */
+  AS_ERR_SPACE_EMPTY = 5,    /* empty domain or no valid configuration */
+  AS_ERR_INDEX_RANGE = 6,    /* raw >= n_raw, cvi >= n_cvi, batch outside [0, n_cvi) */
+  AS_ERR_INVALID_CONFIG = 7, /* observed configuration not valid (structure or resource check) */
+  AS_ERR_NO_OBSERVATIONS = 8,/* EI requested with no observed configuration */
+  AS_ERR_NUMERIC = 9,        /* Cholesky of the GP covariance failed */
+  AS_ERR_CAPACITY = 10,      /* a compile-time limit (features, domain size, M, k', n_cvi) exceeded */
+  AS_ERR_STATE = 11,         /* call not valid in the handle's state (e.g. topk before score, host-only handle) */
+  AS_ERR_UNCERTIFIED = 12,   /* top-k returned but the FP32 screen could not be certified */
+  AS_ERR_CUDA = 13,          /* CUDA runtime error */
+  AS_ERR_OOM = 14            /* device allocation failed */
+} as_status;
+
+typedef enum { AS_MODE_RANGE = 0, AS_MODE_SAMPLE = 1 } as_mode;
+typedef enum { AS_ACQ_EI = 0, AS_ACQ_LCB = 1, AS_ACQ_SIM = 2 } as_acq;
+
+typedef struct {
+  uint64_t n_raw;        /* product of the domain sizes */
+  uint64_t n_cvi;        /* number of structurally valid configurations */
+  int32_t n_features;    /* d */
+  int32_t n_structures;  /* distinct assignments of the structural prefix */
+  int32_t n_prefix;      /* structural prefix length (R4) */
+  int32_t n_components;  /* tail gating groups */
+  int32_t n_observed;    /* M of the current fit */
+  int32_t max_observed;  /* capacity for M */
+  uint64_t n_launches;   /* kernels this handle has launched so far (score, merge, refine, mask) */
+} as_space_info;
+
+typedef struct {
+  int32_t mode;          /* as_mode.  RANGE: candidate j is CVI position begin+j.
+                            SAMPLE: candidate j is pi_seed(begin+j), a Feistel permutation of [0,n_cvi) */
+  int32_t acq;           /* as_acq */
+  uint64_t begin;        /* first position (RANGE) or first sample ordinal (SAMPLE) */
+  uint64_t count;        /* number of candidates; begin+count <= n_cvi */
+  uint64_t seed;         /* SAMPLE permutation seed */
+  double kappa;          /* LCB exploration weight (default 2) */
+  double xi;             /* EI margin (default 0) */
+  int32_t k;             /* the top-k that autoscout_topk will request (1..1024); sizes the pool */
+  int32_t accumulate;    /* 0: reset the running pool before merging this batch; 1: merge into it */
+  float* d_scores;       /* device, nullable, [count] in batch order: FP32 score, -INF if masked */
+  uint64_t* d_raw;       /* device, nullable, [count] raw index of each candidate */
+  uint64_t* d_valid_count; /* device, nullable: atomically incremented by #valid candidates */
+} as_score_args;
+
+/* Parse and validate a space JSON document (schema: DESIGN.md §2), build the
+ * per-structure tables of the compact valid index, and upload them to `cuda_device` (-1: host only).
+ * Source: SPEC.md:54-62 load_space; Table 1. */
+as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as_space** out);
+void autoscout_space_destroy(as_space* s);
+as_status autoscout_space_info(const as_space* s, as_space_info* out);
+
+/* Append n profiled configurations (raw index, cost > 0 in objective units) and refit the GP on
+ * the host in FP64 (Cholesky; alpha = K^-1 r; W = L^-1; f* = min ln c), then upload the fit on
+ * `cuda_stream`.  n may be 0 (refit only).  Errors: INDEX_RANGE, INVALID_CONFIG, INVALID_ARG,
+ * CAPACITY (M > max_observed), NUMERIC.  Source: PAPER.md:263-265 (profiled vs simulated
+ * evaluations); GP reading DESIGN.md R9. */
+as_status autoscout_observe(as_space* s, const uint64_t* raw_idx, const double* cost, int64_t n,
+                            void* cuda_stream);
+as_status autoscout_observe_clear(as_space* s);
+/* Host introspection of the current fit: M, b (prior offset), f* (incumbent ln cost). */
+as_status autoscout_observe_info(const as_space* s, int32_t* m_out, double* b_out, double* fstar_out);
+
+/* Enqueue the scoring of a batch (one kernel launch + one pool-merge launch, asynchronous).
+ * Candidates are generated from indices in registers; per-candidate outputs are optional.
+ * Errors: INDEX_RANGE, NO_OBSERVATIONS, INVALID_ARG, STATE (host-only handle), CUDA. */
+as_status autoscout_score_batch(as_space* s, const as_score_args* a, void* cuda_stream);
+
+/* Finalize: FP64 re-score of the running pool, order (score desc, raw asc), certification
+ * (doubles the pool and re-scores the recorded batches on failure).  Writes
+ * n_out = min(k, #valid finite scores) entries to the host arrays raw_out/score_out (length >= k).
+ * Synchronizes `cuda_stream`.  Errors: STATE (nothing scored), UNCERTIFIED, CUDA. */
+as_status autoscout_topk(as_space* s, int32_t k, uint64_t* raw_out, double* score_out, int32_t* n_out,
+                         void* cuda_stream);
+
+/* Sharding.  topk_pool: refine the local pool and copy it to host memory as
+ * `cap` entries {double score; uint64_t raw} ordered (score desc, raw asc); n_out = entries
+ * written; *cut_out = upper bound on the score of every locally scored candidate NOT in the
+ * pool (-INF if none was dropped).  topk_merge: merge `n_pools` gathered pools laid out as
+ * [n_pools][cap] entries with per-pool counts and cuts; certify globally.  Host-only work:
+ * valid on a host-only handle.  *certified_out = 1 if the merged top-k is certified. */
+as_status autoscout_topk_pool(as_space* s, int32_t k, void* pool_out, int32_t cap, int32_t* n_out,
+                              double* cut_out, void* cuda_stream);
+as_status autoscout_topk_merge(const as_space* s, const void* pools, const int32_t* counts,
+                               const double* cuts, int32_t n_pools, int32_t cap, int32_t k,
+                               uint64_t* raw_out, double* score_out, int32_t* n_out,
+                               int32_t* certified_out);
+
+/* Exact host introspection (parity and tests). */
+as_status autoscout_decode(const as_space* s, uint64_t raw, int32_t* digits_out, int32_t* valid_out);
+as_status autoscout_cvi_to_raw(const as_space* s, uint64_t cvi, uint64_t* raw_out);
+as_status autoscout_sample_to_cvi(const as_space* s, uint64_t seed, uint64_t ordinal, uint64_t* cvi_out);
+/* FP64 simulator + resource check of one configuration (host).  ok_out = G4 passes. */
+as_status autoscout_simulate(const as_space* s, uint64_t raw, double* cost_out, double* mem_out,
+                             int32_t* ok_out);
+/* Mask kernel: validity bit of every raw index in [raw_begin, raw_begin+count) -> d_bits
+ * (device, (count+31)/32 words, bit i of word w = raw_begin+32w+i); d_valid_count (device,
+ * nullable) += number of valid.  Valid = canonical-inactive + structural constraints + resource. */
+as_status autoscout_mask_range(as_space* s, uint64_t raw_begin, uint64_t count, uint32_t* d_bits,
+                               uint64_t* d_valid_count, void* cuda_stream);
+
+/* Device-time of the last score kernel launch in ms (CUDA events on the launching stream,
+ * recorded when `timing` was enabled), for the roofline report in bench.py. */
+as_status autoscout_set_timing(as_space* s, int32_t enable);
+as_status autoscout_last_kernel_ms(as_space* s, double* score_ms, double* merge_ms);
+
+const char* autoscout_last_error(void); /* thread-local */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AUTOSCOUT_H */

@@ -97,11 +97,18 @@ class Fit:
         m0 = np.asarray(m0, dtype=np.float64)
         if self.M == 0:
             return m0 + 0.0, np.full(len(m0), self.sf2), np.zeros((len(m0), 0))
-        ks = cross_cov(self.space, X, self.O)                 # [B, M]
-        mu = m0 + self.b + ks @ self.alpha
-        sol = np.linalg.solve(self.K, ks.T)                   # K^-1 k*, [M, B]
-        quad = np.sum(ks.T * sol, axis=0)
-        s2 = np.maximum(self.sf2 - quad, 0.0)
+        mu = np.empty(len(m0))
+        s2 = np.empty(len(m0))
+        ks_all = []
+        for lo in range(0, len(m0), 2048):                    # chunks bound memory only
+            ks = cross_cov(self.space, X[lo:lo + 2048], self.O)          # [B, M]
+            mu[lo:lo + 2048] = m0[lo:lo + 2048] + self.b + ks @ self.alpha
+            sol = np.linalg.solve(self.K, ks.T)                          # K^-1 k*, [M, B]
+            quad = np.sum(ks.T * sol, axis=0)
+            s2[lo:lo + 2048] = np.maximum(self.sf2 - quad, 0.0)
+            if len(m0) <= 4096:
+                ks_all.append(ks)
+        ks = np.concatenate(ks_all) if ks_all else None
         return mu, s2, ks
 
 

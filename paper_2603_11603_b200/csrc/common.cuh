@@ -1,0 +1,313 @@
+// Shared host/device definitions of the scoring path: device data layout, candidate decode,
+// analytical simulator + FP64 resource check, acquisition.  Compiled for the host (observe,
+// introspection) and for sm_100a (score / refine / mask kernels) from the same source.
+//
+// Formulas: SURVEY.md Appendix A (A.1 index spaces, A.2 bit-exact resource check, A.3 training
+// simulator, A.4 serving simulator, A.5 surrogate/acquisition); readings in DESIGN.md §3.
+#pragma once
+#include <cmath>
+#include <cstdint>
+
+#ifdef __CUDACC__
+#define AS_HD __host__ __device__ __forceinline__
+#else
+#define AS_HD inline
+#endif
+
+namespace as {
+
+constexpr int DMAX = 24;        // max features (3 x 8 digit bytes)
+constexpr int VMAX = 64;        // max domain size (predicates are 64-bit digit masks)
+constexpr int TUPW = 8;         // max features in one tail gating group
+constexpr int MMAX = 256;       // max observed configurations (round-1 SMEM budget)
+constexpr int MAX_CLS = 4;      // device classes of the simulated cluster
+
+// ---- digit vector: 24 digits x 8 bits in three 64-bit words (feature j -> word j>>3, byte j&7)
+struct DV {
+  uint64_t w[3];
+};
+AS_HD uint32_t dv_get(const DV& v, int j) {
+  uint64_t x = (j < 8) ? v.w[0] : ((j < 16) ? v.w[1] : v.w[2]);
+  return static_cast<uint32_t>((x >> ((j & 7) * 8)) & 0xFFu);
+}
+AS_HD void dv_set(DV& v, int j, uint32_t d) {
+  uint64_t m = ~(0xFFull << ((j & 7) * 8));
+  uint64_t b = static_cast<uint64_t>(d) << ((j & 7) * 8);
+  if (j < 8) v.w[0] = (v.w[0] & m) | b;
+  else if (j < 16) v.w[1] = (v.w[1] & m) | b;
+  else v.w[2] = (v.w[2] & m) | b;
+}
+
+// One entry of a per-structure tail-component list: the component's digits pre-placed in the
+// digit vector, its contribution to the raw index, and its activity bits.
+struct Tuple {
+  DV dv;
+  uint64_t raw;
+  uint32_t act;
+  uint32_t pad;
+};
+
+enum Knob {
+  K_PP, K_VPP, K_TP, K_DP, K_CP, K_EP, K_MBS, K_AR, K_ARL, K_SP, K_TPOV, K_TPCOMM, K_DOPT, K_OVG,
+  K_OVP, K_BUCKET, K_DDP, K_DISP, K_NS, K_CPF, K_MBT, K_U, NKNOB
+};
+
+struct SimParams {
+  int mode;                  // 0 spec, 1 derived (A.3), 2 serve (A.4)
+  int kf[NKNOB];             // feature index bound to each knob, -1 if the preset lacks it
+  double neutral[NKNOB];     // value of an absent knob (A.3 "Knobs absent from a preset")
+  int n_cls;                 // device classes, sorted by relative throughput (fastest first)
+  int cls_count[MAX_CLS];
+  double cls_cap[MAX_CLS];   // bytes
+  double cls_eff[MAX_CLS];
+  // SPEC mode constants (S:547 + DESIGN.md R8)
+  double F_work, alpha_tp, alpha_dp, r_ar, B, P_mem, A_mem;
+  // derived / serving constants (model + hardware descriptor)
+  double L, h, a, kv, S, GBS, P, P_exp, E, topk, peak, mfu0, bw_intra, bw_inter, gpn, n_sm;
+  double dh, ffn, P_in, P_out, mml, w_tpot, bw_hbm, G;
+};
+
+// ---- exact FP64 arithmetic for the resource check (A.2): no FMA contraction, fixed order.
+#ifdef __CUDA_ARCH__
+AS_HD double xadd(double a, double b) { return __dadd_rn(a, b); }
+AS_HD double xsub(double a, double b) { return __dsub_rn(a, b); }
+AS_HD double xmul(double a, double b) { return __dmul_rn(a, b); }
+AS_HD double xdiv(double a, double b) { return __ddiv_rn(a, b); }
+#else
+AS_HD double xadd(double a, double b) { return a + b; }   // host: compiled with -ffp-contract=off
+AS_HD double xsub(double a, double b) { return a - b; }
+AS_HD double xmul(double a, double b) { return a * b; }
+AS_HD double xdiv(double a, double b) { return a / b; }
+#endif
+
+struct Knobs {
+  double v[NKNOB];
+  uint32_t act;  // bit k: knob k bound to an active feature
+};
+
+// Effective knob values of a decoded canonical configuration: inactive features carry their
+// default digit (G1), so the digit's value is the effective value.
+AS_HD void load_knobs(const SimParams& P, const double* val, const DV& dv, uint32_t act_bits, Knobs& k) {
+  k.act = 0;
+#pragma unroll
+  for (int i = 0; i < NKNOB; ++i) {
+    int f = P.kf[i];
+    if (f >= 0) {
+      k.v[i] = val[f * VMAX + dv_get(dv, f)];
+      if ((act_bits >> f) & 1u) k.act |= (1u << i);
+    } else {
+      k.v[i] = P.neutral[i];
+    }
+  }
+}
+
+AS_HD void device_assignment(const SimParams& P, double world, double& eff, double& cap) {
+  double rem = world;
+  eff = INFINITY;
+  cap = INFINITY;
+  for (int i = 0; i < P.n_cls; ++i) {
+    if (rem <= 0.0) break;
+    eff = fmin(eff, P.cls_eff[i]);
+    cap = fmin(cap, P.cls_cap[i]);
+    rem -= static_cast<double>(P.cls_count[i]);
+  }
+}
+
+AS_HD double bw_of(const SimParams& P, double span) { return span <= P.gpn ? P.bw_intra : P.bw_inter; }
+AS_HD double clamp(double x, double lo, double hi) { return fmin(fmax(x, lo), hi); }
+
+// Simulator: cost in objective units (s/iter, or the scalarized serving cost), resource check.
+// mem_out = training memory (bytes) or serving usable bytes.
+AS_HD void simulate(const SimParams& P, const Knobs& k, double& cost, bool& ok, double& mem_out) {
+  const double pp = k.v[K_PP], tp = k.v[K_TP], dp = k.v[K_DP], cp = k.v[K_CP], ep = k.v[K_EP],
+               mbs = k.v[K_MBS];
+  if (P.mode == 0) {  // ---- SPEC synthetic_cost, S:489-497 verbatim
+    const bool ar = k.v[K_AR] == 2.0, sp = k.v[K_SP] == 1.0;
+    const double world = pp * tp * dp * cp;
+    double eff, cap;
+    device_assignment(P, world, eff, cap);
+    const double micro = P.B / (dp * mbs);
+    const double r = ar ? P.r_ar : 1.0;
+    const double t_comp = P.F_work * r / (world * eff * (1.0 + 0.1 * log2(mbs)));
+    const double t_bubble = t_comp * (pp - 1.0) / micro;
+    const double ov = tp > 1.0 ? clamp((k.v[K_TPCOMM] - 12.0) / 16.0, 0.0, 0.5) : 0.0;
+    const double t_tp = P.alpha_tp * (tp - 1.0) / tp * (1.0 - ov) * ((sp && tp > 1.0) ? 0.8 : 1.0);
+    const double lb = log2(k.v[K_BUCKET]) - 2.0;
+    const double bp = dp > 1.0 ? 1.0 + 0.1 * lb * lb : 0.0;
+    const double t_dp = P.alpha_dp * (dp - 1.0) / dp * bp;
+    const double t_ep = P.alpha_tp * 0.5 * (ep - 1.0) / ep;
+    cost = t_comp + t_bubble + t_tp + t_dp + t_ep;
+    // S:496 in the normative order (R7): (P_mem/(pp*tp)) + (((A_mem*mbs)*f)/cp)
+    const double m1 = xdiv(P.P_mem, xmul(pp, tp));
+    const double m2 = xmul(P.A_mem, mbs);
+    const double m3 = xmul(m2, ar ? 0.3 : 1.0);
+    const double m4 = xdiv(m3, cp);
+    const double mem = xadd(m1, m4);
+    mem_out = mem;
+    ok = mem <= cap;
+    return;
+  }
+  if (P.mode == 1) {  // ---- derived mode, SURVEY A.3
+    const double vpp = k.v[K_VPP];
+    const double arc = k.v[K_AR];
+    const bool full = arc == 2.0, sel = arc == 1.0, sp = k.v[K_SP] == 1.0;
+    const double world = pp * tp * dp * cp;
+    const double m = P.GBS / (dp * mbs);
+    const double L_st = xdiv(P.L, xmul(pp, vpp));
+    const bool arl_active = (k.act >> K_ARL) & 1u;
+    const double f_rc = full ? (arl_active ? fmin(1.0, xdiv(k.v[K_ARL], L_st)) : 1.0) : 0.0;
+    const double r = 1.0 + 0.33 * f_rc + (sel ? 0.03 : 0.0);
+    const double P_act = P.P - P.P_exp + P.P_exp * P.topk / P.E;
+    const double T_work = P.GBS * P.S * (6.0 * P_act + 12.0 * P.L * P.h * P.S) / (P.peak * P.mfu0);
+    const bool tpc_active = (k.act >> K_TPCOMM) & 1u;
+    const double steal = tpc_active ? 0.5 * k.v[K_TPCOMM] / P.n_sm : 0.0;
+    const double t_comp = T_work * r * (1.0 + steal) / (world * (1.0 + 0.1 * log2(mbs)));
+    const double t_bubble = t_comp * (pp - 1.0) / (m * vpp);
+    const double ov = (tp > 1.0 && tpc_active) ? clamp((k.v[K_TPCOMM] - 12.0) / 16.0, 0.0, 0.5) : 0.0;
+    const double t_tp = tp > 1.0 ? 16.0 * P.L * P.GBS * P.S * P.h / (pp * dp * cp * bw_of(P, tp)) *
+                                       (tp - 1.0) / tp * (1.0 - ov) * (sp ? 0.8 : 1.0)
+                                 : 0.0;
+    const double P_loc = xdiv(xadd(P.P - P.P_exp, xdiv(P.P_exp, ep)), xmul(pp, tp));
+    const double lb = log2(k.v[K_BUCKET]) - 2.0;
+    const bool ovg = k.v[K_OVG] == 1.0, ovp = k.v[K_OVP] == 1.0;
+    const double t_dp = dp > 1.0 ? 4.0 * P_loc / bw_of(P, tp * cp * dp) * (dp - 1.0) / dp *
+                                       (1.0 + 0.1 * lb * lb) * (ovg ? 0.5 : 1.0) * (ovp ? 0.75 : 1.0)
+                                 : 0.0;
+    const double t_ep = ep > 1.0 ? 8.0 * P.topk * P.L * P.GBS * P.S * P.h /
+                                       (pp * dp * cp * (sp ? tp : 1.0) * bw_of(P, tp * cp * ep)) *
+                                       (ep - 1.0) / ep * (k.v[K_DISP] == 1.0 ? 1.5 : 1.0)
+                                 : 0.0;
+    const double t_cp = cp > 1.0 ? 0.5 * 12.0 * P.L * P.GBS * P.S * P.kv * (P.h / P.a) /
+                                       (pp * dp * bw_of(P, tp * cp)) * (cp - 1.0) / cp
+                                 : 0.0;
+    cost = t_comp + t_bubble + t_tp + t_dp + t_ep + t_cp;
+    // memory, normative FP64 order (R7)
+    const bool dopt = k.v[K_DOPT] == 1.0;
+    const double bpp = dopt ? xadd(6.0, xdiv(12.0, dp)) : 18.0;
+    const double act = sp ? xdiv(34.0, tp) : xadd(10.0, xdiv(24.0, tp));
+    const double af = xsub(xsub(1.0, xmul(0.7, f_rc)), sel ? 0.2 : 0.0);
+    const double t1 = xmul(P_loc, bpp);
+    double t2 = xmul(P.L, xdiv(P.S, cp));
+    t2 = xmul(t2, P.h);
+    t2 = xmul(t2, mbs);
+    t2 = xmul(t2, act);
+    t2 = xmul(t2, af);
+    const double mem = xadd(t1, t2);
+    double eff, cap;
+    device_assignment(P, world, eff, cap);
+    mem_out = mem;
+    ok = mem <= cap;
+    return;
+  }
+  // ---- serving, SURVEY A.4
+  const double ns = k.v[K_NS], u = k.v[K_U], mbt = k.v[K_MBT];
+  const bool cpf = k.v[K_CPF] == 1.0;
+  double eff, cap;
+  device_assignment(P, tp, eff, cap);
+  const double W = 2.0 * P.P;
+  const double kvb = xdiv(xmul(xmul(xmul(4.0, P.L), P.kv), P.dh), tp);
+  const double mbt_eff = cpf ? mbt : P.mml;
+  const double t1 = xmul(u, cap);
+  const double t2 = xdiv(W, tp);
+  const double t3 = xmul(mbt_eff, 4.0 * P.h + 2.0 * P.ffn);
+  const double t4 = xmul(t3, 2.0);
+  const double t5 = xdiv(t4, tp);
+  const double usable = xsub(xsub(xsub(t1, t2), t5), 1e9);
+  const double kv_tok = floor(xdiv(usable, kvb));
+  ok = (usable > 0.0) && (kv_tok >= P.mml);
+  mem_out = usable;
+  double b = fmin(ns, floor(kv_tok / (P.P_in + P.P_out)));
+  if (!ok) b = 1.0;
+  const double T_w = (W / tp) / P.bw_hbm;
+  const double T_kv = b * (P.P_in + P.P_out / 2.0) * kvb / P.bw_hbm;
+  const double T_fl = 2.0 * P.P * b / (tp * P.peak);
+  const double T_ar = tp > 1.0 ? 2.0 * P.L * (2.0 * (tp - 1.0) / tp * b * P.h * 2.0 / P.bw_intra + 5e-6) : 0.0;
+  const double t_sched = 5e-4;
+  const double t_dec = fmax(T_w + T_kv, T_fl) + T_ar + t_sched;
+  const double p = b * P.P_in / P.P_out;
+  const double T_pf = 2.0 * P.P / (tp * P.peak * 0.6);
+  const double t_pf = cpf ? p * T_pf + fmax(0.0, p - (mbt - b)) / mbt * (T_w + t_sched)
+                          : (b / P.P_out) * (T_w + t_sched) + p * T_pf;
+  const double TPOT = t_dec + t_pf;
+  const double thr = (P.G / tp) * b / TPOT;
+  cost = pow(TPOT, P.w_tpot) * pow(thr, -(1.0 - P.w_tpot));
+}
+
+// ---- acquisition in FP64 (R10)
+constexpr double LN_2PI = 1.8378770664093454835606594728112;
+constexpr double INV_SQRT_2PI = 0.39894228040143267793994605993438;
+constexpr double INV_SQRT2 = 0.70710678118654752440084436210485;
+
+AS_HD double lnh(double z) {
+  if (z >= -10.0) {
+    const double phi = exp(-0.5 * z * z) * INV_SQRT_2PI;
+    const double Phi = 0.5 * erfc(-z * INV_SQRT2);
+    return log(phi + z * Phi);
+  }
+  const double z2 = z * z;
+  const double z4 = z2 * z2;
+  return -0.5 * z2 - 0.5 * LN_2PI - 2.0 * log(-z) +
+         log1p(-3.0 / z2 + 15.0 / z4 - 105.0 / (z4 * z2) + 945.0 / (z4 * z4));
+}
+
+// acq: 0 EI (log EI), 1 LCB, 2 SIM
+AS_HD double acquisition(int acq, double mu, double s2, double m0, double fstar, double xi, double kappa) {
+  if (acq == 2) return -m0;
+  const double sigma = sqrt(fmax(s2, 0.0));
+  if (acq == 1) return kappa * sigma - mu;
+  const double u = fstar - mu - xi;
+  if (sigma == 0.0) return u > 0.0 ? log(u) : -INFINITY;
+  return log(sigma) + lnh(u / sigma);
+}
+
+// ---- Matern-5/2 / RBF (A.5)
+constexpr double SQRT5 = 2.2360679774997896964091736687313;
+AS_HD double kernel64(int kind, double sf2, double r2) {
+  const double r = sqrt(r2);
+  if (kind == 0) return sf2 * (1.0 + SQRT5 * r + (5.0 / 3.0) * r2) * exp(-SQRT5 * r);
+  return sf2 * exp(-0.5 * r2);
+}
+
+// ---- splitmix64 + Feistel permutation of [0, n) for SAMPLE mode (R3)
+constexpr uint64_t GOLDEN = 0x9E3779B97F4A7C15ull;
+AS_HD uint64_t splitmix64(uint64_t z) {
+  z += GOLDEN;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+struct FeistelKey {
+  uint64_t k[4];
+  uint64_t n;
+  uint32_t h;
+  uint64_t mask;
+};
+inline FeistelKey feistel_make(uint64_t n, uint64_t seed) {
+  FeistelKey f;
+  f.n = n;
+  uint32_t b = 0;
+  while ((1ull << b) < n) ++b;  // ceil(log2 n)
+  if (b < 2) b = 2;
+  if (b & 1u) ++b;
+  f.h = b / 2;
+  f.mask = (1ull << f.h) - 1ull;
+  for (int r = 0; r < 4; ++r) f.k[r] = splitmix64(seed ^ (GOLDEN * static_cast<uint64_t>(r + 1)));
+  return f;
+}
+AS_HD uint64_t feistel_E(const FeistelKey& f, uint64_t x) {
+  uint64_t L = x >> f.h, R = x & f.mask;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    uint64_t nl = R;
+    R = L ^ (splitmix64(R ^ f.k[r]) & f.mask);
+    L = nl;
+  }
+  return (L << f.h) | R;
+}
+AS_HD uint64_t feistel_pi(const FeistelKey& f, uint64_t j) {
+  uint64_t x = feistel_E(f, j);
+  while (x >= f.n) x = feistel_E(f, x);
+  return x;
+}
+
+}  // namespace as

@@ -1,0 +1,710 @@
+// extern "C" boundary of libautoscout.so (include/autoscout.h): host orchestration of the
+// sm_100a kernels in kernels.cuh.  No torch types; plain pointers and sizes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/autoscout.h"
+#include "kernels.cuh"
+#include "space.hpp"
+
+using namespace as;
+
+namespace {
+thread_local std::string g_err;
+
+as_status fail(as_status code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                   \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess) {                                                          \
+      if (e_ == cudaErrorMemoryAllocation) return fail(AS_ERR_OOM, cudaGetErrorString(e_)); \
+      return fail(AS_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));     \
+    }                                                                                 \
+  } while (0)
+
+constexpr int KC_CAP = 4096;  // largest pool the merge kernel handles (P2 = 8192 keys = 64 KB)
+
+inline int next_pow2_h(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+size_t score_smem_bytes(int Mp, int DP, int d, int P) {
+  auto r16 = [](size_t b) { return (b + 15) & ~size_t(15); };
+  const int nb = Mp / 4;
+  size_t s = 0;
+  s += r16(sizeof(float) * 16 * (nb * (nb + 1) / 2));
+  s += r16(sizeof(float) * Mp * DP);
+  s += r16(sizeof(float) * Mp);
+  s += r16(sizeof(float) * Mp);
+  s += r16(sizeof(float) * Mp * 32);
+  s += r16(sizeof(float) * d * VMAX);
+  s += r16(sizeof(DV) * QCAP);
+  s += r16(sizeof(double) * QCAP);
+  s += r16(sizeof(uint64_t) * QCAP);
+  s += r16(sizeof(uint32_t) * QCAP);
+  s += r16(sizeof(uint32_t) * QCAP);
+  s += r16(sizeof(float) * 4 * 8 * 32);
+  s += r16(sizeof(uint64_t) * 32);
+  s += r16(sizeof(uint64_t) * P);
+  return s;
+}
+
+template <typename T>
+as_status dalloc(T** p, size_t n, std::vector<void*>& owned) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)));
+  owned.push_back(*p);
+  return AS_OK;
+}
+
+template <typename T>
+as_status upload(T** p, const std::vector<T>& v, std::vector<void*>& owned) {
+  as_status st = dalloc(p, v.size(), owned);
+  if (st != AS_OK) return st;
+  if (!v.empty()) CUDA_TRY(cudaMemcpy(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return AS_OK;
+}
+
+float key_score(uint64_t key) {
+  const uint32_t ord = ~static_cast<uint32_t>(key >> 32);
+  const uint32_t u = (ord & 0x80000000u) ? (ord & 0x7FFFFFFFu) : ~ord;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+struct Entry {
+  double score;
+  uint64_t raw;
+};
+static_assert(sizeof(Entry) == 16, "pool entry layout");
+
+bool entry_less(const Entry& a, const Entry& b) {  // score desc, raw asc
+  if (a.score != b.score) return a.score > b.score;
+  return a.raw < b.raw;
+}
+}  // namespace
+
+struct as_space {
+  HostSpace H;
+  int device = -1;
+  int n_sm = 0;
+  int smem_optin = 0;
+  std::vector<void*> owned;
+  DevSpace D{};
+  // observed set + fit
+  std::vector<uint64_t> obs_raw;
+  std::vector<double> obs_cost, obs_sim;
+  std::vector<DV> obs_dv;
+  std::vector<uint32_t> obs_act;
+  GPFit fit;
+  DevGP G{};
+  float *d_O = nullptr, *d_alpha = nullptr, *d_aabs = nullptr, *d_Wblk = nullptr;
+  double *d_O64 = nullptr, *d_alpha64 = nullptr, *d_W64 = nullptr;
+  std::vector<float> h_O, h_alpha, h_aabs, h_Wblk;
+  std::vector<double> h_O64, h_alpha64, h_W64;
+  // pool state
+  int KC = 0;
+  int KC_max = 0;
+  uint64_t* d_lists = nullptr;
+  size_t lists_cap = 0;
+  int* d_counts = nullptr;
+  uint64_t* d_drops = nullptr;
+  int counts_cap = 0;
+  uint64_t *d_pool = nullptr, *d_cut = nullptr, *d_valid = nullptr;
+  int* d_pool_n = nullptr;
+  double* d_ref_score = nullptr;
+  uint64_t* d_ref_raw = nullptr;
+  std::vector<as_score_args> batches;
+  bool scored = false;
+  uint64_t n_launches = 0;
+  // timing
+  bool timing = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool ev_recorded = false;
+};
+
+namespace {
+
+as_status upload_gp(as_space* s, cudaStream_t st) {
+  const HostSpace& H = s->H;
+  const GPFit& F = s->fit;
+  const int M = F.M, d = H.d;
+  const int Mp = M > 0 ? ((M + 3) / 4) * 4 : 0;
+  const int DP = ((d + 3) / 4) * 4;
+  const int nb = Mp / 4;
+  s->h_O.assign(static_cast<size_t>(Mp) * DP, 0.f);
+  s->h_alpha.assign(Mp, 0.f);
+  s->h_aabs.assign(Mp, 0.f);
+  s->h_Wblk.assign(static_cast<size_t>(16) * (nb * (nb + 1) / 2), 0.f);
+  s->h_O64.assign(static_cast<size_t>(M) * d, 0.0);
+  s->h_alpha64 = F.alpha;
+  s->h_W64 = F.Wl;
+  for (int i = 0; i < M; ++i) {
+    for (int j = 0; j < d; ++j) {
+      s->h_O[i * DP + j] = H.xt32[j * VMAX + dv_get(s->obs_dv[i], j)];
+      s->h_O64[i * d + j] = F.X[i * d + j];
+    }
+    s->h_alpha[i] = static_cast<float>(F.alpha[i]);
+    s->h_aabs[i] = static_cast<float>(std::fabs(F.alpha[i]));
+  }
+  for (int q = 0; q < nb; ++q)
+    for (int a = 0; a <= q; ++a)
+      for (int b = 0; b < 4; ++b)
+        for (int r = 0; r < 4; ++r) {
+          const int row = 4 * q + r, col = 4 * a + b;
+          float w = 0.f;
+          if (row < M && col < M && col <= row) w = static_cast<float>(F.Wl[static_cast<size_t>(row) * M + col]);
+          s->h_Wblk[(static_cast<size_t>(q) * (q + 1) / 2 + a) * 16 + b * 4 + r] = w;
+        }
+  DevGP& G = s->G;
+  G.M = M;
+  G.Mp = Mp;
+  G.DP = DP;
+  G.kernel = H.kernel;
+  G.sf2 = H.sf2;
+  G.sf2f = static_cast<float>(H.sf2);
+  G.b = F.b;
+  G.fstar = M > 0 ? F.fstar : INFINITY;
+  G.eps = 2.0 * (d + 8 + M) * std::ldexp(1.0, -24);
+  G.w_fro = F.w_fro;
+  if (s->device < 0) return AS_OK;
+  auto cp = [&](void* dst, const void* src, size_t bytes) -> as_status {
+    if (bytes) CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    return AS_OK;
+  };
+  as_status r;
+  if ((r = cp(s->d_O, s->h_O.data(), s->h_O.size() * 4)) != AS_OK) return r;
+  if ((r = cp(s->d_alpha, s->h_alpha.data(), s->h_alpha.size() * 4)) != AS_OK) return r;
+  if ((r = cp(s->d_aabs, s->h_aabs.data(), s->h_aabs.size() * 4)) != AS_OK) return r;
+  if ((r = cp(s->d_Wblk, s->h_Wblk.data(), s->h_Wblk.size() * 4)) != AS_OK) return r;
+  if ((r = cp(s->d_O64, s->h_O64.data(), s->h_O64.size() * 8)) != AS_OK) return r;
+  if ((r = cp(s->d_alpha64, s->h_alpha64.data(), s->h_alpha64.size() * 8)) != AS_OK) return r;
+  if ((r = cp(s->d_W64, s->h_W64.data(), s->h_W64.size() * 8)) != AS_OK) return r;
+  CUDA_TRY(cudaStreamSynchronize(st));  // staging vectors may be reused by the next observe()
+  G.O = s->d_O;
+  G.alpha = s->d_alpha;
+  G.aabs = s->d_aabs;
+  G.Wblk = s->d_Wblk;
+  G.O64 = s->d_O64;
+  G.alpha64 = s->d_alpha64;
+  G.W64 = s->d_W64;
+  return AS_OK;
+}
+
+as_status ensure_lists(as_space* s, int grid) {
+  const size_t need = static_cast<size_t>(grid) * s->KC;
+  if (need > s->lists_cap) {
+    if (s->d_lists) cudaFree(s->d_lists);
+    CUDA_TRY(cudaMalloc(&s->d_lists, need * sizeof(uint64_t)));
+    s->lists_cap = need;
+  }
+  if (grid > s->counts_cap) {
+    if (s->d_counts) cudaFree(s->d_counts);
+    if (s->d_drops) cudaFree(s->d_drops);
+    CUDA_TRY(cudaMalloc(&s->d_counts, grid * sizeof(int)));
+    CUDA_TRY(cudaMalloc(&s->d_drops, grid * sizeof(uint64_t)));
+    s->counts_cap = grid;
+  }
+  return AS_OK;
+}
+
+as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStream_t st) {
+  const bool gp = (a.acq != AS_ACQ_SIM) && s->G.M > 0;
+  const int P = next_pow2_h(s->KC + SCORE_THREADS);
+  const size_t smem = score_smem_bytes(gp ? s->G.Mp : 0, gp ? s->G.DP : 0, s->H.d, P);
+  if (smem > static_cast<size_t>(s->smem_optin))
+    return fail(AS_ERR_CAPACITY, "score kernel shared memory exceeds the per-CTA limit (M or k too large)");
+  const uint64_t ntiles = (a.count + SCORE_THREADS - 1) / SCORE_THREADS;
+  int grid = 0;
+  if (a.count > 0) {
+    int occ = 1;
+    if (gp) {
+      CUDA_TRY(cudaFuncSetAttribute(score_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, score_kernel<true>, SCORE_THREADS, smem));
+    } else {
+      CUDA_TRY(cudaFuncSetAttribute(score_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, score_kernel<false>, SCORE_THREADS, smem));
+    }
+    if (occ < 1) occ = 1;
+    const uint64_t g = std::min<uint64_t>(static_cast<uint64_t>(s->n_sm) * occ, ntiles);
+    grid = static_cast<int>(g);
+  }
+  as_status r = ensure_lists(s, std::max(grid, 1));
+  if (r != AS_OK) return r;
+  BatchArgs A{};
+  A.mode = a.mode;
+  A.acq = a.acq;
+  A.begin = a.begin;
+  A.count = a.count;
+  A.fk = feistel_make(s->H.n_cvi, a.seed);
+  A.kappa = a.kappa;
+  A.xi = a.xi;
+  A.d_scores = a.d_scores;
+  A.d_raw = a.d_raw;
+  A.d_valid_count = a.d_valid_count;
+  CtaOut out{s->d_lists, s->d_counts, s->d_drops, s->d_valid, s->KC, P};
+  DevGP G = s->G;
+  if (s->timing) CUDA_TRY(cudaEventRecord(s->ev[0], st));
+  if (grid > 0) {
+    if (gp) score_kernel<true><<<grid, SCORE_THREADS, smem, st>>>(s->D, G, A, out);
+    else score_kernel<false><<<grid, SCORE_THREADS, smem, st>>>(s->D, G, A, out);
+    CUDA_TRY(cudaGetLastError());
+    ++s->n_launches;
+  }
+  if (s->timing) CUDA_TRY(cudaEventRecord(s->ev[1], st));
+  const int P2 = next_pow2_h(s->KC + MERGE_THREADS);
+  CUDA_TRY(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P2 * 8));
+  merge_kernel<<<1, MERGE_THREADS, P2 * 8, st>>>(s->d_lists, s->d_counts, s->d_drops, grid, s->KC, s->d_pool,
+                                                 s->d_pool_n, s->d_cut, reset ? 1 : 0, P2);
+  CUDA_TRY(cudaGetLastError());
+  ++s->n_launches;
+  if (s->timing) {
+    CUDA_TRY(cudaEventRecord(s->ev[2], st));
+    s->ev_recorded = true;
+  }
+  return AS_OK;
+}
+
+// Refine the running pool in FP64 and bring it to the host, sorted (score desc, raw asc).
+as_status refine_pool(as_space* s, int acq, double kappa, double xi, cudaStream_t st, std::vector<Entry>& ent,
+                      uint64_t& cut, int& n_pool) {
+  const int blocks = (s->KC + REFINE_WARPS - 1) / REFINE_WARPS;
+  const size_t smem = static_cast<size_t>(REFINE_WARPS) * std::max(s->G.M, 1) * sizeof(double);
+  refine_kernel<<<blocks, REFINE_WARPS * 32, smem, st>>>(s->D, s->G, s->d_pool, s->d_pool_n, acq, kappa, xi,
+                                                         s->d_ref_score, s->d_ref_raw);
+  CUDA_TRY(cudaGetLastError());
+  ++s->n_launches;
+  std::vector<double> sc(s->KC);
+  std::vector<uint64_t> rw(s->KC);
+  CUDA_TRY(cudaMemcpyAsync(&n_pool, s->d_pool_n, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&cut, s->d_cut, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(sc.data(), s->d_ref_score, s->KC * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(rw.data(), s->d_ref_raw, s->KC * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  ent.clear();
+  for (int e = 0; e < n_pool; ++e)
+    if (std::isfinite(sc[e])) ent.push_back({sc[e], rw[e]});
+  std::sort(ent.begin(), ent.end(), entry_less);
+  return AS_OK;
+}
+
+as_status rescore_all(as_space* s, cudaStream_t st) {
+  for (size_t i = 0; i < s->batches.size(); ++i) {
+    as_score_args a = s->batches[i];
+    as_status r = launch_batch(s, a, i == 0, st);
+    if (r != AS_OK) return r;
+  }
+  return AS_OK;
+}
+
+// Certified refine: grow k' and re-score the recorded batches until the k-th refined score beats
+// the upper bound of every dropped candidate.
+as_status certified_pool(as_space* s, int k, cudaStream_t st, std::vector<Entry>& ent, double& cut_score,
+                         bool& certified) {
+  const as_score_args& a0 = s->batches.front();
+  for (;;) {
+    uint64_t cut;
+    int n_pool;
+    as_status r = refine_pool(s, a0.acq, a0.kappa, a0.xi, st, ent, cut, n_pool);
+    if (r != AS_OK) return r;
+    cut_score = (cut == KEY_NONE) ? -INFINITY : static_cast<double>(key_score(cut));
+    certified = (cut == KEY_NONE) ||
+                (static_cast<int>(ent.size()) >= k && ent[k - 1].score > cut_score);
+    if (certified || s->KC * 2 > s->KC_max) return AS_OK;
+    s->KC *= 2;
+    r = rescore_all(s, st);
+    if (r != AS_OK) return r;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* autoscout_last_error(void) { return g_err.c_str(); }
+
+as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as_space** out) {
+  if (!space_json || !out) return fail(AS_ERR_INVALID_ARG, "null argument");
+  *out = nullptr;
+  as_space* s = new as_space();
+  Status st = build_space(space_json, s->H);
+  if (!st.ok()) {
+    delete s;
+    return fail(static_cast<as_status>(st.code), st.msg);
+  }
+  s->device = cuda_device;
+  // GP fit with no observations (prior only)
+  gp_fit(s->H, {}, {}, {}, {}, s->fit);
+  s->G = DevGP{};
+  s->G.kernel = s->H.kernel;
+  s->G.sf2 = s->H.sf2;
+  s->G.sf2f = static_cast<float>(s->H.sf2);
+  s->G.fstar = INFINITY;
+  if (cuda_device >= 0) {
+    auto cleanup = [&](as_status r) {
+      autoscout_space_destroy(s);
+      return r;
+    };
+    cudaError_t e = cudaSetDevice(cuda_device);
+    if (e != cudaSuccess) return cleanup(fail(AS_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)));
+    if (cudaDeviceGetAttribute(&s->n_sm, cudaDevAttrMultiProcessorCount, cuda_device) != cudaSuccess ||
+        cudaDeviceGetAttribute(&s->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, cuda_device) != cudaSuccess)
+      return cleanup(fail(AS_ERR_CUDA, "device attribute query failed"));
+    s->smem_optin -= 256;  // static shared memory of the score kernel
+    const HostSpace& H = s->H;
+    DevSpace& D = s->D;
+    D.d = H.d;
+    D.n_prefix = H.n_prefix;
+    D.n_comp = static_cast<int>(H.comp_first.size());
+    D.n_struct = H.n_struct;
+    D.n_cvi = H.n_cvi;
+    D.n_raw = H.n_raw;
+    D.tail_span = H.tail_span;
+    for (int j = 0; j < DMAX; ++j) {
+      D.stride[j] = j < H.d ? H.stride[j] : 0;
+      D.nval[j] = j < H.d ? H.feat[j].n : 1;
+      D.comp_first[j] = j < D.n_comp ? H.comp_first[j] : 0;
+      D.comp_width[j] = j < D.n_comp ? H.comp_width[j] : 0;
+    }
+    D.sim = H.sim;
+    std::vector<uint2> oc(H.s_off.size());
+    for (size_t i = 0; i < oc.size(); ++i) oc[i] = make_uint2(H.s_off[i], H.s_cnt[i]);
+    as_status r;
+    uint64_t *p_prefix, *p_sraw;
+    uint32_t* p_sact;
+    DV* p_sdv;
+    uint2* p_oc;
+    Tuple* p_tu;
+    double *p_val, *p_xt64;
+    float* p_xt32;
+    if ((r = upload(&p_prefix, H.prefix, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = upload(&p_sraw, H.s_raw, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = upload(&p_sact, H.s_act, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = upload(&p_sdv, H.s_dv, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = upload(&p_oc, oc, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = upload(&p_tu, H.tuples, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = upload(&p_val, H.val, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = upload(&p_xt64, H.xt64, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = upload(&p_xt32, H.xt32, s->owned)) != AS_OK) return cleanup(r);
+    D.prefix = p_prefix;
+    D.s_raw = p_sraw;
+    D.s_act = p_sact;
+    D.s_dv = p_sdv;
+    D.s_oc = p_oc;
+    D.tuples = p_tu;
+    D.val = p_val;
+    D.xt64 = p_xt64;
+    D.xt32 = p_xt32;
+    // GP buffers at capacity
+    const int Mc = MMAX, DPc = ((H.d + 3) / 4) * 4, nbc = Mc / 4;
+    if ((r = dalloc(&s->d_O, static_cast<size_t>(Mc) * DPc, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = dalloc(&s->d_alpha, Mc, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = dalloc(&s->d_aabs, Mc, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = dalloc(&s->d_Wblk, static_cast<size_t>(16) * nbc * (nbc + 1) / 2, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = dalloc(&s->d_O64, static_cast<size_t>(Mc) * H.d, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = dalloc(&s->d_alpha64, Mc, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = dalloc(&s->d_W64, static_cast<size_t>(Mc) * Mc, s->owned)) != AS_OK) return cleanup(r);
+    // pool buffers at capacity
+    s->KC_max = KC_CAP;
+    if ((r = dalloc(&s->d_pool, KC_CAP, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = dalloc(&s->d_pool_n, 1, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = dalloc(&s->d_cut, 1, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = dalloc(&s->d_valid, 1, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = dalloc(&s->d_ref_score, KC_CAP, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = dalloc(&s->d_ref_raw, KC_CAP, s->owned)) != AS_OK) return cleanup(r);
+    e = cudaMemset(s->d_pool_n, 0, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(s->d_valid, 0, sizeof(uint64_t));
+    if (e != cudaSuccess) return cleanup(fail(AS_ERR_CUDA, cudaGetErrorString(e)));
+    for (int i = 0; i < 4; ++i)
+      if (cudaEventCreate(&s->ev[i]) != cudaSuccess) return cleanup(fail(AS_ERR_CUDA, "cudaEventCreate"));
+  }
+  *out = s;
+  return AS_OK;
+}
+
+void autoscout_space_destroy(as_space* s) {
+  if (!s) return;
+  if (s->device >= 0) {
+    cudaSetDevice(s->device);
+    for (void* p : s->owned) cudaFree(p);
+    if (s->d_lists) cudaFree(s->d_lists);
+    if (s->d_counts) cudaFree(s->d_counts);
+    if (s->d_drops) cudaFree(s->d_drops);
+    for (auto& e : s->ev)
+      if (e) cudaEventDestroy(e);
+  }
+  delete s;
+}
+
+as_status autoscout_space_info(const as_space* s, as_space_info* out) {
+  if (!s || !out) return fail(AS_ERR_INVALID_ARG, "null argument");
+  out->n_raw = s->H.n_raw;
+  out->n_cvi = s->H.n_cvi;
+  out->n_features = s->H.d;
+  out->n_structures = s->H.n_struct;
+  out->n_prefix = s->H.n_prefix;
+  out->n_components = static_cast<int32_t>(s->H.comp_first.size());
+  out->n_observed = s->fit.M;
+  out->max_observed = MMAX;
+  out->n_launches = s->n_launches;
+  return AS_OK;
+}
+
+as_status autoscout_observe(as_space* s, const uint64_t* raw_idx, const double* cost, int64_t n, void* cuda_stream) {
+  if (!s || n < 0 || (n > 0 && (!raw_idx || !cost))) return fail(AS_ERR_INVALID_ARG, "bad arguments");
+  if (static_cast<int64_t>(s->obs_raw.size()) + n > MMAX)
+    return fail(AS_ERR_CAPACITY, "more than " + std::to_string(MMAX) + " observed configurations");
+  std::vector<DV> ndv;
+  std::vector<uint32_t> nact;
+  std::vector<double> nsim;
+  for (int64_t i = 0; i < n; ++i) {
+    if (!(cost[i] > 0.0) || !std::isfinite(cost[i])) return fail(AS_ERR_INVALID_ARG, "observed cost must be finite and > 0");
+    int dig[DMAX];
+    DV dv;
+    uint32_t act;
+    bool structural;
+    if (!raw_decode(s->H, raw_idx[i], dig, dv, act, structural))
+      return fail(AS_ERR_INDEX_RANGE, "observed raw index >= n_raw");
+    double cs, mem;
+    bool ok;
+    simulate_host(s->H, dv, act, cs, ok, mem);
+    if (!structural || !ok) return fail(AS_ERR_INVALID_CONFIG, "observed configuration is not valid (raw " + std::to_string(raw_idx[i]) + ")");
+    ndv.push_back(dv);
+    nact.push_back(act);
+    nsim.push_back(cs);
+  }
+  std::vector<DV> all_dv = s->obs_dv;
+  std::vector<uint32_t> all_act = s->obs_act;
+  std::vector<double> all_cost = s->obs_cost, all_sim = s->obs_sim;
+  all_dv.insert(all_dv.end(), ndv.begin(), ndv.end());
+  all_act.insert(all_act.end(), nact.begin(), nact.end());
+  all_cost.insert(all_cost.end(), cost, cost + n);
+  all_sim.insert(all_sim.end(), nsim.begin(), nsim.end());
+  GPFit fit;
+  Status st = gp_fit(s->H, all_dv, all_act, all_cost, all_sim, fit);
+  if (!st.ok()) return fail(static_cast<as_status>(st.code), st.msg);
+  s->obs_raw.insert(s->obs_raw.end(), raw_idx, raw_idx + n);
+  s->obs_dv = std::move(all_dv);
+  s->obs_act = std::move(all_act);
+  s->obs_cost = std::move(all_cost);
+  s->obs_sim = std::move(all_sim);
+  s->fit = std::move(fit);
+  return upload_gp(s, static_cast<cudaStream_t>(cuda_stream));
+}
+
+as_status autoscout_observe_clear(as_space* s) {
+  if (!s) return fail(AS_ERR_INVALID_ARG, "null argument");
+  s->obs_raw.clear();
+  s->obs_dv.clear();
+  s->obs_act.clear();
+  s->obs_cost.clear();
+  s->obs_sim.clear();
+  gp_fit(s->H, {}, {}, {}, {}, s->fit);
+  return upload_gp(s, nullptr);
+}
+
+as_status autoscout_observe_info(const as_space* s, int32_t* m_out, double* b_out, double* fstar_out) {
+  if (!s) return fail(AS_ERR_INVALID_ARG, "null argument");
+  if (m_out) *m_out = s->fit.M;
+  if (b_out) *b_out = s->fit.b;
+  if (fstar_out) *fstar_out = s->fit.M > 0 ? s->fit.fstar : INFINITY;
+  return AS_OK;
+}
+
+as_status autoscout_score_batch(as_space* s, const as_score_args* a, void* cuda_stream) {
+  if (!s || !a) return fail(AS_ERR_INVALID_ARG, "null argument");
+  if (s->device < 0) return fail(AS_ERR_STATE, "host-only handle cannot score (no CUDA device)");
+  if (a->mode != AS_MODE_RANGE && a->mode != AS_MODE_SAMPLE) return fail(AS_ERR_INVALID_ARG, "bad mode");
+  if (a->acq < AS_ACQ_EI || a->acq > AS_ACQ_SIM) return fail(AS_ERR_INVALID_ARG, "bad acquisition");
+  if (a->k < 1 || a->k > 1024) return fail(AS_ERR_INVALID_ARG, "k must be in [1, 1024]");
+  if (a->begin > s->H.n_cvi || a->count > s->H.n_cvi - a->begin)
+    return fail(AS_ERR_INDEX_RANGE, "batch exceeds [0, n_cvi)");
+  if (a->acq == AS_ACQ_EI && s->G.M == 0) return fail(AS_ERR_NO_OBSERVATIONS, "EI needs at least one observation");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  CUDA_TRY(cudaSetDevice(s->device));
+  const bool reset = !a->accumulate || !s->scored;
+  if (reset) {
+    s->batches.clear();
+    s->KC = std::min(a->k + std::max(a->k, 64), s->KC_max);
+    CUDA_TRY(cudaMemsetAsync(s->d_valid, 0, sizeof(uint64_t), st));
+  }
+  as_score_args rec = *a;
+  rec.d_scores = nullptr;
+  rec.d_raw = nullptr;
+  rec.d_valid_count = nullptr;
+  s->batches.push_back(rec);
+  as_status r = launch_batch(s, *a, reset, st);
+  if (r != AS_OK) return r;
+  s->scored = true;
+  return AS_OK;
+}
+
+as_status autoscout_topk(as_space* s, int32_t k, uint64_t* raw_out, double* score_out, int32_t* n_out,
+                         void* cuda_stream) {
+  if (!s || !raw_out || !score_out || !n_out || k < 1) return fail(AS_ERR_INVALID_ARG, "bad arguments");
+  if (!s->scored || s->batches.empty()) return fail(AS_ERR_STATE, "nothing scored");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  CUDA_TRY(cudaSetDevice(s->device));
+  std::vector<Entry> ent;
+  double cut_score;
+  bool certified;
+  as_status r = certified_pool(s, k, st, ent, cut_score, certified);
+  if (r != AS_OK) return r;
+  const int n = std::min<int>(k, static_cast<int>(ent.size()));
+  for (int i = 0; i < n; ++i) {
+    raw_out[i] = ent[i].raw;
+    score_out[i] = ent[i].score;
+  }
+  *n_out = n;
+  if (!certified) return fail(AS_ERR_UNCERTIFIED, "top-k could not be certified at the maximum pool size");
+  return AS_OK;
+}
+
+as_status autoscout_topk_pool(as_space* s, int32_t k, void* pool_out, int32_t cap, int32_t* n_out, double* cut_out,
+                              void* cuda_stream) {
+  if (!s || !pool_out || !n_out || !cut_out || cap < 1 || k < 1) return fail(AS_ERR_INVALID_ARG, "bad arguments");
+  if (!s->scored || s->batches.empty()) return fail(AS_ERR_STATE, "nothing scored");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  CUDA_TRY(cudaSetDevice(s->device));
+  std::vector<Entry> ent;
+  double cut_score;
+  bool certified;
+  // locally certified pools make the global certificate cheap; it is re-checked in topk_merge
+  as_status r = certified_pool(s, k, st, ent, cut_score, certified);
+  if (r != AS_OK) return r;
+  // entries beyond `cap` are dropped: their scores raise the cut
+  const int n = std::min<int>(cap, static_cast<int>(ent.size()));
+  double cut = cut_score;
+  if (static_cast<int>(ent.size()) > cap) cut = std::max(cut, ent[cap].score);
+  std::memcpy(pool_out, ent.data(), static_cast<size_t>(n) * sizeof(Entry));
+  *n_out = n;
+  *cut_out = cut;
+  return AS_OK;
+}
+
+as_status autoscout_topk_merge(const as_space* s, const void* pools, const int32_t* counts, const double* cuts,
+                               int32_t n_pools, int32_t cap, int32_t k, uint64_t* raw_out, double* score_out,
+                               int32_t* n_out, int32_t* certified_out) {
+  (void)s;
+  if (!pools || !counts || !cuts || n_pools < 1 || cap < 1 || k < 1 || !raw_out || !score_out || !n_out)
+    return fail(AS_ERR_INVALID_ARG, "bad arguments");
+  const Entry* P = static_cast<const Entry*>(pools);
+  std::vector<Entry> all;
+  double cut = -INFINITY;
+  for (int p = 0; p < n_pools; ++p) {
+    if (counts[p] < 0 || counts[p] > cap) return fail(AS_ERR_INVALID_ARG, "pool count out of range");
+    for (int i = 0; i < counts[p]; ++i) all.push_back(P[static_cast<size_t>(p) * cap + i]);
+    cut = std::max(cut, cuts[p]);
+  }
+  std::sort(all.begin(), all.end(), entry_less);
+  all.erase(std::unique(all.begin(), all.end(), [](const Entry& a, const Entry& b) { return a.raw == b.raw; }),
+            all.end());
+  const int n = std::min<int>(k, static_cast<int>(all.size()));
+  for (int i = 0; i < n; ++i) {
+    raw_out[i] = all[i].raw;
+    score_out[i] = all[i].score;
+  }
+  *n_out = n;
+  const bool cert = (cut == -INFINITY) || (static_cast<int>(all.size()) >= k && all[k - 1].score > cut);
+  if (certified_out) *certified_out = cert ? 1 : 0;
+  return cert ? AS_OK : fail(AS_ERR_UNCERTIFIED, "merged top-k could not be certified");
+}
+
+as_status autoscout_decode(const as_space* s, uint64_t raw, int32_t* digits_out, int32_t* valid_out) {
+  if (!s) return fail(AS_ERR_INVALID_ARG, "null argument");
+  int dig[DMAX];
+  DV dv;
+  uint32_t act;
+  bool structural;
+  if (!raw_decode(s->H, raw, dig, dv, act, structural)) return fail(AS_ERR_INDEX_RANGE, "raw >= n_raw");
+  if (digits_out)
+    for (int j = 0; j < s->H.d; ++j) digits_out[j] = dig[j];
+  if (valid_out) {
+    double c, m;
+    bool ok = false;
+    if (structural) simulate_host(s->H, dv, act, c, ok, m);
+    *valid_out = (structural && ok) ? 1 : 0;
+  }
+  return AS_OK;
+}
+
+as_status autoscout_cvi_to_raw(const as_space* s, uint64_t cvi, uint64_t* raw_out) {
+  if (!s || !raw_out) return fail(AS_ERR_INVALID_ARG, "null argument");
+  DV dv;
+  uint32_t act;
+  if (!cvi_decode(s->H, cvi, dv, act, *raw_out)) return fail(AS_ERR_INDEX_RANGE, "cvi >= n_cvi");
+  return AS_OK;
+}
+
+as_status autoscout_sample_to_cvi(const as_space* s, uint64_t seed, uint64_t ordinal, uint64_t* cvi_out) {
+  if (!s || !cvi_out) return fail(AS_ERR_INVALID_ARG, "null argument");
+  if (ordinal >= s->H.n_cvi) return fail(AS_ERR_INDEX_RANGE, "ordinal >= n_cvi");
+  *cvi_out = feistel_pi(feistel_make(s->H.n_cvi, seed), ordinal);
+  return AS_OK;
+}
+
+as_status autoscout_simulate(const as_space* s, uint64_t raw, double* cost_out, double* mem_out, int32_t* ok_out) {
+  if (!s) return fail(AS_ERR_INVALID_ARG, "null argument");
+  int dig[DMAX];
+  DV dv;
+  uint32_t act;
+  bool structural;
+  if (!raw_decode(s->H, raw, dig, dv, act, structural)) return fail(AS_ERR_INDEX_RANGE, "raw >= n_raw");
+  double c, m;
+  bool ok;
+  simulate_host(s->H, dv, act, c, ok, m);
+  if (cost_out) *cost_out = c;
+  if (mem_out) *mem_out = m;
+  if (ok_out) *ok_out = (ok && structural) ? 1 : 0;
+  return AS_OK;
+}
+
+as_status autoscout_mask_range(as_space* s, uint64_t raw_begin, uint64_t count, uint32_t* d_bits,
+                               uint64_t* d_valid_count, void* cuda_stream) {
+  if (!s || (count > 0 && !d_bits)) return fail(AS_ERR_INVALID_ARG, "bad arguments");
+  if (s->device < 0) return fail(AS_ERR_STATE, "host-only handle");
+  if (raw_begin > s->H.n_raw || count > s->H.n_raw - raw_begin) return fail(AS_ERR_INDEX_RANGE, "range exceeds n_raw");
+  if (count == 0) return AS_OK;
+  CUDA_TRY(cudaSetDevice(s->device));
+  const int threads = 256;
+  const uint64_t blocks = (count + threads - 1) / threads;
+  if (blocks > 0x7FFFFFFFull) return fail(AS_ERR_INVALID_ARG, "range too large for one launch");
+  mask_kernel<<<static_cast<unsigned>(blocks), threads, 0, static_cast<cudaStream_t>(cuda_stream)>>>(
+      s->D, raw_begin, count, d_bits, d_valid_count);
+  CUDA_TRY(cudaGetLastError());
+  ++s->n_launches;
+  return AS_OK;
+}
+
+as_status autoscout_set_timing(as_space* s, int32_t enable) {
+  if (!s) return fail(AS_ERR_INVALID_ARG, "null argument");
+  s->timing = enable != 0 && s->device >= 0;
+  s->ev_recorded = false;
+  return AS_OK;
+}
+
+as_status autoscout_last_kernel_ms(as_space* s, double* score_ms, double* merge_ms) {
+  if (!s || !s->ev_recorded) return fail(AS_ERR_STATE, "no timed launch recorded");
+  float a = 0, b = 0;
+  CUDA_TRY(cudaEventSynchronize(s->ev[2]));
+  CUDA_TRY(cudaEventElapsedTime(&a, s->ev[0], s->ev[1]));
+  CUDA_TRY(cudaEventElapsedTime(&b, s->ev[1], s->ev[2]));
+  if (score_ms) *score_ms = a;
+  if (merge_ms) *merge_ms = b;
+  return AS_OK;
+}
+
+}  // extern "C"

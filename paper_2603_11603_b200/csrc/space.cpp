@@ -1,0 +1,741 @@
+// Host-side space compiler: JSON -> validated feature/constraint model -> CVI structure tables.
+// Compiled with -ffp-contract=off so the host FP64 resource check is bit-identical to the
+// oracle's numpy evaluation and to the device's __dmul_rn/__dadd_rn path (R7).
+#include "space.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <numeric>
+#include <set>
+
+#include "json.hpp"
+
+namespace as {
+
+namespace {
+
+enum { E_ARG = 1, E_SCHEMA = 2, E_CYCLE = 3, E_ORDER = 4, E_EMPTY = 5, E_CAP = 10, E_NUM = 9 };
+
+Status err(int code, const std::string& m) { return Status{code, m}; }
+
+bool cmp_num(double a, const std::string& op, double b) {
+  if (op == ">") return a > b;
+  if (op == ">=") return a >= b;
+  if (op == "==") return a == b;
+  if (op == "!=") return a != b;
+  if (op == "<") return a < b;
+  if (op == "<=") return a <= b;
+  return false;
+}
+
+bool valid_op(const std::string& op) {
+  return op == ">" || op == ">=" || op == "==" || op == "!=" || op == "<" || op == "<=";
+}
+
+// Build the allowed-digit mask of an atomic comparison "ref <op> value".
+Status make_atom(const HostSpace& S, int ref, const std::string& op, const asj::Value& v, Atom& out) {
+  const FeatureH& r = S.feat[ref];
+  if (!valid_op(op)) return err(E_SCHEMA, "bad comparison operator '" + op + "'");
+  out.ref = ref;
+  out.allowed = 0;
+  for (int k = 0; k < r.n; ++k) {
+    bool hold;
+    if (r.vkind == 2 || v.kind == asj::Value::String) {
+      if (r.vkind != 2 || v.kind != asj::Value::String || (op != "==" && op != "!="))
+        return err(E_SCHEMA, "categorical comparison must be ==/!= between strings (" + r.name + ")");
+      hold = (op == "==") == (r.str[k] == v.str);
+    } else {
+      double b;
+      if (v.kind == asj::Value::Bool) b = v.b ? 1.0 : 0.0;
+      else if (v.kind == asj::Value::Number) b = v.num;
+      else return err(E_SCHEMA, "predicate value must be a number, bool or string");
+      hold = cmp_num(r.num[k], op, b);
+    }
+    if (hold) out.allowed |= (1ull << k);
+  }
+  return Status{};
+}
+
+const asj::Value* need(const asj::Value& o, const char* k) { return o.get(k); }
+
+int feature_index(const HostSpace& S, const std::string& n) {
+  for (int i = 0; i < S.d; ++i)
+    if (S.feat[i].name == n) return i;
+  return -1;
+}
+
+double model_const(const asj::Value* model, const std::string& k, double dflt, bool* found = nullptr) {
+  const asj::Value* v = model ? model->get(k) : nullptr;
+  if (found) *found = (v && v->kind == asj::Value::Number);
+  if (!v || v->kind != asj::Value::Number) return dflt;
+  return v->num;
+}
+
+}  // namespace
+
+void activity(const HostSpace& S, const int* dig, bool* act) {
+  for (int j = 0; j < S.d; ++j) {
+    bool a = true;
+    for (const Atom& at : S.feat[j].req) {
+      if (!act[at.ref] || !((at.allowed >> dig[at.ref]) & 1ull)) { a = false; break; }
+    }
+    act[j] = a;
+  }
+}
+
+static double eff_value(const HostSpace& S, int f, const int* dig, const bool* act) {
+  const FeatureH& F = S.feat[f];
+  return F.num[act[f] ? dig[f] : F.dflt];
+}
+
+static bool atom_holds(const Atom& a, const int* dig, const bool* act) {
+  return act[a.ref] && ((a.allowed >> dig[a.ref]) & 1ull);
+}
+
+// One structural constraint on effective values (R5; same semantics as the oracle).
+static bool constraint_ok(const HostSpace& S, const ConstraintH& c, const int* dig, const bool* act) {
+  auto ev = [&](int f) { return eff_value(S, f, dig, act); };
+  auto prod = [&](const std::vector<int>& fs) {
+    double p = 1.0;
+    for (int f : fs) p *= ev(f);
+    return p;
+  };
+  auto imod = [](double a, double b) { return std::fmod(a, b) == 0.0; };
+  switch (c.type) {
+    case C_PROD_EQ_DEV: return prod(c.f) == S.G;
+    case C_PROD_LE_DEV_POW2: {
+      double w = prod(c.f);
+      uint64_t wi = static_cast<uint64_t>(w);
+      bool ok = w <= S.G && (wi & (wi - 1)) == 0;
+      if (c.divides_devices) ok = ok && imod(S.G, w);
+      return ok;
+    }
+    case C_DIVIDES: return imod(ev(c.b), ev(c.a));
+    case C_DIVIDES_CONST: return imod(c.cval, prod(c.f));
+    case C_GBS_DIV: return imod(c.cval, prod(c.f));
+    case C_SEQ_2CP: {
+      double cp = ev(c.a);
+      return cp == 1.0 || imod(c.cval, 2.0 * cp);
+    }
+    case C_GE:
+      if (!(act[c.a] && act[c.b])) return true;
+      return ev(c.a) >= ev(c.b);
+    case C_LE_CONST_DIV:
+      if (!act[c.a]) return true;
+      return ev(c.a) * prod(c.f) <= c.cval;
+    case C_MB_DIV_PP: {  // f = {vpp, pp, dp, mbs}; cval = GBS
+      if (ev(c.f[0]) <= 1.0) return true;
+      double m = std::floor(c.cval / (ev(c.f[2]) * ev(c.f[3])));
+      return imod(m, ev(c.f[1]));
+    }
+    case C_IMPLIES: {
+      bool cond = true;
+      for (const Atom& a : c.iff) cond = cond && atom_holds(a, dig, act);
+      if (!cond) return true;
+      for (const Atom& a : c.then)
+        if (!atom_holds(a, dig, act)) return false;
+      return true;
+    }
+  }
+  return false;
+}
+
+static void dv_from_digits(const HostSpace& S, const int* dig, DV& dv) {
+  dv.w[0] = dv.w[1] = dv.w[2] = 0;
+  for (int j = 0; j < S.d; ++j) dv_set(dv, j, static_cast<uint32_t>(dig[j]));
+}
+
+static uint32_t act_bits(const HostSpace& S, const bool* act) {
+  uint32_t b = 0;
+  for (int j = 0; j < S.d; ++j)
+    if (act[j]) b |= (1u << j);
+  return b;
+}
+
+Status build_space(const char* json, HostSpace& S) {
+  asj::Value doc;
+  try {
+    doc = asj::parse(json);
+  } catch (const std::exception& e) {
+    return err(E_SCHEMA, std::string("JSON: ") + e.what());
+  }
+  if (doc.kind != asj::Value::Object) return err(E_SCHEMA, "space document must be a JSON object");
+  if (const asj::Value* n = doc.get("name"); n && n->kind == asj::Value::String) S.name = n->str;
+
+  // ---------------------------------------------------------------- features
+  const asj::Value* fs = doc.get("features");
+  if (!fs || fs->kind != asj::Value::Array || fs->arr.empty())
+    return err(E_SCHEMA, "space must declare at least one feature (SPEC.md:61)");
+  S.d = static_cast<int>(fs->arr.size());
+  if (S.d > DMAX) return err(E_CAP, "more than 24 features");
+  S.feat.resize(S.d);
+  std::map<std::string, int> idx;
+  for (int i = 0; i < S.d; ++i) {
+    const asj::Value& f = fs->arr[i];
+    const asj::Value* nm = f.get("name");
+    if (f.kind != asj::Value::Object || !nm || nm->kind != asj::Value::String)
+      return err(E_SCHEMA, "feature needs a string name");
+    if (idx.count(nm->str)) return err(E_SCHEMA, "duplicate feature name " + nm->str);
+    idx[nm->str] = i;
+    S.feat[i].name = nm->str;
+  }
+  // cycle detection over activation references
+  {
+    std::vector<std::vector<int>> g(S.d);
+    for (int i = 0; i < S.d; ++i) {
+      const asj::Value* rq = fs->arr[i].get("requires");
+      if (!rq) continue;
+      if (rq->kind != asj::Value::Array) return err(E_SCHEMA, "requires must be an array");
+      for (const asj::Value& a : rq->arr) {
+        const asj::Value* rf = a.get("feature");
+        if (!rf || rf->kind != asj::Value::String || !idx.count(rf->str))
+          return err(E_SCHEMA, "feature " + S.feat[i].name + " requires an unknown feature");
+        g[i].push_back(idx[rf->str]);
+      }
+    }
+    std::vector<int> st(S.d, 0);
+    std::function<bool(int)> dfs = [&](int u) {
+      st[u] = 1;
+      for (int v : g[u]) {
+        if (st[v] == 1) return false;
+        if (st[v] == 0 && !dfs(v)) return false;
+      }
+      st[u] = 2;
+      return true;
+    };
+    for (int u = 0; u < S.d; ++u)
+      if (st[u] == 0 && !dfs(u)) return err(E_CYCLE, "cyclic activation dependency (SPEC.md:62)");
+  }
+  for (int i = 0; i < S.d; ++i) {
+    const asj::Value& f = fs->arr[i];
+    FeatureH& F = S.feat[i];
+    const asj::Value* kind = f.get("kind");
+    if (!kind || kind->kind != asj::Value::String || (kind->str != "sparse" && kind->str != "dense"))
+      return err(E_SCHEMA, "feature " + F.name + ": kind must be sparse|dense");
+    const asj::Value* dom = f.get("domain");
+    if (!dom || dom->kind != asj::Value::Array) return err(E_SCHEMA, "feature " + F.name + ": domain must be an array");
+    if (dom->arr.empty()) return err(E_EMPTY, "feature " + F.name + " has an empty domain (SPEC.md:58)");
+    F.n = static_cast<int>(dom->arr.size());
+    if (F.n > VMAX) return err(E_CAP, "feature " + F.name + ": domain larger than 64");
+    const asj::Value::Kind k0 = dom->arr[0].kind;
+    F.vkind = k0 == asj::Value::Number ? 0 : (k0 == asj::Value::Bool ? 1 : 2);
+    if (k0 != asj::Value::Number && k0 != asj::Value::Bool && k0 != asj::Value::String)
+      return err(E_SCHEMA, "feature " + F.name + ": domain values must be numbers, bools or strings");
+    for (int k = 0; k < F.n; ++k) {
+      const asj::Value& v = dom->arr[k];
+      if (v.kind != k0) return err(E_SCHEMA, "feature " + F.name + ": mixed domain types");
+      F.num.push_back(v.kind == asj::Value::Number ? v.num : (v.kind == asj::Value::Bool ? (v.b ? 1.0 : 0.0) : double(k)));
+      F.str.push_back(v.kind == asj::Value::String ? v.str : std::string());
+    }
+    F.dflt = 0;
+    if (const asj::Value* dv = f.get("default")) {
+      int found = -1;
+      for (int k = 0; k < F.n && found < 0; ++k) {
+        const asj::Value& v = dom->arr[k];
+        if (v.kind != dv->kind) continue;
+        if ((v.kind == asj::Value::Number && v.num == dv->num) || (v.kind == asj::Value::Bool && v.b == dv->b) ||
+            (v.kind == asj::Value::String && v.str == dv->str))
+          found = k;
+      }
+      if (found < 0) return err(E_SCHEMA, "feature " + F.name + ": default not in domain (SPEC.md:30)");
+      F.dflt = found;
+    }
+    if (const asj::Value* rq = f.get("requires")) {
+      for (const asj::Value& a : rq->arr) {
+        int ref = idx[a.get("feature")->str];
+        if (ref >= i) return err(E_ORDER, "feature " + F.name + " requires a later feature (SPEC.md:30)");
+        const asj::Value* op = a.get("op");
+        const asj::Value* val = a.get("value");
+        if (!op || op->kind != asj::Value::String || !val) return err(E_SCHEMA, "requires atom needs op and value");
+        Atom at;
+        Status st = make_atom(S, ref, op->str, *val, at);
+        if (!st.ok()) return st;
+        F.req.push_back(at);
+      }
+    }
+  }
+  // raw mixed radix
+  S.stride[S.d - 1] = 1;
+  for (int j = S.d - 2; j >= 0; --j) {
+    unsigned __int128 s = static_cast<unsigned __int128>(S.stride[j + 1]) * S.feat[j + 1].n;
+    if (s > (static_cast<unsigned __int128>(1) << 63)) return err(E_SCHEMA, "raw index range exceeds 2^63");
+    S.stride[j] = static_cast<uint64_t>(s);
+  }
+  {
+    unsigned __int128 nr = static_cast<unsigned __int128>(S.stride[0]) * S.feat[0].n;
+    if (nr > (static_cast<unsigned __int128>(1) << 63)) return err(E_SCHEMA, "raw index range exceeds 2^63");
+    S.n_raw = static_cast<uint64_t>(nr);
+  }
+
+  // ---------------------------------------------------------------- hardware / model
+  const asj::Value* hw = doc.get("hardware");
+  const asj::Value* model = doc.get("model");
+  if (!hw || hw->kind != asj::Value::Object) return err(E_SCHEMA, "missing hardware object");
+  const asj::Value* devs = hw->get("devices");
+  if (!devs || devs->kind != asj::Value::Array || devs->arr.empty()) return err(E_SCHEMA, "hardware.devices must be a non-empty array");
+  struct Cls { int count; double cap, eff; };
+  std::vector<Cls> cls;
+  S.G = 0;
+  for (const asj::Value& c : devs->arr) {
+    const asj::Value *cnt = c.get("count"), *mem = c.get("mem_gb"), *rel = c.get("rel_throughput");
+    if (!cnt || !mem || !rel) return err(E_SCHEMA, "device class needs count, mem_gb, rel_throughput");
+    cls.push_back({static_cast<int>(cnt->num), mem->num * 1e9, rel->num});
+    S.G += cnt->num;
+  }
+  if (cls.size() > static_cast<size_t>(MAX_CLS)) return err(E_CAP, "more than 4 device classes");
+  std::stable_sort(cls.begin(), cls.end(), [](const Cls& a, const Cls& b) { return a.eff > b.eff; });
+
+  // ---------------------------------------------------------------- constraints
+  std::vector<int> cref;  // features referenced by constraints
+  if (const asj::Value* cs = doc.get("constraints")) {
+    for (const asj::Value& c : cs->arr) {
+      const asj::Value* t = c.get("type");
+      if (!t || t->kind != asj::Value::String) return err(E_SCHEMA, "constraint needs a type");
+      ConstraintH C;
+      auto fidx = [&](const asj::Value* v, int& out) -> Status {
+        if (!v || v->kind != asj::Value::String || feature_index(S, v->str) < 0)
+          return err(E_SCHEMA, "constraint references an unknown feature");
+        out = feature_index(S, v->str);
+        return Status{};
+      };
+      auto flist = [&](const asj::Value* v) -> Status {
+        if (!v || v->kind != asj::Value::Array) return err(E_SCHEMA, "constraint features must be an array");
+        for (const asj::Value& x : v->arr) {
+          int i;
+          Status st = fidx(&x, i);
+          if (!st.ok()) return st;
+          C.f.push_back(i);
+        }
+        return Status{};
+      };
+      auto cst = [&](const asj::Value* v, double& out) -> Status {
+        if (!v || v->kind != asj::Value::String) return err(E_SCHEMA, "constraint const must be a name");
+        if (v->str == "G") { out = S.G; return Status{}; }
+        bool found;
+        out = model_const(model, v->str, 0, &found);
+        if (!found) return err(E_SCHEMA, "unknown model constant " + v->str);
+        return Status{};
+      };
+      auto atoms = [&](const asj::Value* v, std::vector<Atom>& out) -> Status {
+        if (!v || v->kind != asj::Value::Array) return err(E_SCHEMA, "implies needs atom arrays");
+        for (const asj::Value& a : v->arr) {
+          int r;
+          Status st = fidx(a.get("feature"), r);
+          if (!st.ok()) return st;
+          const asj::Value* op = a.get("op");
+          const asj::Value* val = a.get("value");
+          if (!op || !val) return err(E_SCHEMA, "atom needs op and value");
+          Atom at;
+          st = make_atom(S, r, op->str, *val, at);
+          if (!st.ok()) return st;
+          out.push_back(at);
+        }
+        return Status{};
+      };
+      Status st;
+      const std::string& ty = t->str;
+      if (ty == "product_eq_devices") { C.type = C_PROD_EQ_DEV; st = flist(c.get("features")); }
+      else if (ty == "product_le_devices_pow2") {
+        C.type = C_PROD_LE_DEV_POW2; st = flist(c.get("features"));
+        if (const asj::Value* dd = c.get("divides_devices")) C.divides_devices = dd->kind == asj::Value::Bool && dd->b;
+      } else if (ty == "divides") {
+        C.type = C_DIVIDES; st = fidx(c.get("a"), C.a);
+        if (st.ok()) st = fidx(c.get("b"), C.b);
+      } else if (ty == "divides_const") { C.type = C_DIVIDES_CONST; st = flist(c.get("features")); if (st.ok()) st = cst(c.get("const"), C.cval); }
+      else if (ty == "gbs_divisible") {
+        C.type = C_GBS_DIV; st = flist(c.get("features"));
+        bool f; C.cval = model_const(model, "GBS", 0, &f);
+        if (st.ok() && !f) st = err(E_SCHEMA, "gbs_divisible needs model.GBS");
+      } else if (ty == "seq_divisible_2cp") {
+        C.type = C_SEQ_2CP; st = fidx(c.get("feature"), C.a);
+        bool f; C.cval = model_const(model, "S", 0, &f);
+        if (st.ok() && !f) st = err(E_SCHEMA, "seq_divisible_2cp needs model.S");
+      } else if (ty == "ge") {
+        C.type = C_GE; st = fidx(c.get("a"), C.a);
+        if (st.ok()) st = fidx(c.get("b"), C.b);
+      } else if (ty == "le_const_div") {
+        C.type = C_LE_CONST_DIV; st = fidx(c.get("feature"), C.a);
+        if (st.ok()) st = flist(c.get("div"));
+        if (st.ok()) st = cst(c.get("const"), C.cval);
+      } else if (ty == "microbatch_divisible_pp") {
+        C.type = C_MB_DIV_PP;
+        for (const char* k : {"vpp", "pp", "dp", "mbs"}) {
+          int i;
+          if (st.ok()) st = fidx(c.get(k), i);
+          if (st.ok()) C.f.push_back(i);
+        }
+        bool f; C.cval = model_const(model, "GBS", 0, &f);
+        if (st.ok() && !f) st = err(E_SCHEMA, "microbatch_divisible_pp needs model.GBS");
+      } else if (ty == "implies") {
+        C.type = C_IMPLIES; st = atoms(c.get("if"), C.iff);
+        if (st.ok()) st = atoms(c.get("then"), C.then);
+      } else {
+        return err(E_SCHEMA, "unknown constraint type " + ty);
+      }
+      if (!st.ok()) return st;
+      std::vector<int> refs = C.f;
+      if (C.a >= 0) refs.push_back(C.a);
+      if (C.b >= 0) refs.push_back(C.b);
+      for (const Atom& a : C.iff) refs.push_back(a.ref);
+      for (const Atom& a : C.then) refs.push_back(a.ref);
+      C.last = refs.empty() ? 0 : *std::max_element(refs.begin(), refs.end());
+      cref.insert(cref.end(), refs.begin(), refs.end());
+      S.cons.push_back(C);
+    }
+  }
+
+  // ---------------------------------------------------------------- structural prefix (R4)
+  // smallest declaration-order prefix holding every constraint-referenced feature and, transitively,
+  // every feature its activation predicates reference.
+  {
+    std::vector<bool> need(S.d, false);
+    std::vector<int> stack(cref.begin(), cref.end());
+    while (!stack.empty()) {
+      int f = stack.back();
+      stack.pop_back();
+      if (need[f]) continue;
+      need[f] = true;
+      for (const Atom& a : S.feat[f].req) stack.push_back(a.ref);
+    }
+    S.n_prefix = 0;
+    for (int j = 0; j < S.d; ++j)
+      if (need[j]) S.n_prefix = j + 1;
+  }
+  // tail gating groups: connected components of gate edges among tail features; each must be a
+  // contiguous run of features so the CVI order stays the raw order.
+  {
+    std::vector<int> par(S.d);
+    std::iota(par.begin(), par.end(), 0);
+    std::function<int(int)> find = [&](int x) { return par[x] == x ? x : par[x] = find(par[x]); };
+    for (int j = S.n_prefix; j < S.d; ++j)
+      for (const Atom& a : S.feat[j].req)
+        if (a.ref >= S.n_prefix) par[find(j)] = find(a.ref);
+    int j = S.n_prefix;
+    while (j < S.d) {
+      int r = find(j), e = j;
+      while (e + 1 < S.d && find(e + 1) == r) ++e;
+      for (int q = e + 1; q < S.d; ++q)
+        if (find(q) == r) return err(E_ORDER, "tail gating group of " + S.feat[j].name + " is not contiguous");
+      if (e - j + 1 > TUPW) return err(E_CAP, "tail gating group wider than 8 features");
+      S.comp_first.push_back(j);
+      S.comp_width.push_back(e - j + 1);
+      j = e + 1;
+    }
+  }
+  const int n_comp = static_cast<int>(S.comp_first.size());
+  S.tail_span = S.n_prefix > 0 ? S.stride[S.n_prefix - 1] : S.n_raw;
+
+  // ---------------------------------------------------------------- enumerate structures
+  {
+    int dig[DMAX] = {0};
+    bool act[DMAX] = {false};
+    std::map<std::vector<uint64_t>, uint32_t> list_cache;
+    uint64_t acc = 0;
+    Status failure;
+    std::function<void(int)> rec_prefix;
+    std::function<void(int, int, int, std::vector<Tuple>&)> rec_comp;
+    rec_comp = [&](int c, int j, int end, std::vector<Tuple>& out) {
+      if (j == end) {
+        Tuple t{};
+        for (int q = S.comp_first[c]; q < end; ++q) {
+          dv_set(t.dv, q, static_cast<uint32_t>(dig[q]));
+          t.raw += static_cast<uint64_t>(dig[q]) * S.stride[q];
+          if (act[q]) t.act |= (1u << q);
+        }
+        out.push_back(t);
+        return;
+      }
+      const FeatureH& F = S.feat[j];
+      for (int v = 0; v < F.n; ++v) {
+        dig[j] = v;
+        bool a = true;
+        for (const Atom& at : F.req)
+          if (!act[at.ref] || !((at.allowed >> dig[at.ref]) & 1ull)) { a = false; break; }
+        act[j] = a;
+        if (!a && v != F.dflt) continue;  // G1
+        rec_comp(c, j + 1, end, out);
+      }
+      dig[j] = S.feat[j].dflt;
+    };
+    rec_prefix = [&](int j) {
+      if (!failure.ok()) return;
+      if (j == S.n_prefix) {
+        DV dv{};
+        uint64_t raw = 0;
+        for (int q = 0; q < S.n_prefix; ++q) {
+          dv_set(dv, q, static_cast<uint32_t>(dig[q]));
+          raw += static_cast<uint64_t>(dig[q]) * S.stride[q];
+        }
+        uint32_t ab = 0;
+        for (int q = 0; q < S.n_prefix; ++q)
+          if (act[q]) ab |= (1u << q);
+        uint64_t tail = 1;
+        for (int c = 0; c < n_comp; ++c) {
+          std::vector<Tuple> lst;
+          rec_comp(c, S.comp_first[c], S.comp_first[c] + S.comp_width[c], lst);
+          std::vector<uint64_t> key;
+          for (const Tuple& t : lst) { key.push_back(t.raw); key.push_back(t.act); }
+          auto it = list_cache.find(key);
+          uint32_t off;
+          if (it == list_cache.end()) {
+            off = static_cast<uint32_t>(S.tuples.size());
+            S.tuples.insert(S.tuples.end(), lst.begin(), lst.end());
+            list_cache[key] = off;
+          } else {
+            off = it->second;
+          }
+          S.s_off.push_back(off);
+          S.s_cnt.push_back(static_cast<uint32_t>(lst.size()));
+          tail *= lst.size();
+        }
+        if (tail >= (1ull << 32)) { failure = err(E_CAP, "a structure has >= 2^32 valid tails"); return; }
+        S.prefix.push_back(acc);
+        S.s_raw.push_back(raw);
+        S.s_act.push_back(ab);
+        S.s_dv.push_back(dv);
+        acc += tail;
+        return;
+      }
+      const FeatureH& F = S.feat[j];
+      for (int v = 0; v < F.n; ++v) {
+        dig[j] = v;
+        bool a = true;
+        for (const Atom& at : F.req)
+          if (!act[at.ref] || !((at.allowed >> dig[at.ref]) & 1ull)) { a = false; break; }
+        act[j] = a;
+        if (!a && v != F.dflt) continue;  // G1
+        bool ok = true;
+        for (const ConstraintH& c : S.cons)
+          if (c.last == j && !constraint_ok(S, c, dig, act)) { ok = false; break; }
+        if (!ok) continue;
+        rec_prefix(j + 1);
+      }
+      dig[j] = 0;
+    };
+    rec_prefix(0);
+    if (!failure.ok()) return failure;
+    S.n_struct = static_cast<int>(S.s_raw.size());
+    S.prefix.push_back(acc);
+    S.n_cvi = acc;
+    if (S.n_cvi == 0) return err(E_EMPTY, "no configuration satisfies the constraints (SPEC.md:34)");
+    if (S.n_cvi >= (1ull << 32)) return err(E_CAP, "n_cvi >= 2^32");
+  }
+
+  // ---------------------------------------------------------------- simulator binding
+  const asj::Value* sm = doc.get("sim_mode");
+  std::string mode = (sm && sm->kind == asj::Value::String) ? sm->str : "spec";
+  SimParams& P = S.sim;
+  P.mode = mode == "spec" ? 0 : (mode == "derived" ? 1 : (mode == "serve" ? 2 : -1));
+  if (P.mode < 0) return err(E_SCHEMA, "sim_mode must be spec|derived|serve");
+  static const char* train_names[NKNOB] = {"pp", "vpp", "tp", "dp", "cp", "ep", "mbs", "ar", "arl", "sp", "tpov",
+                                           "tp_comm", "dopt", "ovg", "ovp", "ddp_bucket", "ddp", "disp",
+                                           nullptr, nullptr, nullptr, nullptr};
+  static const double neutral[NKNOB] = {1, 1, 1, 1, 1, 1, 1, 0, 1, 0, 0, 0, 0, 0, 0, 4, 1, 0, 1, 0, 1, 0.9};
+  for (int k = 0; k < NKNOB; ++k) {
+    P.neutral[k] = neutral[k];
+    P.kf[k] = -1;
+    const char* nm = nullptr;
+    if (P.mode != 2) nm = train_names[k];
+    else if (k == K_TP) nm = "tp";
+    else if (k == K_NS) nm = "max_num_seqs";
+    else if (k == K_CPF) nm = "cpf";
+    else if (k == K_MBT) nm = "mbt";
+    else if (k == K_U) nm = "u";
+    if (nm) P.kf[k] = feature_index(S, nm);
+  }
+  S.val.assign(static_cast<size_t>(S.d) * VMAX, 0.0);
+  for (int j = 0; j < S.d; ++j) {
+    const FeatureH& F = S.feat[j];
+    for (int v = 0; v < F.n; ++v) {
+      double x = F.num[v];
+      if (j == P.kf[K_AR]) {
+        if (F.vkind == 1) x = F.num[v] != 0.0 ? 2.0 : 0.0;
+        else if (F.vkind == 2) {
+          if (F.str[v] == "none") x = 0;
+          else if (F.str[v] == "sel") x = 1;
+          else if (F.str[v] == "full") x = 2;
+          else return err(E_SCHEMA, "ar values must be bool or none|sel|full");
+        }
+      } else if (j == P.kf[K_DISP] && F.vkind == 2) {
+        if (F.str[v] == "alltoall") x = 0;
+        else if (F.str[v] == "allgather") x = 1;
+        else return err(E_SCHEMA, "disp values must be alltoall|allgather");
+      }
+      S.val[j * VMAX + v] = x;
+    }
+  }
+  P.n_cls = static_cast<int>(cls.size());
+  for (int i = 0; i < P.n_cls; ++i) {
+    P.cls_count[i] = cls[i].count;
+    P.cls_cap[i] = cls[i].cap;
+    P.cls_eff[i] = cls[i].eff;
+  }
+  auto mc = [&](const char* k, double d) { return model_const(model, k, d); };
+  auto hc = [&](const char* k, double d) { return model_const(hw, k, d); };
+  P.F_work = mc("F_work", 100); P.alpha_tp = mc("alpha_tp", 2.0); P.alpha_dp = mc("alpha_dp", 1.5);
+  P.r_ar = mc("r_ar", 1.33); P.B = mc("B", 64); P.P_mem = mc("P_mem", 0); P.A_mem = mc("A_mem", 0);
+  P.L = mc("L", 1); P.h = mc("h", 1); P.a = mc("a", 1); P.kv = mc("kv", 1); P.S = mc("S", 1);
+  P.GBS = mc("GBS", 1); P.P = mc("P", 0); P.P_exp = mc("P_exp", 0); P.E = mc("E", 1); P.topk = mc("topk", 1);
+  P.dh = mc("dh", 128); P.ffn = mc("ffn", 0); P.P_in = mc("P_in", 1); P.P_out = mc("P_out", 1);
+  P.mml = mc("max_model_len", 1); P.w_tpot = mc("w_tpot", 0.5);
+  P.peak = hc("peak_flops", 312e12); P.mfu0 = hc("mfu0", 0.5); P.bw_intra = hc("bw_intra", 240e9);
+  P.bw_inter = hc("bw_inter", 25e9); P.gpn = hc("gpus_per_node", 8); P.n_sm = hc("n_sm", 108);
+  P.bw_hbm = hc("bw_hbm", 2.039e12);
+  P.G = S.G;
+
+  // ---------------------------------------------------------------- GP hyper-parameters + features
+  const asj::Value* gp = doc.get("gp");
+  S.ls.assign(S.d, 1.0);
+  if (gp) {
+    if (const asj::Value* k = gp->get("kernel")) {
+      if (k->str == "matern52") S.kernel = 0;
+      else if (k->str == "rbf") S.kernel = 1;
+      else return err(E_SCHEMA, "gp.kernel must be matern52|rbf");
+    }
+    if (const asj::Value* l = gp->get("lengthscale")) {
+      if (l->kind == asj::Value::Number) S.ls.assign(S.d, l->num);
+      else if (l->kind == asj::Value::Array && static_cast<int>(l->arr.size()) == S.d)
+        for (int j = 0; j < S.d; ++j) S.ls[j] = l->arr[j].num;
+      else return err(E_SCHEMA, "gp.lengthscale must be a number or an array of d numbers");
+    }
+    S.sf2 = model_const(gp, "sf2", 0.1);
+    S.sn2 = model_const(gp, "sn2", 1e-3);
+    S.xi = model_const(gp, "xi", 0.0);
+    S.kappa = model_const(gp, "kappa", 2.0);
+  }
+  for (double l : S.ls)
+    if (!(l > 0)) return err(E_SCHEMA, "gp.lengthscale must be positive");
+  if (!(S.sf2 > 0) || !(S.sn2 > 0)) return err(E_SCHEMA, "gp.sf2 and gp.sn2 must be positive");
+  S.xt64.assign(static_cast<size_t>(S.d) * VMAX, 0.0);
+  S.xt32.assign(static_cast<size_t>(S.d) * VMAX, 0.0f);
+  for (int j = 0; j < S.d; ++j)
+    for (int v = 0; v < S.feat[j].n; ++v) {
+      const double phi = S.feat[j].n > 1 ? double(v) / double(S.feat[j].n - 1) : 0.0;
+      S.xt64[j * VMAX + v] = phi / S.ls[j];
+      S.xt32[j * VMAX + v] = static_cast<float>(phi / S.ls[j]);
+    }
+  return Status{};
+}
+
+bool cvi_decode(const HostSpace& S, uint64_t p, DV& dv, uint32_t& act, uint64_t& raw) {
+  if (p >= S.n_cvi) return false;
+  int lo = 0, hi = S.n_struct;
+  while (hi - lo > 1) {
+    int mid = (lo + hi) / 2;
+    if (S.prefix[mid] <= p) lo = mid; else hi = mid;
+  }
+  const int n_comp = static_cast<int>(S.comp_first.size());
+  uint64_t t = p - S.prefix[lo];
+  dv = S.s_dv[lo];
+  act = S.s_act[lo];
+  raw = S.s_raw[lo];
+  for (int c = n_comp - 1; c >= 0; --c) {
+    const uint32_t off = S.s_off[static_cast<size_t>(lo) * n_comp + c], cnt = S.s_cnt[static_cast<size_t>(lo) * n_comp + c];
+    const Tuple& tu = S.tuples[off + t % cnt];
+    t /= cnt;
+    dv.w[0] |= tu.dv.w[0]; dv.w[1] |= tu.dv.w[1]; dv.w[2] |= tu.dv.w[2];
+    act |= tu.act;
+    raw += tu.raw;
+  }
+  return true;
+}
+
+bool raw_decode(const HostSpace& S, uint64_t raw, int* dig, DV& dv, uint32_t& act, bool& structural) {
+  if (raw >= S.n_raw) return false;
+  for (int j = 0; j < S.d; ++j) dig[j] = static_cast<int>((raw / S.stride[j]) % S.feat[j].n);
+  bool a[DMAX];
+  activity(S, dig, a);
+  structural = true;
+  for (int j = 0; j < S.d; ++j)
+    if (!a[j] && dig[j] != S.feat[j].dflt) structural = false;
+  for (const ConstraintH& c : S.cons)
+    if (!constraint_ok(S, c, dig, a)) structural = false;
+  dv_from_digits(S, dig, dv);
+  act = act_bits(S, a);
+  return true;
+}
+
+void simulate_host(const HostSpace& S, const DV& dv, uint32_t act, double& cost, bool& ok, double& mem) {
+  Knobs k;
+  load_knobs(S.sim, S.val.data(), dv, act, k);
+  simulate(S.sim, k, cost, ok, mem);
+}
+
+Status gp_fit(const HostSpace& S, const std::vector<DV>& obs_dv, const std::vector<uint32_t>& obs_act,
+              const std::vector<double>& cost, const std::vector<double>& cost_sim, GPFit& fit) {
+  (void)obs_act;
+  const int M = static_cast<int>(obs_dv.size());
+  const int d = S.d;
+  fit = GPFit{};
+  fit.M = M;
+  if (M == 0) return Status{};
+  fit.X.resize(static_cast<size_t>(M) * d);
+  std::vector<double> y(M), m0(M), r(M);
+  for (int i = 0; i < M; ++i) {
+    for (int j = 0; j < d; ++j) fit.X[i * d + j] = S.xt64[j * VMAX + dv_get(obs_dv[i], j)];
+    y[i] = std::log(cost[i]);
+    m0[i] = std::log(cost_sim[i]);
+  }
+  double sum = 0.0;
+  for (int i = 0; i < M; ++i) sum += y[i] - m0[i];
+  fit.b = sum / M;
+  fit.fstar = INFINITY;
+  for (int i = 0; i < M; ++i) {
+    r[i] = (y[i] - m0[i]) - fit.b;
+    fit.fstar = std::fmin(fit.fstar, y[i]);
+  }
+  // K = k(o_i, o_j) + sn2 I ; Cholesky K = L L^T
+  std::vector<double> L(static_cast<size_t>(M) * M, 0.0);
+  for (int i = 0; i < M; ++i)
+    for (int j = 0; j <= i; ++j) {
+      double r2 = 0.0;
+      for (int q = 0; q < d; ++q) {
+        const double df = fit.X[i * d + q] - fit.X[j * d + q];
+        r2 += df * df;
+      }
+      L[i * M + j] = kernel64(S.kernel, S.sf2, r2) + (i == j ? S.sn2 : 0.0);
+    }
+  for (int j = 0; j < M; ++j) {
+    double s = L[j * M + j];
+    for (int q = 0; q < j; ++q) s -= L[j * M + q] * L[j * M + q];
+    if (!(s > 0.0)) return err(E_NUM, "Cholesky of the GP covariance failed (not positive definite)");
+    const double ljj = std::sqrt(s);
+    L[j * M + j] = ljj;
+    for (int i = j + 1; i < M; ++i) {
+      double t = L[i * M + j];
+      for (int q = 0; q < j; ++q) t -= L[i * M + q] * L[j * M + q];
+      L[i * M + j] = t / ljj;
+    }
+  }
+  // alpha = L^-T L^-1 r
+  std::vector<double> z(M);
+  for (int i = 0; i < M; ++i) {
+    double t = r[i];
+    for (int q = 0; q < i; ++q) t -= L[i * M + q] * z[q];
+    z[i] = t / L[i * M + i];
+  }
+  fit.alpha.assign(M, 0.0);
+  for (int i = M - 1; i >= 0; --i) {
+    double t = z[i];
+    for (int q = i + 1; q < M; ++q) t -= L[q * M + i] * fit.alpha[q];
+    fit.alpha[i] = t / L[i * M + i];
+  }
+  // W = L^-1 (lower triangular), column by column
+  fit.Wl.assign(static_cast<size_t>(M) * M, 0.0);
+  for (int c = 0; c < M; ++c) {
+    for (int i = c; i < M; ++i) {
+      double t = (i == c) ? 1.0 : 0.0;
+      for (int q = c; q < i; ++q) t -= L[i * M + q] * fit.Wl[q * M + c];
+      fit.Wl[i * M + c] = t / L[i * M + i];
+    }
+  }
+  double fro = 0.0;
+  for (double w : fit.Wl) fro += w * w;
+  fit.w_fro = std::sqrt(fro);
+  return Status{};
+}
+
+}  // namespace as

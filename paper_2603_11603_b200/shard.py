@@ -1,0 +1,67 @@
+"""Sharding layer: split one scoring batch across 1/2/4/8 GPUs (one process per GPU) and merge
+the per-GPU top-k with ONE all-gather.
+
+The candidate positions [begin, begin+count) are cut into `world` contiguous shares (remainder to
+the lowest ranks); each rank scores its share on its own device, refines its pool in FP64 and
+exports it with an upper bound ("cut") on every candidate it dropped.  One
+`torch.distributed.all_gather` of the packed pools (NCCL over NVLink on GPUs, gloo in CPU tests)
+gives every rank all pools; `autoscout_topk_merge` (host C++) merges them with the total order
+(score desc, raw asc) and certifies globally.  Every rank ends with the identical top-k.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .autoscout import ENTRY_DTYPE, topk_merge
+
+
+def shard_range(begin, count, rank, world):
+    share, rem = divmod(count, world)
+    lo = begin + rank * share + min(rank, rem)
+    return lo, share + (1 if rank < rem else 0)
+
+
+def pack_pool(pool, n, cut):
+    """-> int64 array [2 + 2*cap]: (n, cut bits, then (score bits, raw) pairs)."""
+    cap = len(pool)
+    buf = np.zeros(2 + 2 * cap, dtype=np.int64)
+    buf[0] = n
+    buf[1] = np.array([cut], dtype=np.float64).view(np.int64)[0]
+    buf[2:] = pool.view(np.int64)
+    return buf
+
+
+def unpack_pools(mat, cap):
+    mat = np.asarray(mat, dtype=np.int64).reshape(-1, 2 + 2 * cap)
+    counts = mat[:, 0].astype(np.int32)
+    cuts = mat[:, 1].copy().view(np.float64)
+    pools = np.ascontiguousarray(mat[:, 2:]).view(ENTRY_DTYPE).reshape(len(mat), cap)
+    return pools, counts, cuts
+
+
+def gather_merge(pool, n, cut, k, group=None, device=None):
+    """All-gather packed pools (one collective) and merge -> (top-k list, certified)."""
+    import torch
+    import torch.distributed as dist
+
+    cap = len(pool)
+    packed = torch.from_numpy(pack_pool(pool, n, cut))
+    if device is not None:
+        packed = packed.to(device)
+    world = dist.get_world_size(group)
+    outs = [torch.empty_like(packed) for _ in range(world)]
+    dist.all_gather(outs, packed, group=group)
+    mat = torch.stack(outs).cpu().numpy()
+    pools, counts, cuts = unpack_pools(mat, cap)
+    return topk_merge(pools, counts, cuts, k)
+
+
+def score_topk_sharded(space, k, begin, count, rank, world, mode="sample", seed=0, acq="ei", cap=None,
+                       group=None, device=None, stream=None):
+    """Score this rank's share on its GPU, then merge all ranks' pools.  -> (top-k, certified)."""
+    lo, n = shard_range(begin, count, rank, world)
+    space.score_batch(mode=mode, begin=lo, count=n, seed=seed, acq=acq, k=k, stream=stream)
+    cap = cap or (k + max(k, 64))
+    pool, npool, cut = space.topk_pool(k, cap, stream=stream)
+    return gather_merge(pool, npool, cut, k, group=group, device=device)

@@ -23,8 +23,9 @@ def _cmp(a, op, b):
     return {">": a > b, ">=": a >= b, "==": a == b, "!=": a != b, "<": a < b, "<=": a <= b}[op]
 
 
-def enumerate_valid_raw(doc, G, chunk=1 << 22):
-    """-> sorted np.ndarray of raw indices satisfying G1 and every structural constraint."""
+def enumerate_valid_raw(doc, G, chunk=1 << 22, window=None):
+    """-> sorted np.ndarray of raw indices (optionally within window=(lo, hi)) satisfying G1 and every
+    structural constraint."""
     feats = doc["features"]
     names = [f["name"] for f in feats]
     idx = {n: i for i, n in enumerate(names)}
@@ -40,8 +41,9 @@ def enumerate_valid_raw(doc, G, chunk=1 << 22):
     model = doc.get("model", {})
     const = lambda n: G if n == "G" else model[n]
     out = []
-    for lo in range(0, n_raw, chunk):
-        raw = np.arange(lo, min(n_raw, lo + chunk), dtype=np.int64)
+    w_lo, w_hi = window if window is not None else (0, n_raw)
+    for lo in range(w_lo, w_hi, chunk):
+        raw = np.arange(lo, min(w_hi, lo + chunk), dtype=np.int64)
         D = [(raw // strides[j]) % sizes[j] for j in range(d)]
         act = []
         for j, f in enumerate(feats):
