@@ -118,16 +118,18 @@ as_status autoscout_score_batch(as_space* s, const as_score_args* a, void* cuda_
 as_status autoscout_topk(as_space* s, int32_t k, uint64_t* raw_out, double* score_out, int32_t* n_out,
                          void* cuda_stream);
 
-/* Sharding.  topk_pool: refine the local pool and copy it to host memory as
- * `cap` entries {double score; uint64_t raw} ordered (score desc, raw asc); n_out = entries
- * written; *cut_out = upper bound on the score of every locally scored candidate NOT in the
- * pool (-INF if none was dropped).  topk_merge: merge `n_pools` gathered pools laid out as
- * [n_pools][cap] entries with per-pool counts and cuts; certify globally.  Host-only work:
- * valid on a host-only handle.  *certified_out = 1 if the merged top-k is certified. */
+/* Sharding.  Pool entries are {double score; uint64_t raw} (16 bytes), ordered
+ * (score desc, raw asc).  topk_pool: refine the local pool and copy up to `cap` entries to host
+ * memory; n_out = entries written; *cut_out = an entry that every locally scored candidate NOT in
+ * the exported pool ranks after or equals in the total order (cut score = upper bound on its
+ * score; score -INF when nothing was dropped).  topk_merge: merge `n_pools` gathered pools laid out
+ * as [n_pools][cap] entries with per-pool counts and cuts ([n_pools] entries); certify globally:
+ * certified iff the k-th merged entry ranks strictly before every cut.  Host-only work: valid on
+ * a host-only handle (s may be NULL).  *certified_out = 1 if the merged top-k is certified. */
 as_status autoscout_topk_pool(as_space* s, int32_t k, void* pool_out, int32_t cap, int32_t* n_out,
-                              double* cut_out, void* cuda_stream);
+                              void* cut_out, void* cuda_stream);
 as_status autoscout_topk_merge(const as_space* s, const void* pools, const int32_t* counts,
-                               const double* cuts, int32_t n_pools, int32_t cap, int32_t k,
+                               const void* cuts, int32_t n_pools, int32_t cap, int32_t k,
                                uint64_t* raw_out, double* score_out, int32_t* n_out,
                                int32_t* certified_out);
 

@@ -73,8 +73,8 @@ def _load():
         "autoscout_observe_info": ([P, pI32, pD, pD], I32),
         "autoscout_score_batch": ([P, ctypes.POINTER(ScoreArgs), P], I32),
         "autoscout_topk": ([P, I32, pU64, pD, pI32, P], I32),
-        "autoscout_topk_pool": ([P, I32, P, I32, pI32, pD, P], I32),
-        "autoscout_topk_merge": ([P, P, pI32, pD, I32, I32, I32, pU64, pD, pI32, pI32], I32),
+        "autoscout_topk_pool": ([P, I32, P, I32, pI32, P, P], I32),
+        "autoscout_topk_merge": ([P, P, pI32, P, I32, I32, I32, pU64, pD, pI32, pI32], I32),
         "autoscout_decode": ([P, U64, pI32, pI32], I32),
         "autoscout_cvi_to_raw": ([P, U64, pU64], I32),
         "autoscout_sample_to_cvi": ([P, U64, U64, pU64], I32),
@@ -227,12 +227,13 @@ class Space:
         return [(int(raw[i]), float(sc[i])) for i in range(n.value)]
 
     def topk_pool(self, k, cap, stream=None):
+        """-> (pool [cap] ENTRY_DTYPE, n, cut ENTRY_DTYPE scalar array of 1)."""
         buf = np.zeros(cap, dtype=ENTRY_DTYPE)
+        cut = np.zeros(1, dtype=ENTRY_DTYPE)
         n = ctypes.c_int32()
-        cut = ctypes.c_double()
         _check(_LIB.autoscout_topk_pool(self.h, int(k), buf.ctypes.data_as(ctypes.c_void_p), int(cap),
-                                        ctypes.byref(n), ctypes.byref(cut), _stream_ptr(stream)))
-        return buf, n.value, cut.value
+                                        ctypes.byref(n), cut.ctypes.data_as(ctypes.c_void_p), _stream_ptr(stream)))
+        return buf, n.value, cut
 
     def mask_range(self, raw_begin, count, d_bits, d_valid_count=None, stream=None):
         _check(_LIB.autoscout_mask_range(self.h, int(raw_begin), int(count), _ptr(d_bits), _ptr(d_valid_count),
@@ -248,22 +249,30 @@ class Space:
 
 
 def topk_merge(pools, counts, cuts, k):
-    """Merge gathered pools ([n_pools, cap] ENTRY_DTYPE) -> (list[(raw, score)], certified)."""
+    """Merge gathered pools ([n_pools, cap] ENTRY_DTYPE, counts [n_pools], cuts [n_pools] ENTRY_DTYPE)
+    -> (list[(raw, score)], certified)."""
     pools = np.ascontiguousarray(pools, dtype=ENTRY_DTYPE)
     n_pools, cap = pools.shape
     counts = np.ascontiguousarray(counts, dtype=np.int32)
-    cuts = np.ascontiguousarray(cuts, dtype=np.float64)
+    cuts = np.ascontiguousarray(cuts, dtype=ENTRY_DTYPE).reshape(n_pools)
     raw = (ctypes.c_uint64 * k)()
     sc = (ctypes.c_double * k)()
     n = ctypes.c_int32()
     cert = ctypes.c_int32()
     st = _LIB.autoscout_topk_merge(None, pools.ctypes.data_as(ctypes.c_void_p),
                                    counts.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-                                   cuts.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), int(n_pools), int(cap),
+                                   cuts.ctypes.data_as(ctypes.c_void_p), int(n_pools), int(cap),
                                    int(k), raw, sc, ctypes.byref(n), ctypes.byref(cert))
     if st not in (0, 12):
         _check(st)
     return [(int(raw[i]), float(sc[i])) for i in range(n.value)], bool(cert.value)
+
+
+def no_cut():
+    c = np.zeros(1, dtype=ENTRY_DTYPE)
+    c["score"] = -np.inf
+    c["raw"] = np.iinfo(np.uint64).max
+    return c
 
 
 # C-ABI-named entry points (same names as include/autoscout.h)

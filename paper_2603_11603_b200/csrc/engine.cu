@@ -57,6 +57,7 @@ size_t score_smem_bytes(int Mp, int DP, int d, int P) {
   s += r16(sizeof(float) * 4 * 8 * 32);
   s += r16(sizeof(uint64_t) * 32);
   s += r16(sizeof(uint64_t) * P);
+  s += r16(sizeof(double) * (Mp > 0 ? Mp : 1));
   return s;
 }
 
@@ -312,7 +313,7 @@ as_status rescore_all(as_space* s, cudaStream_t st) {
 
 // Certified refine: grow k' and re-score the recorded batches until the k-th refined score beats
 // the upper bound of every dropped candidate.
-as_status certified_pool(as_space* s, int k, cudaStream_t st, std::vector<Entry>& ent, double& cut_score,
+as_status certified_pool(as_space* s, int k, cudaStream_t st, std::vector<Entry>& ent, Entry& cut_e,
                          bool& certified) {
   const as_score_args& a0 = s->batches.front();
   for (;;) {
@@ -320,9 +321,16 @@ as_status certified_pool(as_space* s, int k, cudaStream_t st, std::vector<Entry>
     int n_pool;
     as_status r = refine_pool(s, a0.acq, a0.kappa, a0.xi, st, ent, cut, n_pool);
     if (r != AS_OK) return r;
-    cut_score = (cut == KEY_NONE) ? -INFINITY : static_cast<double>(key_score(cut));
-    certified = (cut == KEY_NONE) ||
-                (static_cast<int>(ent.size()) >= k && ent[k - 1].score > cut_score);
+    if (cut == KEY_NONE) {
+      cut_e = Entry{-INFINITY, ~0ull};
+    } else {
+      DV dv;
+      uint32_t act;
+      uint64_t raw = 0;
+      cvi_decode(s->H, cut & 0xFFFFFFFFull, dv, act, raw);
+      cut_e = Entry{static_cast<double>(key_score(cut)), raw};
+    }
+    certified = (cut == KEY_NONE) || (static_cast<int>(ent.size()) >= k && entry_less(ent[k - 1], cut_e));
     if (certified || s->KC * 2 > s->KC_max) return AS_OK;
     s->KC *= 2;
     r = rescore_all(s, st);
@@ -559,9 +567,9 @@ as_status autoscout_topk(as_space* s, int32_t k, uint64_t* raw_out, double* scor
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   CUDA_TRY(cudaSetDevice(s->device));
   std::vector<Entry> ent;
-  double cut_score;
+  Entry cut_e;
   bool certified;
-  as_status r = certified_pool(s, k, st, ent, cut_score, certified);
+  as_status r = certified_pool(s, k, st, ent, cut_e, certified);
   if (r != AS_OK) return r;
   const int n = std::min<int>(k, static_cast<int>(ent.size()));
   for (int i = 0; i < n; ++i) {
@@ -573,41 +581,45 @@ as_status autoscout_topk(as_space* s, int32_t k, uint64_t* raw_out, double* scor
   return AS_OK;
 }
 
-as_status autoscout_topk_pool(as_space* s, int32_t k, void* pool_out, int32_t cap, int32_t* n_out, double* cut_out,
+as_status autoscout_topk_pool(as_space* s, int32_t k, void* pool_out, int32_t cap, int32_t* n_out, void* cut_out,
                               void* cuda_stream) {
   if (!s || !pool_out || !n_out || !cut_out || cap < 1 || k < 1) return fail(AS_ERR_INVALID_ARG, "bad arguments");
   if (!s->scored || s->batches.empty()) return fail(AS_ERR_STATE, "nothing scored");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   CUDA_TRY(cudaSetDevice(s->device));
   std::vector<Entry> ent;
-  double cut_score;
+  Entry cut_e;
   bool certified;
-  // locally certified pools make the global certificate cheap; it is re-checked in topk_merge
-  as_status r = certified_pool(s, k, st, ent, cut_score, certified);
+  // a locally certified pool keeps the global certificate cheap; it is re-checked in topk_merge
+  as_status r = certified_pool(s, k, st, ent, cut_e, certified);
   if (r != AS_OK) return r;
-  // entries beyond `cap` are dropped: their scores raise the cut
   const int n = std::min<int>(cap, static_cast<int>(ent.size()));
-  double cut = cut_score;
-  if (static_cast<int>(ent.size()) > cap) cut = std::max(cut, ent[cap].score);
+  // entries beyond `cap` are dropped here: the best of them bounds the rest
+  if (static_cast<int>(ent.size()) > cap && entry_less(ent[cap], cut_e)) cut_e = ent[cap];
   std::memcpy(pool_out, ent.data(), static_cast<size_t>(n) * sizeof(Entry));
+  std::memcpy(cut_out, &cut_e, sizeof(Entry));
   *n_out = n;
-  *cut_out = cut;
   return AS_OK;
 }
 
-as_status autoscout_topk_merge(const as_space* s, const void* pools, const int32_t* counts, const double* cuts,
+as_status autoscout_topk_merge(const as_space* s, const void* pools, const int32_t* counts, const void* cuts,
                                int32_t n_pools, int32_t cap, int32_t k, uint64_t* raw_out, double* score_out,
                                int32_t* n_out, int32_t* certified_out) {
   (void)s;
   if (!pools || !counts || !cuts || n_pools < 1 || cap < 1 || k < 1 || !raw_out || !score_out || !n_out)
     return fail(AS_ERR_INVALID_ARG, "bad arguments");
   const Entry* P = static_cast<const Entry*>(pools);
+  const Entry* C = static_cast<const Entry*>(cuts);
   std::vector<Entry> all;
-  double cut = -INFINITY;
+  Entry cut{-INFINITY, ~0ull};
+  bool any_cut = false;
   for (int p = 0; p < n_pools; ++p) {
     if (counts[p] < 0 || counts[p] > cap) return fail(AS_ERR_INVALID_ARG, "pool count out of range");
     for (int i = 0; i < counts[p]; ++i) all.push_back(P[static_cast<size_t>(p) * cap + i]);
-    cut = std::max(cut, cuts[p]);
+    if (C[p].score != -INFINITY) {
+      if (!any_cut || entry_less(C[p], cut)) cut = C[p];
+      any_cut = true;
+    }
   }
   std::sort(all.begin(), all.end(), entry_less);
   all.erase(std::unique(all.begin(), all.end(), [](const Entry& a, const Entry& b) { return a.raw == b.raw; }),
@@ -618,7 +630,7 @@ as_status autoscout_topk_merge(const as_space* s, const void* pools, const int32
     score_out[i] = all[i].score;
   }
   *n_out = n;
-  const bool cert = (cut == -INFINITY) || (static_cast<int>(all.size()) >= k && all[k - 1].score > cut);
+  const bool cert = !any_cut || (static_cast<int>(all.size()) >= k && entry_less(all[k - 1], cut));
   if (certified_out) *certified_out = cert ? 1 : 0;
   return cert ? AS_OK : fail(AS_ERR_UNCERTIFIED, "merged top-k could not be certified");
 }

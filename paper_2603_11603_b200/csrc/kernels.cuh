@@ -126,6 +126,43 @@ __device__ __forceinline__ void sim_dev(const DevSpace& S, const DV& dv, uint32_
   simulate(S.sim, k, cost, ok, mem);
 }
 
+// FP64 posterior of one candidate computed by a whole warp (lanes split the observed set):
+// returns mu - m0 - b (= k^T alpha) and ||L^-1 k||^2.  ksh: M doubles of per-warp scratch.
+__device__ __forceinline__ void posterior64_warp(const DevSpace& S, const DevGP& G, const DV& dv, int lane,
+                                                 double* ksh, double& kalpha, double& vsq) {
+  double x[DMAX];
+#pragma unroll
+  for (int f = 0; f < DMAX; ++f) x[f] = (f < S.d) ? __ldg(S.xt64 + f * VMAX + dv_get(dv, f)) : 0.0;
+  double mp = 0.0;
+  for (int i = lane; i < G.M; i += 32) {
+    double r2 = 0.0;
+#pragma unroll
+    for (int f = 0; f < DMAX; ++f)
+      if (f < S.d) {
+        const double df = x[f] - __ldg(G.O64 + i * S.d + f);
+        r2 += df * df;
+      }
+    const double kv = kernel64(G.kernel, G.sf2, r2);
+    ksh[i] = kv;
+    mp += kv * __ldg(G.alpha64 + i);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mp += __shfl_xor_sync(0xffffffffu, mp, o);
+  kalpha = mp;
+  __syncwarp();
+  double vs = 0.0;
+  for (int i = 0; i < G.M; ++i) {
+    double part = 0.0;
+    const double* wr = G.W64 + static_cast<size_t>(i) * G.M;
+    for (int jj = lane; jj <= i; jj += 32) part += __ldg(wr + jj) * ksh[jj];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    vs += part * part;
+  }
+  __syncwarp();
+  vsq = vs;
+}
+
 // Bitonic sort of arr[0..n) ascending (n power of two), all threads of the block.
 __device__ __forceinline__ void bitonic_sort(uint64_t* arr, int n) {
   for (int k = 2; k <= n; k <<= 1) {
@@ -205,6 +242,7 @@ struct ScoreSmem {
   float* red;      // [4][8][32]
   uint64_t* arr;   // [P]
   uint64_t* ckey;  // [32]
+  double* k64;     // [Mp] FP64 scratch of the sensitive-candidate fallback
 };
 
 template <bool GP>
@@ -240,6 +278,7 @@ score_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out) {
   sm.red = reinterpret_cast<float*>(take(sizeof(float) * 4 * 8 * 32));
   sm.ckey = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 32));
   sm.arr = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * out.P));
+  sm.k64 = reinterpret_cast<double*>(take(sizeof(double) * (Mp > 0 ? Mp : 1)));
 
   // ---- stage the observed set, L^-1 blocks and the feature table into SMEM
   if (GP) {
@@ -413,11 +452,50 @@ score_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out) {
           const double kn = sqrt(static_cast<double>(kk));
           const double d_s2 = 2.5 * ew * sqrt(vs) * kn + ew * ew * static_cast<double>(kk) +
                               G.eps * vs + 4.0 * static_cast<double>(U32) * G.sf2;
-          const double sc = acquisition(A.acq, mu, s2, cm0, G.fstar, A.xi, A.kappa);
+          double sc = acquisition(A.acq, mu, s2, cm0, G.fstar, A.xi, A.kappa);
           double ub = acquisition(A.acq, mu - d_mu, s2 + d_s2, cm0, G.fstar, A.xi, A.kappa);
           ub += 1e-12 * fmax(1.0, fabs(ub));
-          if (A.d_scores) A.d_scores[sm.q_j[slot]] = static_cast<float>(sc);
-          if (ub > -INFINITY) key = make_key(__double2float_ru(ub), sm.q_cvi[slot]);
+          // Per-candidate EI outputs whose FP32 error could exceed 1e-5 (small sigma^2 near an observed
+          // point, z >= -3.2) are recomputed in FP64.  Error model calibrated against
+          // the FP64 oracle: |d s2| <= 20 u ||v||^2, |d mu| <= u (1 + sum k(1+a)|alpha|).  Only when
+          // d_scores is requested: the top-k itself is certified and FP64-refined regardless.
+          bool sensitive = false;
+          if (A.d_scores && A.acq == 0) {
+            if (s2 > 0.0) {
+              const double sg = sqrt(s2), z = (G.fstar - mu - A.xi) / sg;
+              if (z >= -3.2) {
+                const double Phi = 0.5 * erfc(-z * INV_SQRT2);
+                const double h = exp(-0.5 * z * z) * INV_SQRT_2PI + z * Phi;
+                const double uu = static_cast<double>(U32);
+                const double e_s = (1.0 - z * Phi / h) / (2.0 * s2) * 20.0 * uu * vs +
+                                   Phi / (sg * h) * uu * (1.0 + static_cast<double>(sb));
+                sensitive = e_s > 5e-6;
+              }
+            } else {
+              sensitive = true;
+            }
+          }
+          sm.ckey[lane] = sensitive ? 1ull : 0ull;
+          if (!sensitive) {
+            if (A.d_scores) A.d_scores[sm.q_j[slot]] = static_cast<float>(sc);
+            if (ub > -INFINITY) key = make_key(__double2float_ru(ub), sm.q_cvi[slot]);
+          }
+        }
+        // warp-cooperative FP64 posterior for the flagged lanes
+        unsigned fl = __ballot_sync(0xffffffffu, has && sm.ckey[lane] == 1ull);
+        while (fl) {
+          const int src = __ffs(fl) - 1;
+          fl &= fl - 1;
+          const int fslot = head + src;
+          double kalpha, vsq;
+          posterior64_warp(S, G, sm.q_dv[fslot], lane, sm.k64, kalpha, vsq);
+          if (lane == src) {
+            const double cm0 = sm.q_m0[fslot];
+            const double sc = acquisition(A.acq, cm0 + G.b + kalpha, G.sf2 - vsq, cm0, G.fstar, A.xi, A.kappa);
+            const double ub = sc + 1e-12 * fmax(1.0, fabs(sc));
+            if (A.d_scores) A.d_scores[sm.q_j[fslot]] = static_cast<float>(sc);
+            if (ub > -INFINITY) key = make_key(__double2float_ru(ub), sm.q_cvi[fslot]);
+          }
         }
         sm.ckey[lane] = key;
       }
@@ -533,35 +611,9 @@ refine_kernel(DevSpace S, DevGP G, const uint64_t* pool, const int* pool_n, int 
   const double m0 = log(cost);
   double mu = m0 + G.b, s2 = G.sf2;
   if (G.M > 0 && acq != 2) {
-    double x[DMAX];
-#pragma unroll
-    for (int f = 0; f < DMAX; ++f) x[f] = (f < S.d) ? S.xt64[f * VMAX + dv_get(dv, f)] : 0.0;
-    double mp = 0.0;
-    for (int i = lane; i < G.M; i += 32) {
-      double r2 = 0.0;
-#pragma unroll
-      for (int f = 0; f < DMAX; ++f)
-        if (f < S.d) {
-          const double df = x[f] - G.O64[i * S.d + f];
-          r2 += df * df;
-        }
-      const double kv = kernel64(G.kernel, G.sf2, r2);
-      ksh[i] = kv;
-      mp += kv * G.alpha64[i];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mp += __shfl_xor_sync(0xffffffffu, mp, o);
-    mu += mp;
-    __syncwarp();
-    double vsq = 0.0;
-    for (int i = 0; i < G.M; ++i) {
-      double part = 0.0;
-      const double* wr = G.W64 + static_cast<size_t>(i) * G.M;
-      for (int jj = lane; jj <= i; jj += 32) part += wr[jj] * ksh[jj];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      vsq += part * part;
-    }
+    double kalpha, vsq;
+    posterior64_warp(S, G, dv, lane, ksh, kalpha, vsq);
+    mu += kalpha;
     s2 = G.sf2 - vsq;
   }
   const double sc = acquisition(acq, mu, s2, m0, G.fstar, xi, kappa);

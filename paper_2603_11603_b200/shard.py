@@ -23,20 +23,20 @@ def shard_range(begin, count, rank, world):
 
 
 def pack_pool(pool, n, cut):
-    """-> int64 array [2 + 2*cap]: (n, cut bits, then (score bits, raw) pairs)."""
+    """-> int64 array [4 + 2*cap]: (n, 0, cut entry (score bits, raw), then (score bits, raw) pairs)."""
     cap = len(pool)
-    buf = np.zeros(2 + 2 * cap, dtype=np.int64)
+    buf = np.zeros(4 + 2 * cap, dtype=np.int64)
     buf[0] = n
-    buf[1] = np.array([cut], dtype=np.float64).view(np.int64)[0]
-    buf[2:] = pool.view(np.int64)
+    buf[2:4] = np.ascontiguousarray(cut, dtype=ENTRY_DTYPE).view(np.int64)
+    buf[4:] = np.ascontiguousarray(pool, dtype=ENTRY_DTYPE).view(np.int64)
     return buf
 
 
 def unpack_pools(mat, cap):
-    mat = np.asarray(mat, dtype=np.int64).reshape(-1, 2 + 2 * cap)
+    mat = np.asarray(mat, dtype=np.int64).reshape(-1, 4 + 2 * cap)
     counts = mat[:, 0].astype(np.int32)
-    cuts = mat[:, 1].copy().view(np.float64)
-    pools = np.ascontiguousarray(mat[:, 2:]).view(ENTRY_DTYPE).reshape(len(mat), cap)
+    cuts = np.ascontiguousarray(mat[:, 2:4]).view(ENTRY_DTYPE).reshape(len(mat))
+    pools = np.ascontiguousarray(mat[:, 4:]).view(ENTRY_DTYPE).reshape(len(mat), cap)
     return pools, counts, cuts
 
 

@@ -159,17 +159,27 @@ def test_host_only_cannot_score(host_spaces):
 def test_topk_merge_host():
     rng = np.random.default_rng(0)
     pools = np.zeros((3, 8), dtype=A.ENTRY_DTYPE)
-    allv = []
     for p in range(3):
         sc = np.sort(rng.normal(size=8))[::-1]
         pools[p]["score"] = sc
         pools[p]["raw"] = rng.choice(10_000, 8, replace=False) + 10_000 * p
-        allv += list(zip(pools[p]["raw"].tolist(), sc.tolist()))
     pools[1]["score"][2] = pools[0]["score"][1]          # a tie across pools -> raw breaks it
+    for p in range(3):                                   # keep each pool ordered (score desc, raw asc)
+        order = sorted(range(8), key=lambda i: (-pools[p]["score"][i], pools[p]["raw"][i]))
+        pools[p] = pools[p][order]
     allv = [(int(r), float(s)) for r, s in zip(pools["raw"].ravel(), pools["score"].ravel())]
     ref = sorted(allv, key=lambda t: (-t[1], t[0]))[:5]
-    got, cert = A.topk_merge(pools, [8, 8, 8], [-np.inf] * 3, 5)
+    nocut = np.concatenate([A.no_cut()] * 3)
+    got, cert = A.topk_merge(pools, [8, 8, 8], nocut, 5)
     assert got == ref and cert
-    # a cut above the 5th score -> not certified
-    got, cert = A.topk_merge(pools, [8, 8, 8], [-np.inf, ref[4][1] + 1.0, -np.inf], 5)
+    # a cut entry ranking before the 5th -> not certified
+    cuts = nocut.copy()
+    cuts[1]["score"] = ref[4][1] + 1.0
+    cuts[1]["raw"] = 5
+    got, cert = A.topk_merge(pools, [8, 8, 8], cuts, 5)
     assert not cert
+    # a cut tied with the 5th score but with a larger raw index ranks after it -> certified
+    cuts[1]["score"] = ref[4][1]
+    cuts[1]["raw"] = ref[4][0] + 1
+    got, cert = A.topk_merge(pools, [8, 8, 8], cuts, 5)
+    assert cert and got == ref
