@@ -146,6 +146,11 @@ as_status autoscout_simulate(const as_space* s, uint64_t raw, double* cost_out, 
 as_status autoscout_mask_range(as_space* s, uint64_t raw_begin, uint64_t count, uint32_t* d_bits,
                                uint64_t* d_valid_count, void* cuda_stream);
 
+/* Posterior path of the score kernel: 0 = auto (tcgen05 3xTF32 tensor-core kernel when M >= 64,
+ * SIMT FP32 kernel below), 1 = force SIMT, 2 = force tensor cores.  Both compute the same
+ * quantities; the override exists for A/B parity tests and profiling. */
+as_status autoscout_set_path(as_space* s, int32_t path);
+
 /* Device-time of the last score kernel launch in ms (CUDA events on the launching stream,
  * recorded when `timing` was enabled), for the roofline report in bench.py. */
 as_status autoscout_set_timing(as_space* s, int32_t enable);

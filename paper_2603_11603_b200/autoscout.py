@@ -33,7 +33,8 @@ ENTRY_DTYPE = np.dtype([("score", "<f8"), ("raw", "<u8")])
 EXPORTS = ["autoscout_space_create", "autoscout_space_destroy", "autoscout_space_info", "autoscout_observe",
            "autoscout_observe_clear", "autoscout_observe_info", "autoscout_score_batch", "autoscout_topk",
            "autoscout_topk_pool", "autoscout_topk_merge", "autoscout_decode", "autoscout_cvi_to_raw",
-           "autoscout_sample_to_cvi", "autoscout_simulate", "autoscout_mask_range", "autoscout_set_timing",
+           "autoscout_sample_to_cvi", "autoscout_simulate", "autoscout_mask_range", "autoscout_set_path",
+           "autoscout_set_timing",
            "autoscout_last_kernel_ms", "autoscout_last_error"]
 
 
@@ -80,6 +81,7 @@ def _load():
         "autoscout_sample_to_cvi": ([P, U64, U64, pU64], I32),
         "autoscout_simulate": ([P, U64, pD, pD, pI32], I32),
         "autoscout_mask_range": ([P, U64, U64, P, P, P], I32),
+        "autoscout_set_path": ([P, I32], I32),
         "autoscout_set_timing": ([P, I32], I32),
         "autoscout_last_kernel_ms": ([P, pD, pD], I32),
         "autoscout_last_error": ([], ctypes.c_char_p),
@@ -238,6 +240,11 @@ class Space:
     def mask_range(self, raw_begin, count, d_bits, d_valid_count=None, stream=None):
         _check(_LIB.autoscout_mask_range(self.h, int(raw_begin), int(count), _ptr(d_bits), _ptr(d_valid_count),
                                          _stream_ptr(stream)))
+
+    def set_path(self, path):
+        """0 auto, 1 SIMT, 2 tensor cores (or 'auto' / 'simt' / 'tc')."""
+        path = {"auto": 0, "simt": 1, "tc": 2}.get(path, path)
+        _check(_LIB.autoscout_set_path(self.h, int(path)))
 
     def set_timing(self, enable=True):
         _check(_LIB.autoscout_set_timing(self.h, 1 if enable else 0))

@@ -10,6 +10,7 @@
 
 #include "../../include/autoscout.h"
 #include "kernels.cuh"
+#include "kernels_tc.cuh"
 #include "space.hpp"
 
 using namespace as;
@@ -59,6 +60,35 @@ size_t score_smem_bytes(int Mp, int DP, int d, int P) {
   s += r16(sizeof(uint64_t) * P);
   s += r16(sizeof(double) * (Mp > 0 ? Mp : 1));
   return s;
+}
+
+size_t tc_smem_bytes(int Mp16, int DP, int d, int P) {
+  auto r128 = [](size_t b) { return (b + 127) & ~size_t(127); };
+  size_t s = 0;
+  s += 2 * TC_NA * r128(static_cast<size_t>(TC_ROWS) * TC_KCH * 4);
+  s += TC_NB * r128(2ull * Mp16 * TC_KCH * 4);
+  s += r128(sizeof(float) * Mp16 * DP);
+  s += 2 * r128(sizeof(float) * Mp16);
+  s += r128(sizeof(float) * d * VMAX);
+  s += r128(sizeof(DV) * TC_QCAP);
+  s += r128(sizeof(double) * TC_QCAP);
+  s += 2 * r128(sizeof(uint32_t) * TC_QCAP);
+  s += 2 * r128(sizeof(uint32_t) * TC_TI * TC_ROWS);
+  s += r128(sizeof(double) * TC_TI * TC_ROWS);
+  s += r128(sizeof(float) * TC_TI * 6 * TC_ROWS);
+  s += r128(sizeof(uint64_t) * P);
+  s += r128(sizeof(uint64_t) * 32);
+  return s;
+}
+
+// TF32 round-to-nearest (ties away), as cvt.rna.tf32.f32
+float tf32_rna(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  u = (u + 0x1000u) & 0xFFFFE000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
 }
 
 template <typename T>
@@ -114,7 +144,12 @@ struct as_space {
   DevGP G{};
   float *d_O = nullptr, *d_alpha = nullptr, *d_aabs = nullptr, *d_Wblk = nullptr;
   double *d_O64 = nullptr, *d_alpha64 = nullptr, *d_W64 = nullptr;
-  std::vector<float> h_O, h_alpha, h_aabs, h_Wblk;
+  std::vector<float> h_O, h_alpha, h_aabs, h_Wblk, h_Bch;
+  float* d_Bch = nullptr;          // L^-1^T hi/lo chunks for the tensor-core path
+  double* d_scratch = nullptr;     // FP64 scratch of the sensitive-output fallback (TC path)
+  size_t scratch_cap = 0;
+  TcB tb{};
+  int path = 0;                    // 0 auto (tensor cores for M >= 64), 1 SIMT, 2 tensor cores
   std::vector<double> h_O64, h_alpha64, h_W64;
   // pool state
   int KC = 0;
@@ -170,6 +205,30 @@ as_status upload_gp(as_space* s, cudaStream_t st) {
           if (row < M && col < M && col <= row) w = static_cast<float>(F.Wl[static_cast<size_t>(row) * M + col]);
           s->h_Wblk[(static_cast<size_t>(q) * (q + 1) / 2 + a) * 16 + b * 4 + r] = w;
         }
+  // B operand of the tensor-core path: chunk c = rows i in [16c, Mp16) x columns j in [16c, 16c+16)
+  // of L^-1 (i.e. L^-1^T in K-major form), split hi/lo TF32, core-matrix layout (kmajor_off).
+  const int Mp16 = M > 0 ? ((M + 15) / 16) * 16 : 0;
+  const int nch = Mp16 / TC_KCH;
+  s->h_Bch.clear();
+  s->tb = TcB{};
+  s->tb.Mp16 = Mp16;
+  s->tb.nch = nch;
+  for (int c = 0; c < nch; ++c) {
+    const int N = Mp16 - c * TC_KCH;
+    s->tb.off[c] = static_cast<uint32_t>(s->h_Bch.size());
+    const size_t base = s->h_Bch.size();
+    s->h_Bch.resize(base + 2ull * N * TC_KCH, 0.f);
+    for (int n = 0; n < N; ++n)
+      for (int k = 0; k < TC_KCH; ++k) {
+        const int i = c * TC_KCH + n, j = c * TC_KCH + k;
+        float w = 0.f;
+        if (i < M && j < M && j <= i) w = static_cast<float>(F.Wl[static_cast<size_t>(i) * M + j]);
+        const float hi = tf32_rna(w), lo = tf32_rna(w - hi);
+        const uint32_t off = tc::kmajor_off(n, k, TC_KCH / 4) / 4;
+        s->h_Bch[base + off] = hi;
+        s->h_Bch[base + static_cast<size_t>(N) * TC_KCH + off] = lo;
+      }
+  }
   DevGP& G = s->G;
   G.M = M;
   G.Mp = Mp;
@@ -194,6 +253,8 @@ as_status upload_gp(as_space* s, cudaStream_t st) {
   if ((r = cp(s->d_O64, s->h_O64.data(), s->h_O64.size() * 8)) != AS_OK) return r;
   if ((r = cp(s->d_alpha64, s->h_alpha64.data(), s->h_alpha64.size() * 8)) != AS_OK) return r;
   if ((r = cp(s->d_W64, s->h_W64.data(), s->h_W64.size() * 8)) != AS_OK) return r;
+  if ((r = cp(s->d_Bch, s->h_Bch.data(), s->h_Bch.size() * 4)) != AS_OK) return r;
+  s->tb.chunks = s->d_Bch;
   CUDA_TRY(cudaStreamSynchronize(st));  // staging vectors may be reused by the next observe()
   G.O = s->d_O;
   G.alpha = s->d_alpha;
@@ -224,15 +285,24 @@ as_status ensure_lists(as_space* s, int grid) {
 
 as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStream_t st) {
   const bool gp = (a.acq != AS_ACQ_SIM) && s->G.M > 0;
+  const bool use_tc = gp && (s->path == 2 || (s->path == 0 && s->G.M >= 64));
   const int P = next_pow2_h(s->KC + SCORE_THREADS);
-  const size_t smem = score_smem_bytes(gp ? s->G.Mp : 0, gp ? s->G.DP : 0, s->H.d, P);
+  size_t smem = 0;
+  if (use_tc) {
+    smem = tc_smem_bytes(s->tb.Mp16, s->G.DP, s->H.d, P);
+  } else {
+    smem = score_smem_bytes(gp ? s->G.Mp : 0, gp ? s->G.DP : 0, s->H.d, P);
+  }
   if (smem > static_cast<size_t>(s->smem_optin))
     return fail(AS_ERR_CAPACITY, "score kernel shared memory exceeds the per-CTA limit (M or k too large)");
   const uint64_t ntiles = (a.count + SCORE_THREADS - 1) / SCORE_THREADS;
   int grid = 0;
   if (a.count > 0) {
     int occ = 1;
-    if (gp) {
+    if (use_tc) {
+      CUDA_TRY(cudaFuncSetAttribute(score_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      occ = 1;
+    } else if (gp) {
       CUDA_TRY(cudaFuncSetAttribute(score_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, score_kernel<true>, SCORE_THREADS, smem));
     } else {
@@ -245,6 +315,14 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
   }
   as_status r = ensure_lists(s, std::max(grid, 1));
   if (r != AS_OK) return r;
+  if (use_tc && a.d_scores && a.acq == AS_ACQ_EI) {
+    const size_t need = static_cast<size_t>(std::max(grid, 1)) * TC_EPI_WARPS * std::max(s->tb.Mp16, 1);
+    if (need > s->scratch_cap) {
+      if (s->d_scratch) cudaFree(s->d_scratch);
+      CUDA_TRY(cudaMalloc(&s->d_scratch, need * sizeof(double)));
+      s->scratch_cap = need;
+    }
+  }
   BatchArgs A{};
   A.mode = a.mode;
   A.acq = a.acq;
@@ -260,8 +338,15 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
   DevGP G = s->G;
   if (s->timing) CUDA_TRY(cudaEventRecord(s->ev[0], st));
   if (grid > 0) {
-    if (gp) score_kernel<true><<<grid, SCORE_THREADS, smem, st>>>(s->D, G, A, out);
-    else score_kernel<false><<<grid, SCORE_THREADS, smem, st>>>(s->D, G, A, out);
+    if (use_tc) {
+      TcB tb = s->tb;
+      tb.scratch = s->d_scratch;
+      score_tc_kernel<<<grid, TC_THREADS, smem, st>>>(s->D, G, A, out, tb);
+    } else if (gp) {
+      score_kernel<true><<<grid, SCORE_THREADS, smem, st>>>(s->D, G, A, out);
+    } else {
+      score_kernel<false><<<grid, SCORE_THREADS, smem, st>>>(s->D, G, A, out);
+    }
     CUDA_TRY(cudaGetLastError());
     ++s->n_launches;
   }
@@ -425,6 +510,9 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
     if ((r = dalloc(&s->d_O64, static_cast<size_t>(Mc) * H.d, s->owned)) != AS_OK) return cleanup(r);
     if ((r = dalloc(&s->d_alpha64, Mc, s->owned)) != AS_OK) return cleanup(r);
     if ((r = dalloc(&s->d_W64, static_cast<size_t>(Mc) * Mc, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = dalloc(&s->d_Bch, static_cast<size_t>(2) * TC_KCH * (Mc / TC_KCH) * (Mc / TC_KCH + 1) / 2 * TC_KCH,
+                    s->owned)) != AS_OK)
+      return cleanup(r);
     // pool buffers at capacity
     s->KC_max = KC_CAP;
     if ((r = dalloc(&s->d_pool, KC_CAP, s->owned)) != AS_OK) return cleanup(r);
@@ -451,6 +539,7 @@ void autoscout_space_destroy(as_space* s) {
     if (s->d_lists) cudaFree(s->d_lists);
     if (s->d_counts) cudaFree(s->d_counts);
     if (s->d_drops) cudaFree(s->d_drops);
+    if (s->d_scratch) cudaFree(s->d_scratch);
     for (auto& e : s->ev)
       if (e) cudaEventDestroy(e);
   }
@@ -698,6 +787,12 @@ as_status autoscout_mask_range(as_space* s, uint64_t raw_begin, uint64_t count, 
       s->D, raw_begin, count, d_bits, d_valid_count);
   CUDA_TRY(cudaGetLastError());
   ++s->n_launches;
+  return AS_OK;
+}
+
+as_status autoscout_set_path(as_space* s, int32_t path) {
+  if (!s || path < 0 || path > 2) return fail(AS_ERR_INVALID_ARG, "path must be 0 (auto), 1 (SIMT) or 2 (tensor cores)");
+  s->path = path;
   return AS_OK;
 }
 

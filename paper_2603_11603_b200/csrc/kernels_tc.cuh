@@ -1,0 +1,516 @@
+// Tensor-core score kernel: the posterior contraction v = L^-1 k of 128-candidate
+// tiles on tcgen05 (kind::tf32, 3xTF32 split, FP32 accumulators in TMEM), fed by SIMT producer
+// warps that generate candidates from indices and compute the cross-covariance tile.
+//
+// Warp roles (448 threads, 1 CTA per SM):
+//   warps 0-3   epilogue: TMEM -> registers, ||v||^2, mu, FP64 acquisition + bound, CTA top-k'
+//   warps 4-11  producers: decode + mask + simulator -> queue of valid candidates -> per tile of
+//               128: k(x_c, o_j) in K-chunks of 16 observed points, split into TF32 hi/lo and
+//               written in the K-major core-matrix layout of the A operand (3-stage ring)
+//   warp 12     MMA issuer (one thread): per K-chunk c, 3 MMAs x 2 k-steps into D[:, 16c : Mp)
+//               (triangular skipping: L^-1 has no entries above the diagonal)
+//   warp 13     loader (one thread): bulk async copies of the L^-1^T hi/lo chunks (B operand),
+//               pre-laid-out on the host, into a 3-stage ring
+// Synchronisation: mbarriers only (named barriers inside the producer and epilogue groups).
+#pragma once
+#include "kernels.cuh"
+#include "tc_ptx.cuh"
+
+namespace as {
+
+constexpr int TC_EPI_WARPS = 4;
+constexpr int TC_PROD_WARPS = 8;
+constexpr int TC_PROD_THREADS = TC_PROD_WARPS * 32;
+constexpr int TC_THREADS = (TC_EPI_WARPS + TC_PROD_WARPS + 2) * 32;
+constexpr int TC_MMA_WARP = TC_EPI_WARPS + TC_PROD_WARPS;
+constexpr int TC_LOAD_WARP = TC_MMA_WARP + 1;
+constexpr int TC_ROWS = 128;  // candidates per tile = TMEM lanes
+constexpr int TC_KCH = 16;    // observed points per K-chunk
+constexpr int TC_NA = 3;      // A ring stages
+constexpr int TC_NB = 3;      // B ring stages
+constexpr int TC_TI = 4;      // tile-info / meta ring
+constexpr int TC_QCAP = 384;  // 127 leftover + 256 new
+constexpr int TC_MAXCH = MMAX / TC_KCH;
+
+struct TcB {
+  const float* chunks;          // all chunks back to back: [hi (N_c x 16)][lo (N_c x 16)] per chunk
+  uint32_t off[TC_MAXCH];       // float offset of chunk c
+  int nch;                      // Mp16 / 16
+  int Mp16;                     // M padded to 16
+  double* scratch;              // [grid][4][Mp16] FP64 scratch of the sensitive-output fallback
+};
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// CTA-group top-k' admission among `n` threads synchronised by named barrier `id`.
+__device__ __forceinline__ void group_bitonic(uint64_t* arr, int n_el, int t, int nt, int id) {
+  for (int k = 2; k <= n_el; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = t; i < (n_el >> 1); i += nt) {
+        const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+        const int hi = lo | j;
+        const bool asc = (lo & k) == 0;
+        const uint64_t a = arr[lo], b = arr[hi];
+        if ((a > b) == asc) {
+          arr[lo] = b;
+          arr[hi] = a;
+        }
+      }
+      named_sync(id, nt);
+    }
+}
+
+__device__ __forceinline__ void group_admit(uint64_t key, uint64_t* arr, TopkSmem& ts, int KC, int t, int nt, int id) {
+  if (key != KEY_NONE) {
+    if (key < ts.tau) {
+      const int pos = atomicAdd(&ts.n_add, 1);
+      arr[ts.n_list + pos] = key;
+    } else {
+      atomicMin(reinterpret_cast<unsigned long long*>(&ts.drop), static_cast<unsigned long long>(key));
+    }
+  }
+  named_sync(id, nt);
+  const int n_add = ts.n_add;
+  if (n_add > 0) {
+    const int n_tot = ts.n_list + n_add;
+    group_bitonic(arr, next_pow2(n_tot < 2 ? 2 : n_tot), t, nt, id);
+    const int keep = n_tot < KC ? n_tot : KC;
+    if (t == 0) {
+      if (n_tot > KC && arr[KC] < ts.drop) ts.drop = arr[KC];
+      ts.n_list = keep;
+      ts.tau = (keep == KC) ? arr[KC - 1] : KEY_NONE;
+      ts.n_add = 0;
+    }
+    for (int i = keep + t; i < n_tot; i += nt) arr[i] = KEY_NONE;
+    named_sync(id, nt);
+  }
+}
+
+struct TcSmem {
+  float* Ahi[TC_NA];
+  float* Alo[TC_NA];
+  float* B[TC_NB];          // hi then lo
+  float* O;                 // [Mp16][DP]
+  float* alpha;
+  float* aabs;
+  float* xt;
+  DV* q_dv;
+  double* q_m0;
+  uint32_t* q_cvi;
+  uint32_t* q_j;
+  uint32_t* m_cvi;          // [TI][128]
+  uint32_t* m_j;
+  double* m_m0;
+  float* m_part;            // [TI][3][2][128]  mu, sb, kk partials of the two j-halves
+  uint64_t* arr;            // top-k' [P]
+  uint64_t* bars;           // mbarriers
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ TopkSmem ts;
+  __shared__ int q_n;
+  __shared__ int tinfo[TC_TI];
+  __shared__ uint32_t tmem_base;
+  __shared__ unsigned long long valid_cta;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int Mp16 = TB.Mp16, DP = G.DP, nch = TB.nch;
+  const uint32_t a_stage_bytes = TC_ROWS * TC_KCH * 4;          // per split
+  const uint32_t b_stage_bytes = 2u * Mp16 * TC_KCH * 4;         // hi + lo at the widest chunk
+  TcSmem sm;
+  unsigned char* p = smem_raw;
+  auto take = [&](size_t bytes) {
+    unsigned char* r = p;
+    p += (bytes + 127) & ~size_t(127);
+    return r;
+  };
+  for (int s = 0; s < TC_NA; ++s) {
+    sm.Ahi[s] = reinterpret_cast<float*>(take(a_stage_bytes));
+    sm.Alo[s] = reinterpret_cast<float*>(take(a_stage_bytes));
+  }
+  for (int s = 0; s < TC_NB; ++s) sm.B[s] = reinterpret_cast<float*>(take(b_stage_bytes));
+  sm.O = reinterpret_cast<float*>(take(sizeof(float) * Mp16 * DP));
+  sm.alpha = reinterpret_cast<float*>(take(sizeof(float) * Mp16));
+  sm.aabs = reinterpret_cast<float*>(take(sizeof(float) * Mp16));
+  sm.xt = reinterpret_cast<float*>(take(sizeof(float) * S.d * VMAX));
+  sm.q_dv = reinterpret_cast<DV*>(take(sizeof(DV) * TC_QCAP));
+  sm.q_m0 = reinterpret_cast<double*>(take(sizeof(double) * TC_QCAP));
+  sm.q_cvi = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_QCAP));
+  sm.q_j = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_QCAP));
+  sm.m_cvi = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_TI * TC_ROWS));
+  sm.m_j = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_TI * TC_ROWS));
+  sm.m_m0 = reinterpret_cast<double*>(take(sizeof(double) * TC_TI * TC_ROWS));
+  sm.m_part = reinterpret_cast<float*>(take(sizeof(float) * TC_TI * 6 * TC_ROWS));
+  sm.arr = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * out.P));
+  sm.bars = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 32));
+  uint64_t* a_full = sm.bars;                 // [NA] count 8 (producer warps)
+  uint64_t* a_empty = a_full + TC_NA;         // [NA] count 1 (commit)
+  uint64_t* b_full = a_empty + TC_NA;         // [NB] count 1 + tx
+  uint64_t* b_empty = b_full + TC_NB;         // [NB] count 1 (commit)
+  uint64_t* d_full = b_empty + TC_NB;         // [2]  count 1 (commit)
+  uint64_t* d_empty = d_full + 2;             // [2]  count 128 (epilogue threads)
+  uint64_t* t_ready = d_empty + 2;            // [TI] count 1 (producer leader)
+  uint64_t* m_full = t_ready + TC_TI;         // [TI] count 8 (producer warps)
+
+  // ---- setup: stage observed set + tables, init barriers, allocate TMEM
+  for (int i = tid; i < Mp16 * DP; i += TC_THREADS) sm.O[i] = (i < G.Mp * DP) ? __ldg(G.O + i) : 0.f;
+  for (int i = tid; i < Mp16; i += TC_THREADS) {
+    sm.alpha[i] = i < G.Mp ? __ldg(G.alpha + i) : 0.f;
+    sm.aabs[i] = i < G.Mp ? __ldg(G.aabs + i) : 0.f;
+  }
+  for (int i = tid; i < S.d * VMAX; i += TC_THREADS) sm.xt[i] = __ldg(S.xt32 + i);
+  for (int i = tid; i < out.P; i += TC_THREADS) sm.arr[i] = KEY_NONE;
+  if (tid == 0) {
+    for (int s = 0; s < TC_NA; ++s) {
+      tc::mbar_init(a_full + s, TC_PROD_WARPS);
+      tc::mbar_init(a_empty + s, 1);
+    }
+    for (int s = 0; s < TC_NB; ++s) {
+      tc::mbar_init(b_full + s, 1);
+      tc::mbar_init(b_empty + s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(d_full + s, 1);
+      tc::mbar_init(d_empty + s, TC_EPI_WARPS * 32);
+    }
+    for (int s = 0; s < TC_TI; ++s) {
+      tc::mbar_init(t_ready + s, 1);
+      tc::mbar_init(m_full + s, TC_PROD_WARPS);
+    }
+    tc::mbar_fence_init();
+    ts.n_list = 0;
+    ts.n_add = 0;
+    ts.tau = KEY_NONE;
+    ts.drop = KEY_NONE;
+    q_n = 0;
+    valid_cta = 0;
+  }
+  const uint32_t tmem_cols = (2 * Mp16 <= 256) ? 256u : 512u;
+  if (warp == 0) tc::tmem_alloc(&tmem_base, tmem_cols);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = tmem_base;
+
+  if (warp >= TC_EPI_WARPS && warp < TC_MMA_WARP) {
+    // =========================================================== producers
+    const int pt = tid - TC_EPI_WARPS * 32;          // 0..255
+    const int cand = pt & (TC_ROWS - 1);
+    const int half = pt >> 7;                        // which 8 observed points of a chunk
+    const uint64_t ntiles = (A.count + TC_PROD_THREADS - 1) / TC_PROD_THREADS;
+    uint32_t g = 0;                                   // global A-chunk counter
+    int t = 0;                                        // tile counter
+    int head = 0;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      // ---- phase 0: index -> configuration -> validity -> simulator -> queue
+      const uint64_t j = tile * TC_PROD_THREADS + pt;
+      const bool in = j < A.count;
+      bool ok = false;
+      if (in) {
+        const uint64_t pcvi = (A.mode == 0) ? A.begin + j : feistel_pi(A.fk, A.begin + j);
+        DV dv;
+        uint32_t act;
+        uint64_t raw;
+        decode_dev(S, pcvi, dv, act, raw);
+        double cost;
+        sim_dev(S, dv, act, cost, ok);
+        if (A.d_raw) A.d_raw[j] = raw;
+        if (!ok && A.d_scores) A.d_scores[j] = -INFINITY;
+        if (ok) {
+          const int slot = atomicAdd(&q_n, 1);
+          sm.q_dv[slot] = dv;
+          sm.q_m0[slot] = log(cost);
+          sm.q_cvi[slot] = static_cast<uint32_t>(pcvi);
+          sm.q_j[slot] = static_cast<uint32_t>(j);
+        }
+      }
+      const unsigned vb = __ballot_sync(0xffffffffu, in && ok);
+      if (lane == 0 && vb) atomicAdd(&valid_cta, static_cast<unsigned long long>(__popc(vb)));
+      named_sync(1, TC_PROD_THREADS);
+      const bool last_tile = tile + gridDim.x >= ntiles;
+      head = 0;
+      while (true) {
+        const int avail = q_n - head;
+        const int n = avail >= TC_ROWS ? TC_ROWS : (last_tile ? avail : 0);
+        if (n <= 0) break;
+        // ---- publish tile t: meta + tile info
+        const int ts_ = t % TC_TI;
+        if (pt < TC_ROWS && pt < n) {
+          sm.m_cvi[ts_ * TC_ROWS + pt] = sm.q_cvi[head + pt];
+          sm.m_j[ts_ * TC_ROWS + pt] = sm.q_j[head + pt];
+          sm.m_m0[ts_ * TC_ROWS + pt] = sm.q_m0[head + pt];
+        }
+        float x[DMAX];
+#pragma unroll
+        for (int f = 0; f < DMAX; ++f) x[f] = 0.f;
+        const bool has = cand < n;
+        if (has) {
+          const DV cdv = sm.q_dv[head + cand];
+#pragma unroll
+          for (int f = 0; f < DMAX; ++f)
+            if (f < S.d) x[f] = sm.xt[f * VMAX + dv_get(cdv, f)];
+        }
+        named_sync(1, TC_PROD_THREADS);
+        if (pt == 0) {
+          tinfo[ts_] = n;
+          tc::mbar_arrive(t_ready + ts_);
+        }
+        // ---- cross-covariance chunks -> A ring
+        float mu_p = 0.f, sb_p = 0.f, kk_p = 0.f;
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int s = g % TC_NA;
+          tc::mbar_wait(a_empty + s, ((g / TC_NA) & 1u) ^ 1u);
+          float kh[8], kl[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int jo = c * TC_KCH + half * 8 + q;
+            float kval = 0.f;
+            if (has && jo < G.M) {
+              const float4* o4 = reinterpret_cast<const float4*>(sm.O + jo * DP);
+              float r2 = 0.f;
+#pragma unroll
+              for (int f4 = 0; f4 < DMAX / 4; ++f4) {
+                if (4 * f4 < DP) {
+                  const float4 o = o4[f4];
+                  const float d0 = x[4 * f4] - o.x, d1 = x[4 * f4 + 1] - o.y, d2 = x[4 * f4 + 2] - o.z,
+                              d3 = x[4 * f4 + 3] - o.w;
+                  r2 = fmaf(d0, d0, r2);
+                  r2 = fmaf(d1, d1, r2);
+                  r2 = fmaf(d2, d2, r2);
+                  r2 = fmaf(d3, d3, r2);
+                }
+              }
+              float arg, poly;
+              if (G.kernel == 0) {
+                arg = 2.2360679774997896f * sqrtf(r2);
+                poly = fmaf(arg, fmaf(arg, 0.33333333333333333f, 1.0f), 1.0f);
+              } else {
+                arg = 0.5f * r2;
+                poly = 1.0f;
+              }
+              kval = G.sf2f * poly * __expf(-arg);
+              const float cc = kval * (1.0f + arg);
+              mu_p = fmaf(kval, sm.alpha[jo], mu_p);
+              sb_p = fmaf(cc, sm.aabs[jo], sb_p);
+              kk_p = fmaf(cc, cc, kk_p);
+            }
+            tc::split_tf32(kval, kh[q], kl[q]);
+          }
+          const uint32_t o0 = tc::kmajor_off(cand, half * 8, TC_KCH / 4) / 4;
+          const uint32_t o1 = tc::kmajor_off(cand, half * 8 + 4, TC_KCH / 4) / 4;
+          *reinterpret_cast<float4*>(sm.Ahi[s] + o0) = make_float4(kh[0], kh[1], kh[2], kh[3]);
+          *reinterpret_cast<float4*>(sm.Ahi[s] + o1) = make_float4(kh[4], kh[5], kh[6], kh[7]);
+          *reinterpret_cast<float4*>(sm.Alo[s] + o0) = make_float4(kl[0], kl[1], kl[2], kl[3]);
+          *reinterpret_cast<float4*>(sm.Alo[s] + o1) = make_float4(kl[4], kl[5], kl[6], kl[7]);
+          tc::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(a_full + s);
+        }
+        float* mp = sm.m_part + ts_ * 6 * TC_ROWS;
+        mp[(0 * 2 + half) * TC_ROWS + cand] = mu_p;
+        mp[(1 * 2 + half) * TC_ROWS + cand] = sb_p;
+        mp[(2 * 2 + half) * TC_ROWS + cand] = kk_p;
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(m_full + ts_);
+        head += n;
+        ++t;
+      }
+      // ---- compact the queue: leftovers (< 128) to the front
+      const int left = q_n - head;
+      named_sync(1, TC_PROD_THREADS);
+      DV mdv;
+      double mm0 = 0;
+      uint32_t mcvi = 0, mj = 0;
+      if (pt < left) {
+        mdv = sm.q_dv[head + pt];
+        mm0 = sm.q_m0[head + pt];
+        mcvi = sm.q_cvi[head + pt];
+        mj = sm.q_j[head + pt];
+      }
+      named_sync(1, TC_PROD_THREADS);
+      if (pt < left) {
+        sm.q_dv[pt] = mdv;
+        sm.q_m0[pt] = mm0;
+        sm.q_cvi[pt] = mcvi;
+        sm.q_j[pt] = mj;
+      }
+      if (pt == 0) q_n = left;
+      named_sync(1, TC_PROD_THREADS);
+    }
+    // ---- end of stream
+    if (pt == 0) {
+      const int ts_ = t % TC_TI;
+      tinfo[ts_] = -1;
+      tc::mbar_arrive(t_ready + ts_);
+    }
+  } else if (warp == TC_MMA_WARP) {
+    // =========================================================== MMA issuer
+    if (lane == 0) {
+      uint32_t ga = 0, gb = 0;
+      for (int t = 0;; ++t) {
+        const int ts_ = t % TC_TI;
+        tc::mbar_wait(t_ready + ts_, (t / TC_TI) & 1);
+        if (tinfo[ts_] < 0) break;
+        const int buf = t & 1;
+        tc::mbar_wait(d_empty + buf, ((t >> 1) & 1) ^ 1);
+        tc::fence_after_sync();
+        const uint32_t dcol = tmem + buf * Mp16;
+        for (int c = 0; c < nch; ++c, ++ga, ++gb) {
+          const int sa = ga % TC_NA, sbb = gb % TC_NB;
+          tc::mbar_wait(a_full + sa, (ga / TC_NA) & 1);
+          tc::mbar_wait(b_full + sbb, (gb / TC_NB) & 1);
+          tc::fence_after_sync();
+          const int N = Mp16 - c * TC_KCH;
+          const uint32_t idesc = tc::idesc_tf32(TC_ROWS, N);
+          const uint32_t a_h = tc::smem_u32(sm.Ahi[sa]), a_l = tc::smem_u32(sm.Alo[sa]);
+          const uint32_t b_h = tc::smem_u32(sm.B[sbb]);
+          const uint32_t b_l = b_h + N * TC_KCH * 4;
+          const uint32_t sbo = (TC_KCH / 4) * 128;
+#pragma unroll
+          for (int ks = 0; ks < TC_KCH / 8; ++ks) {
+            const uint64_t ah = tc::sdesc(a_h + 256 * ks, 128, sbo), al = tc::sdesc(a_l + 256 * ks, 128, sbo);
+            const uint64_t bh = tc::sdesc(b_h + 256 * ks, 128, sbo), bl = tc::sdesc(b_l + 256 * ks, 128, sbo);
+            const uint32_t d = dcol + c * TC_KCH;
+            tc::mma_tf32(d, ah, bh, idesc, (c > 0 || ks > 0) ? 1u : 0u);
+            tc::mma_tf32(d, ah, bl, idesc, 1u);
+            tc::mma_tf32(d, al, bh, idesc, 1u);
+          }
+          tc::mma_commit(a_empty + sa);
+          tc::mma_commit(b_empty + sbb);
+        }
+        tc::mma_commit(d_full + buf);
+      }
+    }
+    __syncwarp();
+  } else if (warp == TC_LOAD_WARP) {
+    // =========================================================== B loader
+    if (lane == 0) {
+      uint32_t gb = 0;
+      for (int t = 0;; ++t) {
+        const int ts_ = t % TC_TI;
+        tc::mbar_wait(t_ready + ts_, (t / TC_TI) & 1);
+        if (tinfo[ts_] < 0) break;
+        for (int c = 0; c < nch; ++c, ++gb) {
+          const int s = gb % TC_NB;
+          tc::mbar_wait(b_empty + s, ((gb / TC_NB) & 1u) ^ 1u);
+          const uint32_t bytes = 2u * (Mp16 - c * TC_KCH) * TC_KCH * 4;
+          tc::mbar_arrive_expect_tx(b_full + s, bytes);
+          tc::bulk_g2s(sm.B[s], TB.chunks + TB.off[c], bytes, b_full + s);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // =========================================================== epilogue (warps 0-3)
+    const int et = tid;                           // 0..127 = TMEM lane = row of the tile
+    double* scratch = TB.scratch + (static_cast<size_t>(blockIdx.x) * TC_EPI_WARPS + warp) * Mp16;
+    for (int t = 0;; ++t) {
+      const int ts_ = t % TC_TI;
+      tc::mbar_wait(t_ready + ts_, (t / TC_TI) & 1);
+      const int n = tinfo[ts_];
+      if (n < 0) break;
+      const int buf = t & 1;
+      tc::mbar_wait(d_full + buf, (t >> 1) & 1);
+      tc::fence_after_sync();
+      float vsq = 0.f;
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + buf * Mp16;
+      for (int c = 0; c < Mp16; c += 16) {
+        float v[16];
+        tc::tmem_ld16(taddr + c, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) vsq = fmaf(v[i], v[i], vsq);
+      }
+      tc::fence_before_sync();
+      tc::mbar_arrive(d_empty + buf);
+      tc::mbar_wait(m_full + ts_, (t / TC_TI) & 1);
+      uint64_t key = KEY_NONE;
+      const bool has = et < n;
+      bool sensitive = false;
+      if (has) {
+        const float* mp = sm.m_part + ts_ * 6 * TC_ROWS;
+        const float mu32 = mp[0 * TC_ROWS + et] + mp[1 * TC_ROWS + et];
+        const float sb = mp[2 * TC_ROWS + et] + mp[3 * TC_ROWS + et];
+        const float kk = mp[4 * TC_ROWS + et] + mp[5 * TC_ROWS + et];
+        const double cm0 = sm.m_m0[ts_ * TC_ROWS + et];
+        const double mu = cm0 + G.b + static_cast<double>(mu32);
+        const double vs = static_cast<double>(vsq);
+        const double s2 = G.sf2 - vs;
+        // FP32 SIMT k + 3xTF32 contraction: error coefficient 8x the SIMT one
+        const double eps = 8.0 * G.eps;
+        const double d_mu = eps * static_cast<double>(sb) + 1e-13 * fabs(mu);
+        const double ew = eps * G.w_fro;
+        const double kn = sqrt(static_cast<double>(kk));
+        const double d_s2 = 2.5 * ew * sqrt(vs) * kn + ew * ew * static_cast<double>(kk) + eps * vs +
+                            4.0 * static_cast<double>(U32) * G.sf2;
+        const double sc = acquisition(A.acq, mu, s2, cm0, G.fstar, A.xi, A.kappa);
+        double ub = acquisition(A.acq, mu - d_mu, s2 + d_s2, cm0, G.fstar, A.xi, A.kappa);
+        ub += 1e-12 * fmax(1.0, fabs(ub));
+        if (A.d_scores && A.acq == 0) {
+          if (s2 > 0.0) {
+            const double sg = sqrt(s2), z = (G.fstar - mu - A.xi) / sg;
+            if (z >= -3.2) {
+              const double Phi = 0.5 * erfc(-z * INV_SQRT2);
+              const double h = exp(-0.5 * z * z) * INV_SQRT_2PI + z * Phi;
+              const double uu = static_cast<double>(U32);
+              const double e_s = (1.0 - z * Phi / h) / (2.0 * s2) * 160.0 * uu * vs +
+                                 Phi / (sg * h) * uu * (1.0 + static_cast<double>(sb));
+              sensitive = e_s > 5e-6;
+            }
+          } else {
+            sensitive = true;
+          }
+        }
+        if (!sensitive) {
+          if (A.d_scores) A.d_scores[sm.m_j[ts_ * TC_ROWS + et]] = static_cast<float>(sc);
+          if (ub > -INFINITY) key = make_key(__double2float_ru(ub), sm.m_cvi[ts_ * TC_ROWS + et]);
+        }
+      }
+      // warp-cooperative FP64 posterior for flagged rows of this warp
+      unsigned fl = __ballot_sync(0xffffffffu, sensitive);
+      while (fl) {
+        const int src = __ffs(fl) - 1;
+        fl &= fl - 1;
+        const int row = warp * 32 + src;
+        const uint32_t cvi = sm.m_cvi[ts_ * TC_ROWS + row];
+        DV dv;
+        uint32_t act;
+        uint64_t raw;
+        decode_dev(S, cvi, dv, act, raw);
+        double kalpha, vq;
+        posterior64_warp(S, G, dv, lane, scratch, kalpha, vq);
+        if (lane == src) {
+          const double cm0 = sm.m_m0[ts_ * TC_ROWS + row];
+          const double sc = acquisition(A.acq, cm0 + G.b + kalpha, G.sf2 - vq, cm0, G.fstar, A.xi, A.kappa);
+          const double ub = sc + 1e-12 * fmax(1.0, fabs(sc));
+          A.d_scores[sm.m_j[ts_ * TC_ROWS + row]] = static_cast<float>(sc);
+          if (ub > -INFINITY) key = make_key(__double2float_ru(ub), cvi);
+        }
+      }
+      group_admit(key, sm.arr, ts, out.KC, et, TC_EPI_WARPS * 32, 2);
+    }
+    // ---- CTA list
+    named_sync(2, TC_EPI_WARPS * 32);
+    const int n = ts.n_list;
+    uint64_t* dst = out.lists + static_cast<size_t>(blockIdx.x) * out.KC;
+    for (int i = et; i < n; i += TC_EPI_WARPS * 32) dst[i] = sm.arr[i];
+    if (et == 0) {
+      out.counts[blockIdx.x] = n;
+      out.drop[blockIdx.x] = ts.drop;
+    }
+  }
+  // ---- teardown
+  tc::fence_before_sync();
+  __syncthreads();
+  if (tid == 0 && valid_cta) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(out.valid), valid_cta);
+    if (A.d_valid_count) atomicAdd(reinterpret_cast<unsigned long long*>(A.d_valid_count), valid_cta);
+  }
+  if (warp == 0) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(tmem, tmem_cols);
+  }
+}
+
+}  // namespace as
