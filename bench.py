@@ -64,6 +64,24 @@ def flops_per_valid(M, d):
     return M * (3 * d + 10) + 2 * M + M * (M + 1) + 2 * M
 
 
+def split_flops(M, d):
+    """(SIMT flops, contraction flops) per valid candidate: the tensor-core path runs the
+    cross-covariance, mu and ||v||^2 on the FP32 pipe and v = L^-1 k (M(M+1)) on tcgen05."""
+    return M * (3 * d + 10) + 4 * M, M * (M + 1)
+
+
+def tf32_peak_tflops():
+    """TF32 dense peak = measured bf16 cuBLAS burst x nominal TF32/BF16 ratio (1.1/2.25 PFLOP/s,
+    B200_PROFILING.md); 3xTF32 delivers FP32-accurate products at one third of it."""
+    bf16 = 1691.9
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            bf16 = float(json.load(fh)["bf16_tflops"])
+    except Exception:
+        pass
+    return bf16 * 1.1 / 2.25
+
+
 def fp32_peak_tflops(sm_mhz, n_sm=148):
     """FP32 SIMT peak: 148 SMs x 128 FP32 lanes x 2 flops/FMA x clock."""
     return n_sm * 128 * 2 * sm_mhz * 1e6 / 1e12
@@ -303,11 +321,34 @@ def run_ours(args):
         sm_max = (clk or {}).get("sm_max_mhz") or 1965.0
         peak = fp32_peak_tflops(sm_max)
         achieved = fl / (score_ms * 1e-3) / 1e12 if score_ms > 0 else 0.0
+        f_simt, f_tc = split_flops(M, d)
+        tc_path = M >= 64
         traffic = None
         prof = os.path.join(ROOT, "profiles", "score_kernel_traffic.json")
         if os.path.exists(prof):
             with open(prof) as fh:
                 traffic = json.load(fh).get("dram_bytes_per_launch")
+        if tc_path:
+            simt_ach = f_simt * valid_per_step / (score_ms * 1e-3) / 1e12
+            tc_ach = f_tc * valid_per_step / (score_ms * 1e-3) / 1e12
+            tc_peak = tf32_peak_tflops() / 3.0
+            t_simt, t_tc = f_simt * valid_per_step / (peak * 1e12), f_tc * valid_per_step / (tc_peak * 1e12)
+            if t_tc >= t_simt:
+                bound, ach, pk, src = "tensor", tc_ach, tc_peak, "tcgen05 TF32 = measured bf16 x 1.1/2.25, /3 for 3xTF32"
+            else:
+                bound, ach, pk, src = "alu", simt_ach, peak, f"FP32 SIMT 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz"
+            roof = {"bound": bound, "kernel": "score_tc_kernel", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+                    "frac": ach / pk, "traffic": traffic, "kernel_ms": score_ms, "merge_ms": merge_ms,
+                    "kernel_share": score_ms / ms_per_step, "peak_source": src,
+                    "simt": {"flops_per_valid": f_simt, "achieved": simt_ach, "peak": peak, "frac": simt_ach / peak},
+                    "tensor": {"flops_per_valid": f_tc, "achieved": tc_ach, "peak": tc_peak, "frac": tc_ach / tc_peak},
+                    "t_bound_ms": 1e3 * max(t_simt, t_tc)}
+        else:
+            roof = {"bound": "alu", "kernel": "score_kernel", "achieved": achieved, "peak": peak,
+                    "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": traffic,
+                    "kernel_ms": score_ms, "merge_ms": merge_ms, "kernel_share": score_ms / ms_per_step,
+                    "flops_per_valid": flops_per_valid(M, d),
+                    "peak_source": f"FP32 SIMT 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz (guide unit counts)"}
         line = {
             "metric": METRIC, "value": count / (ms_per_step / 1e3), "unit": "candidates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -318,11 +359,7 @@ def run_ours(args):
                        "parallelism": f"dp{world} (candidate-range shards, one all-gather)",
                        "arith": "decode int; simulator + resource check + acquisition FP64; GP FP32; refine FP64"},
             "valid_per_s": valid_per_step_all / (ms_per_step / 1e3),
-            "roofline": {"bound": "alu", "kernel": "score_kernel", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": traffic,
-                         "kernel_ms": score_ms, "merge_ms": merge_ms, "kernel_share": score_ms / ms_per_step,
-                         "flops_per_valid": flops_per_valid(M, d),
-                         "peak_source": f"FP32 SIMT 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz (guide unit counts)"},
+            "roofline": roof,
             "e2e": {"value": count / (e2e_step_ms / 1e3), "unit": "candidates/s", "ms_per_step": e2e_step_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "observe(host arrays) + score_batch + topk(host outputs) via the C ABI"},

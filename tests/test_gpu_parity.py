@@ -26,22 +26,29 @@ if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 A = pytest.importorskip("paper_2603_11603_b200.autoscout")
 
-_CACHE = {}
+_ORC = {}
+_SPACES = {}
 
 
-def case(name, M, mode="range", begin=0, count=None, seed=0, obs_seed=0):
+def case(name, M, mode="range", begin=0, count=None, seed=0, obs_seed=0, path="auto"):
+    """Oracle records (cached per inputs) + a GPU space with the same observed set (cached per path)."""
     key = (name, M, mode, begin, count, seed, obs_seed)
-    if key not in _CACHE:
+    if key not in _ORC:
         o = oracle_space(name)
         raws, costs = observed(o, M, obs_seed)
         fit = run.observed_fit(o, raws, costs)
         n = o.n_cvi() - begin if count is None else count
         rec = oracle_records(o, fit, mode, begin, n, seed)
+        _ORC[key] = (o, fit, rec, (raws, costs), (mode, begin, n, seed))
+    o, fit, rec, (raws, costs), batch = _ORC[key]
+    skey = (name, M, obs_seed, path)
+    if skey not in _SPACES:
         sp = A.Space(space_path(name), 0)
         if M:
             sp.observe(raws, costs)
-        _CACHE[key] = (o, fit, rec, sp, (mode, begin, n, seed))
-    return _CACHE[key]
+        sp.set_path(path)
+        _SPACES[skey] = sp
+    return o, fit, rec, _SPACES[skey], batch
 
 
 def gpu_run(sp, batch, acq, kappa=None, k=32):
@@ -78,9 +85,10 @@ def test_full_space_sim_mask_raw(name, M):
     check_topk(top, oracle_topk(rec, ref, 32))
 
 
+@pytest.mark.parametrize("path", ["simt", "tc"])
 @pytest.mark.parametrize("name,M", FULL)
-def test_full_space_posterior(name, M):
-    o, fit, rec, sp, batch = case(name, M)
+def test_full_space_posterior(name, M, path):
+    o, fit, rec, sp, batch = case(name, M, path=path)
     s0, _, _, top0 = gpu_run(sp, batch, "lcb", kappa=0.0)
     s1, _, _, top1 = gpu_run(sp, batch, "lcb", kappa=1.0)
     v = rec["valid"]
@@ -94,9 +102,10 @@ def test_full_space_posterior(name, M):
     check_topk(top1, oracle_topk(rec, oracle_scores(o, fit, rec, "lcb", kappa=1.0), 32))
 
 
+@pytest.mark.parametrize("path", ["simt", "tc"])
 @pytest.mark.parametrize("name,M", FULL)
-def test_full_space_ei(name, M):
-    o, fit, rec, sp, batch = case(name, M)
+def test_full_space_ei(name, M, path):
+    o, fit, rec, sp, batch = case(name, M, path=path)
     sc, _, _, top = gpu_run(sp, batch, "ei")
     ref = oracle_scores(o, fit, rec, "ei")
     v = rec["valid"]
@@ -105,15 +114,17 @@ def test_full_space_ei(name, M):
     check_topk(top, oracle_topk(rec, ref, 32))
 
 
-@pytest.mark.parametrize("name,M,mode,begin,count,seed", [
-    ("C4", 256, "sample", 0, 1 << 16, 0),         # bench shape (M=256), 65,536 sampled candidates
-    ("C4", 64, "sample", 12345, 20000, 7),        # M at the 64 boundary
-    ("C4", 65, "range", 100_000_000, 30000, 0),   # M not a multiple of 4, ragged RANGE window
-    ("C5", 128, "range", 1_234_567, 50000, 0),    # C5 bench M, RANGE window
-    ("C5", 1, "sample", 0, 10000, 3),             # M = 1
+@pytest.mark.parametrize("name,M,mode,begin,count,seed,path", [
+    ("C4", 256, "sample", 0, 1 << 16, 0, "tc"),         # bench shape (M=256), 65,536 sampled candidates
+    ("C4", 256, "sample", 0, 1 << 16, 0, "simt"),       # same inputs, SIMT posterior
+    ("C4", 64, "sample", 12345, 20000, 7, "auto"),      # M at the 64 boundary (tensor cores)
+    ("C4", 65, "range", 100_000_000, 30000, 0, "auto"), # M not a multiple of 16, ragged RANGE window
+    ("C5", 128, "range", 1_234_567, 50000, 0, "auto"),  # C5 bench M, RANGE window
+    ("C5", 1, "sample", 0, 10000, 3, "auto"),           # M = 1 (SIMT)
+    ("C5", 1, "sample", 0, 10000, 3, "tc"),             # M = 1 on tensor cores (one 16-wide chunk)
 ])
-def test_large_space_windows(name, M, mode, begin, count, seed):
-    o, fit, rec, sp, batch = case(name, M, mode, begin, count, seed)
+def test_large_space_windows(name, M, mode, begin, count, seed, path):
+    o, fit, rec, sp, batch = case(name, M, mode, begin, count, seed, path=path)
     s0, rw, nv, top0 = gpu_run(sp, batch, "lcb", kappa=0.0)
     assert np.array_equal(rw, rec["raw"])
     assert np.array_equal(np.isfinite(s0), rec["valid"]) and nv == int(rec["valid"].sum())
