@@ -78,6 +78,7 @@ size_t tc_smem_bytes(int Mp16, int DP, int d, int P) {
   s += r128(sizeof(float) * TC_TI * 6 * TC_ROWS);
   s += r128(sizeof(uint64_t) * P);
   s += r128(sizeof(uint64_t) * 32);
+  s += r128(sizeof(uint64_t) * CI);
   return s;
 }
 

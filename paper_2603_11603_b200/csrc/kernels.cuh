@@ -109,6 +109,94 @@ __device__ __forceinline__ void decode_dev(const DevSpace& S, uint64_t p, DV& dv
   }
 }
 
+// Decode with a coarse SMEM index of the structure prefix array: cidx[k] = prefix[k * n_struct / CI]
+// (k < CI) brackets the structure before a short binary search in global memory.
+constexpr int CI = 256;
+__device__ __forceinline__ void decode_dev_idx(const DevSpace& S, const uint64_t* cidx, uint64_t p, DV& dv,
+                                               uint32_t& act, uint64_t& raw) {
+  const int ci_n = S.n_struct < CI ? S.n_struct : CI;
+  int a = 0, b = ci_n;                       // largest k with cidx[k] <= p
+  while (b - a > 1) {
+    const int mid = (a + b) >> 1;
+    if (cidx[mid] <= p) a = mid; else b = mid;
+  }
+  int lo = static_cast<int>((static_cast<long long>(a) * S.n_struct) / ci_n);
+  int hi = (b >= ci_n) ? S.n_struct : static_cast<int>((static_cast<long long>(b) * S.n_struct) / ci_n);
+  if (hi <= lo) hi = lo + 1;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(S.prefix + mid) <= p) lo = mid; else hi = mid;
+  }
+  uint32_t t = static_cast<uint32_t>(p - __ldg(S.prefix + lo));
+  const DV* sd = S.s_dv + lo;
+  dv.w[0] = __ldg(&sd->w[0]);
+  dv.w[1] = __ldg(&sd->w[1]);
+  dv.w[2] = __ldg(&sd->w[2]);
+  act = __ldg(S.s_act + lo);
+  raw = __ldg(S.s_raw + lo);
+  for (int c = S.n_comp - 1; c >= 0; --c) {
+    const uint2 oc = __ldg(S.s_oc + static_cast<size_t>(lo) * S.n_comp + c);
+    const uint32_t q = t / oc.y;
+    const uint32_t r = t - q * oc.y;
+    t = q;
+    const Tuple* tu = S.tuples + oc.x + r;
+    dv.w[0] |= __ldg(&tu->dv.w[0]);
+    dv.w[1] |= __ldg(&tu->dv.w[1]);
+    dv.w[2] |= __ldg(&tu->dv.w[2]);
+    act |= __ldg(&tu->act);
+    raw += __ldg(&tu->raw);
+  }
+}
+__device__ __forceinline__ void load_cidx(const DevSpace& S, uint64_t* cidx, int tid, int nthreads) {
+  const int ci_n = S.n_struct < CI ? S.n_struct : CI;
+  for (int k = tid; k < ci_n; k += nthreads)
+    cidx[k] = __ldg(S.prefix + static_cast<int>((static_cast<long long>(k) * S.n_struct) / ci_n));
+}
+
+// Packed FP32x2 helpers (FFMA2 / FADD2 on sm_100a): r^2 = sum_f (x_f - o_f)^2 two features at a time.
+__device__ __forceinline__ unsigned long long f2_pack(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2_unpack(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2_sub(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// r^2 between packed candidate features xp[DMAX/2] and an observed row o (DP floats, 16-byte aligned)
+__device__ __forceinline__ float r2_packed(const unsigned long long* xp, const float* o, int DP) {
+  unsigned long long acc0 = 0ull, acc1 = 0ull;
+  const ulonglong2* o2 = reinterpret_cast<const ulonglong2*>(o);
+#pragma unroll
+  for (int f4 = 0; f4 < DMAX / 4; ++f4) {
+    if (4 * f4 < DP) {
+      const ulonglong2 ov = o2[f4];
+      const unsigned long long d0 = f2_sub(xp[2 * f4], ov.x);
+      const unsigned long long d1 = f2_sub(xp[2 * f4 + 1], ov.y);
+      acc0 = f2_fma(d0, d0, acc0);
+      acc1 = f2_fma(d1, d1, acc1);
+    }
+  }
+  const float2 a = f2_unpack(acc0), b = f2_unpack(acc1);
+  return (a.x + b.x) + (a.y + b.y);
+}
+
 __device__ __forceinline__ void sim_dev(const DevSpace& S, const DV& dv, uint32_t act, double& cost, bool& ok) {
   Knobs k;
   k.act = 0;

@@ -104,6 +104,7 @@ struct TcSmem {
   float* m_part;            // [TI][3][2][128]  mu, sb, kk partials of the two j-halves
   uint64_t* arr;            // top-k' [P]
   uint64_t* bars;           // mbarriers
+  uint64_t* cidx;           // coarse structure index [CI]
 };
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -145,6 +146,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
   sm.m_part = reinterpret_cast<float*>(take(sizeof(float) * TC_TI * 6 * TC_ROWS));
   sm.arr = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * out.P));
   sm.bars = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 32));
+  sm.cidx = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * CI));
   uint64_t* a_full = sm.bars;                 // [NA] count 8 (producer warps)
   uint64_t* a_empty = a_full + TC_NA;         // [NA] count 1 (commit)
   uint64_t* b_full = a_empty + TC_NA;         // [NB] count 1 + tx
@@ -162,6 +164,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
   }
   for (int i = tid; i < S.d * VMAX; i += TC_THREADS) sm.xt[i] = __ldg(S.xt32 + i);
   for (int i = tid; i < out.P; i += TC_THREADS) sm.arr[i] = KEY_NONE;
+  load_cidx(S, sm.cidx, tid, TC_THREADS);
   if (tid == 0) {
     for (int s = 0; s < TC_NA; ++s) {
       tc::mbar_init(a_full + s, TC_PROD_WARPS);
@@ -213,7 +216,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
         DV dv;
         uint32_t act;
         uint64_t raw;
-        decode_dev(S, pcvi, dv, act, raw);
+        decode_dev_idx(S, sm.cidx, pcvi, dv, act, raw);
         double cost;
         sim_dev(S, dv, act, cost, ok);
         if (A.d_raw) A.d_raw[j] = raw;
@@ -242,15 +245,18 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
           sm.m_j[ts_ * TC_ROWS + pt] = sm.q_j[head + pt];
           sm.m_m0[ts_ * TC_ROWS + pt] = sm.q_m0[head + pt];
         }
-        float x[DMAX];
-#pragma unroll
-        for (int f = 0; f < DMAX; ++f) x[f] = 0.f;
+        unsigned long long xp[DMAX / 2];
         const bool has = cand < n;
-        if (has) {
-          const DV cdv = sm.q_dv[head + cand];
+        {
+          DV cdv;
+          cdv.w[0] = cdv.w[1] = cdv.w[2] = 0;
+          if (has) cdv = sm.q_dv[head + cand];
 #pragma unroll
-          for (int f = 0; f < DMAX; ++f)
-            if (f < S.d) x[f] = sm.xt[f * VMAX + dv_get(cdv, f)];
+          for (int f = 0; f < DMAX; f += 2) {
+            const float a = (has && f < S.d) ? sm.xt[f * VMAX + dv_get(cdv, f)] : 0.f;
+            const float b = (has && f + 1 < S.d) ? sm.xt[(f + 1) * VMAX + dv_get(cdv, f + 1)] : 0.f;
+            xp[f / 2] = f2_pack(a, b);
+          }
         }
         named_sync(1, TC_PROD_THREADS);
         if (pt == 0) {
@@ -268,23 +274,10 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
             const int jo = c * TC_KCH + half * 8 + q;
             float kval = 0.f;
             if (has && jo < G.M) {
-              const float4* o4 = reinterpret_cast<const float4*>(sm.O + jo * DP);
-              float r2 = 0.f;
-#pragma unroll
-              for (int f4 = 0; f4 < DMAX / 4; ++f4) {
-                if (4 * f4 < DP) {
-                  const float4 o = o4[f4];
-                  const float d0 = x[4 * f4] - o.x, d1 = x[4 * f4 + 1] - o.y, d2 = x[4 * f4 + 2] - o.z,
-                              d3 = x[4 * f4 + 3] - o.w;
-                  r2 = fmaf(d0, d0, r2);
-                  r2 = fmaf(d1, d1, r2);
-                  r2 = fmaf(d2, d2, r2);
-                  r2 = fmaf(d3, d3, r2);
-                }
-              }
+              const float r2 = r2_packed(xp, sm.O + jo * DP, DP);
               float arg, poly;
               if (G.kernel == 0) {
-                arg = 2.2360679774997896f * sqrtf(r2);
+                arg = 2.2360679774997896f * sqrt_approx(r2);
                 poly = fmaf(arg, fmaf(arg, 0.33333333333333333f, 1.0f), 1.0f);
               } else {
                 arg = 0.5f * r2;
