@@ -82,6 +82,18 @@ size_t tc_smem_bytes(int Mp16, int DP, int d, int P) {
   return s;
 }
 
+using TcKernelFn = void (*)(DevSpace, DevGP, BatchArgs, CtaOut, TcB);
+TcKernelFn tc_kernel_for(int DP) {
+  switch (DP / 4) {
+    case 1: return score_tc_kernel<1>;
+    case 2: return score_tc_kernel<2>;
+    case 3: return score_tc_kernel<3>;
+    case 4: return score_tc_kernel<4>;
+    case 5: return score_tc_kernel<5>;
+    default: return score_tc_kernel<6>;
+  }
+}
+
 // TF32 round-to-nearest (ties away), as cvt.rna.tf32.f32
 float tf32_rna(float x) {
   uint32_t u;
@@ -301,7 +313,8 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
   if (a.count > 0) {
     int occ = 1;
     if (use_tc) {
-      CUDA_TRY(cudaFuncSetAttribute(score_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      CUDA_TRY(cudaFuncSetAttribute(tc_kernel_for(s->G.DP), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
       occ = 1;
     } else if (gp) {
       CUDA_TRY(cudaFuncSetAttribute(score_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -342,7 +355,7 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
     if (use_tc) {
       TcB tb = s->tb;
       tb.scratch = s->d_scratch;
-      score_tc_kernel<<<grid, TC_THREADS, smem, st>>>(s->D, G, A, out, tb);
+      tc_kernel_for(s->G.DP)<<<grid, TC_THREADS, smem, st>>>(s->D, G, A, out, tb);
     } else if (gp) {
       score_kernel<true><<<grid, SCORE_THREADS, smem, st>>>(s->D, G, A, out);
     } else {

@@ -107,6 +107,8 @@ struct TcSmem {
   uint64_t* cidx;           // coarse structure index [CI]
 };
 
+// NF4 = feature width in float4 units (d padded to 4); compile-time so the r^2 loop has no guards.
+template <int NF4>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -245,14 +247,14 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
           sm.m_j[ts_ * TC_ROWS + pt] = sm.q_j[head + pt];
           sm.m_m0[ts_ * TC_ROWS + pt] = sm.q_m0[head + pt];
         }
-        unsigned long long xp[DMAX / 2];
+        unsigned long long xp[2 * NF4];
         const bool has = cand < n;
         {
           DV cdv;
           cdv.w[0] = cdv.w[1] = cdv.w[2] = 0;
           if (has) cdv = sm.q_dv[head + cand];
 #pragma unroll
-          for (int f = 0; f < DMAX; f += 2) {
+          for (int f = 0; f < 4 * NF4; f += 2) {
             const float a = (has && f < S.d) ? sm.xt[f * VMAX + dv_get(cdv, f)] : 0.f;
             const float b = (has && f + 1 < S.d) ? sm.xt[(f + 1) * VMAX + dv_get(cdv, f + 1)] : 0.f;
             xp[f / 2] = f2_pack(a, b);
@@ -265,16 +267,30 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
         }
         // ---- cross-covariance chunks -> A ring
         float mu_p = 0.f, sb_p = 0.f, kk_p = 0.f;
+        const uint32_t sO = tc::smem_u32(sm.O), sAl = tc::smem_u32(sm.alpha), sAa = tc::smem_u32(sm.aabs);
+        const uint32_t o0 = tc::kmajor_off(cand, half * 8, TC_KCH / 4), o1 = tc::kmajor_off(cand, half * 8 + 4, TC_KCH / 4);
+        const float hmask = has ? 1.0f : 0.0f;
         for (int c = 0; c < nch; ++c, ++g) {
           const int s = g % TC_NA;
           tc::mbar_wait(a_empty + s, ((g / TC_NA) & 1u) ^ 1u);
           float kh[8], kl[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const int jo = c * TC_KCH + half * 8 + q;
+            const int jo = c * TC_KCH + half * 8 + q;           // warp-uniform
             float kval = 0.f;
-            if (has && jo < G.M) {
-              const float r2 = r2_packed(xp, sm.O + jo * DP, DP);
+            if (jo < G.M) {
+              unsigned long long acc0 = 0ull, acc1 = 0ull;
+              const uint32_t orow = sO + static_cast<uint32_t>(jo * NF4 * 16);
+#pragma unroll
+              for (int f4 = 0; f4 < NF4; ++f4) {
+                unsigned long long ox, oy;
+                tc::lds_u64x2(orow + 16 * f4, ox, oy);
+                const unsigned long long d0 = f2_sub(xp[2 * f4], ox), d1 = f2_sub(xp[2 * f4 + 1], oy);
+                acc0 = f2_fma(d0, d0, acc0);
+                acc1 = f2_fma(d1, d1, acc1);
+              }
+              const float2 ra = f2_unpack(acc0), rb = f2_unpack(acc1);
+              const float r2 = (ra.x + rb.x) + (ra.y + rb.y);
               float arg, poly;
               if (G.kernel == 0) {
                 arg = 2.2360679774997896f * sqrt_approx(r2);
@@ -283,20 +299,19 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
                 arg = 0.5f * r2;
                 poly = 1.0f;
               }
-              kval = G.sf2f * poly * __expf(-arg);
+              kval = hmask * G.sf2f * poly * __expf(-arg);
               const float cc = kval * (1.0f + arg);
-              mu_p = fmaf(kval, sm.alpha[jo], mu_p);
-              sb_p = fmaf(cc, sm.aabs[jo], sb_p);
+              mu_p = fmaf(kval, tc::lds_f32(sAl + 4 * jo), mu_p);
+              sb_p = fmaf(cc, tc::lds_f32(sAa + 4 * jo), sb_p);
               kk_p = fmaf(cc, cc, kk_p);
             }
             tc::split_tf32(kval, kh[q], kl[q]);
           }
-          const uint32_t o0 = tc::kmajor_off(cand, half * 8, TC_KCH / 4) / 4;
-          const uint32_t o1 = tc::kmajor_off(cand, half * 8 + 4, TC_KCH / 4) / 4;
-          *reinterpret_cast<float4*>(sm.Ahi[s] + o0) = make_float4(kh[0], kh[1], kh[2], kh[3]);
-          *reinterpret_cast<float4*>(sm.Ahi[s] + o1) = make_float4(kh[4], kh[5], kh[6], kh[7]);
-          *reinterpret_cast<float4*>(sm.Alo[s] + o0) = make_float4(kl[0], kl[1], kl[2], kl[3]);
-          *reinterpret_cast<float4*>(sm.Alo[s] + o1) = make_float4(kl[4], kl[5], kl[6], kl[7]);
+          const uint32_t ah = tc::smem_u32(sm.Ahi[s]), al = tc::smem_u32(sm.Alo[s]);
+          tc::sts_f32x4(ah + o0, kh[0], kh[1], kh[2], kh[3]);
+          tc::sts_f32x4(ah + o1, kh[4], kh[5], kh[6], kh[7]);
+          tc::sts_f32x4(al + o0, kl[0], kl[1], kl[2], kl[3]);
+          tc::sts_f32x4(al + o1, kl[4], kl[5], kl[6], kl[7]);
           tc::fence_proxy_async();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(a_full + s);
@@ -383,11 +398,11 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
       uint32_t gb = 0;
       for (int t = 0;; ++t) {
         const int ts_ = t % TC_TI;
-        tc::mbar_wait(t_ready + ts_, (t / TC_TI) & 1);
+        tc::mbar_wait_backoff(t_ready + ts_, (t / TC_TI) & 1, 1024);
         if (tinfo[ts_] < 0) break;
         for (int c = 0; c < nch; ++c, ++gb) {
           const int s = gb % TC_NB;
-          tc::mbar_wait(b_empty + s, ((gb / TC_NB) & 1u) ^ 1u);
+          tc::mbar_wait_backoff(b_empty + s, ((gb / TC_NB) & 1u) ^ 1u, 256);
           const uint32_t bytes = 2u * (Mp16 - c * TC_KCH) * TC_KCH * 4;
           tc::mbar_arrive_expect_tx(b_full + s, bytes);
           tc::bulk_g2s(sm.B[s], TB.chunks + TB.off[c], bytes, b_full + s);
@@ -401,11 +416,11 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
     double* scratch = TB.scratch + (static_cast<size_t>(blockIdx.x) * TC_EPI_WARPS + warp) * Mp16;
     for (int t = 0;; ++t) {
       const int ts_ = t % TC_TI;
-      tc::mbar_wait(t_ready + ts_, (t / TC_TI) & 1);
+      tc::mbar_wait_backoff(t_ready + ts_, (t / TC_TI) & 1, 2048);
       const int n = tinfo[ts_];
       if (n < 0) break;
       const int buf = t & 1;
-      tc::mbar_wait(d_full + buf, (t >> 1) & 1);
+      tc::mbar_wait_backoff(d_full + buf, (t >> 1) & 1, 2048);
       tc::fence_after_sync();
       float vsq = 0.f;
       const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + buf * Mp16;
@@ -417,7 +432,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
       }
       tc::fence_before_sync();
       tc::mbar_arrive(d_empty + buf);
-      tc::mbar_wait(m_full + ts_, (t / TC_TI) & 1);
+      tc::mbar_wait_backoff(m_full + ts_, (t / TC_TI) & 1, 512);
       uint64_t key = KEY_NONE;
       const bool has = et < n;
       bool sensitive = false;
