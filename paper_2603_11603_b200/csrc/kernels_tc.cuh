@@ -2,35 +2,38 @@
 // tiles on tcgen05 (kind::tf32, 3xTF32 split, FP32 accumulators in TMEM), fed by SIMT producer
 // warps that generate candidates from indices and compute the cross-covariance tile.
 //
-// Warp roles (448 threads, 1 CTA per SM):
-//   warps 0-3   epilogue: TMEM -> registers, ||v||^2, mu, FP64 acquisition + bound, CTA top-k'
-//   warps 4-11  producers: decode + mask + simulator -> queue of valid candidates -> per tile of
-//               128: k(x_c, o_j) in K-chunks of 16 observed points, split into TF32 hi/lo and
-//               written in the K-major core-matrix layout of the A operand (3-stage ring)
-//   warp 12     MMA issuer (one thread): per K-chunk c, 3 MMAs x 2 k-steps into D[:, 16c : Mp)
-//               (triangular skipping: L^-1 has no entries above the diagonal)
-//   warp 13     loader (one thread): bulk async copies of the L^-1^T hi/lo chunks (B operand),
-//               pre-laid-out on the host, into a 3-stage ring
-// Synchronisation: mbarriers only (named barriers inside the producer and epilogue groups).
+// Warp roles (544 threads, 1 CTA per SM):
+//   warps 0-15  producers: decode + mask + simulator -> queue of valid candidates -> per tile of
+//               128: k(x_c, o_j) in K-chunks of 16 observed points (4 per thread), split into
+//               TF32 hi/lo and written in the K-major core-matrix layout of the A operand
+//               (3-stage ring); then the epilogue of the PREVIOUS tile (whose accumulator is
+//               complete by then): tcgen05.ld of their TMEM lane quadrant (warp % 4) and column
+//               quarter (warp / 4) -> ||v||^2 -> mu, FP64 acquisition + bound -> CTA top-k'.
+//   warp 16     MMA issuer + B loader (one thread): per K-chunk c, 3 MMAs x 2 k-steps into
+//               D[:, 16c : Mp16) (triangular skipping: L^-1 has no entries above the diagonal);
+//               bulk async copies of the host-pre-laid-out L^-1^T hi/lo chunks, 2 chunks ahead.
+// No warp is idle by design: idle-waiting warps were measured to steal issue slots from the
+// producers (profiles/r1_tc_*.md).
 #pragma once
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
 
 namespace as {
 
-constexpr int TC_EPI_WARPS = 4;
-constexpr int TC_PROD_WARPS = 8;
+constexpr int TC_PROD_WARPS = 16;
 constexpr int TC_PROD_THREADS = TC_PROD_WARPS * 32;
-constexpr int TC_THREADS = (TC_EPI_WARPS + TC_PROD_WARPS + 2) * 32;
-constexpr int TC_MMA_WARP = TC_EPI_WARPS + TC_PROD_WARPS;
-constexpr int TC_LOAD_WARP = TC_MMA_WARP + 1;
-constexpr int TC_ROWS = 128;  // candidates per tile = TMEM lanes
-constexpr int TC_KCH = 16;    // observed points per K-chunk
-constexpr int TC_NA = 3;      // A ring stages
-constexpr int TC_NB = 3;      // B ring stages
-constexpr int TC_TI = 4;      // tile-info / meta ring
-constexpr int TC_QCAP = 384;  // 127 leftover + 256 new
+constexpr int TC_THREADS = TC_PROD_THREADS + 32;
+constexpr int TC_MMA_WARP = TC_PROD_WARPS;
+constexpr int TC_ROWS = 128;                 // candidates per tile = TMEM lanes
+constexpr int TC_KCH = 16;                   // observed points per K-chunk
+constexpr int TC_JQ = TC_PROD_THREADS / TC_ROWS;   // producer threads per candidate (4)
+constexpr int TC_JPT = TC_KCH / TC_JQ;       // observed points per thread per chunk (4)
+constexpr int TC_NA = 3;                     // A ring stages
+constexpr int TC_NB = 3;                     // B ring stages
+constexpr int TC_TI = 2;                     // tile-info / meta slots
+constexpr int TC_QCAP = TC_ROWS - 1 + TC_PROD_THREADS;
 constexpr int TC_MAXCH = MMAX / TC_KCH;
+constexpr int TC_EPI_WARPS = 4;              // warps that finalise rows (rows 0..127)
 
 struct TcB {
   const float* chunks;          // all chunks back to back: [hi (N_c x 16)][lo (N_c x 16)] per chunk
@@ -42,7 +45,7 @@ struct TcB {
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// CTA-group top-k' admission among `n` threads synchronised by named barrier `id`.
+// Top-k' admission among the `nt` threads synchronised by named barrier `id`.
 __device__ __forceinline__ void group_bitonic(uint64_t* arr, int n_el, int t, int nt, int id) {
   for (int k = 2; k <= n_el; k <<= 1)
     for (int j = k >> 1; j > 0; j >>= 1) {
@@ -101,7 +104,8 @@ struct TcSmem {
   uint32_t* m_cvi;          // [TI][128]
   uint32_t* m_j;
   double* m_m0;
-  float* m_part;            // [TI][3][2][128]  mu, sb, kk partials of the two j-halves
+  float* m_part;            // [TI][3][JQ][128]  mu, sb, kk partials of the JQ observed-point groups
+  float* vpart;             // [4][128] ||v||^2 partials of the 4 column quarters
   uint64_t* arr;            // top-k' [P]
   uint64_t* bars;           // mbarriers
   uint64_t* cidx;           // coarse structure index [CI]
@@ -145,18 +149,18 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
   sm.m_cvi = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_TI * TC_ROWS));
   sm.m_j = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_TI * TC_ROWS));
   sm.m_m0 = reinterpret_cast<double*>(take(sizeof(double) * TC_TI * TC_ROWS));
-  sm.m_part = reinterpret_cast<float*>(take(sizeof(float) * TC_TI * 6 * TC_ROWS));
+  sm.m_part = reinterpret_cast<float*>(take(sizeof(float) * TC_TI * 3 * TC_JQ * TC_ROWS));
+  sm.vpart = reinterpret_cast<float*>(take(sizeof(float) * 4 * TC_ROWS));
   sm.arr = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * out.P));
   sm.bars = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 32));
   sm.cidx = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * CI));
-  uint64_t* a_full = sm.bars;                 // [NA] count 8 (producer warps)
+  uint64_t* a_full = sm.bars;                 // [NA] count 16 (producer warps)
   uint64_t* a_empty = a_full + TC_NA;         // [NA] count 1 (commit)
   uint64_t* b_full = a_empty + TC_NA;         // [NB] count 1 + tx
   uint64_t* b_empty = b_full + TC_NB;         // [NB] count 1 (commit)
   uint64_t* d_full = b_empty + TC_NB;         // [2]  count 1 (commit)
-  uint64_t* d_empty = d_full + 2;             // [2]  count 128 (epilogue threads)
+  uint64_t* d_empty = d_full + 2;             // [2]  count 16 (producer warps)
   uint64_t* t_ready = d_empty + 2;            // [TI] count 1 (producer leader)
-  uint64_t* m_full = t_ready + TC_TI;         // [TI] count 8 (producer warps)
 
   // ---- setup: stage observed set + tables, init barriers, allocate TMEM
   for (int i = tid; i < Mp16 * DP; i += TC_THREADS) sm.O[i] = (i < G.Mp * DP) ? __ldg(G.O + i) : 0.f;
@@ -178,12 +182,9 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(d_full + s, 1);
-      tc::mbar_init(d_empty + s, TC_EPI_WARPS * 32);
+      tc::mbar_init(d_empty + s, TC_PROD_WARPS);
     }
-    for (int s = 0; s < TC_TI; ++s) {
-      tc::mbar_init(t_ready + s, 1);
-      tc::mbar_init(m_full + s, TC_PROD_WARPS);
-    }
+    for (int s = 0; s < TC_TI; ++s) tc::mbar_init(t_ready + s, 1);
     tc::mbar_fence_init();
     ts.n_list = 0;
     ts.n_add = 0;
@@ -199,251 +200,51 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
   tc::fence_after_sync();
   const uint32_t tmem = tmem_base;
 
-  if (warp >= TC_EPI_WARPS && warp < TC_MMA_WARP) {
-    // =========================================================== producers
-    const int pt = tid - TC_EPI_WARPS * 32;          // 0..255
-    const int cand = pt & (TC_ROWS - 1);
-    const int half = pt >> 7;                        // which 8 observed points of a chunk
-    const uint64_t ntiles = (A.count + TC_PROD_THREADS - 1) / TC_PROD_THREADS;
-    uint32_t g = 0;                                   // global A-chunk counter
-    int t = 0;                                        // tile counter
-    int head = 0;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      // ---- phase 0: index -> configuration -> validity -> simulator -> queue
-      const uint64_t j = tile * TC_PROD_THREADS + pt;
-      const bool in = j < A.count;
-      bool ok = false;
-      if (in) {
-        const uint64_t pcvi = (A.mode == 0) ? A.begin + j : feistel_pi(A.fk, A.begin + j);
-        DV dv;
-        uint32_t act;
-        uint64_t raw;
-        decode_dev_idx(S, sm.cidx, pcvi, dv, act, raw);
-        double cost;
-        sim_dev(S, dv, act, cost, ok);
-        if (A.d_raw) A.d_raw[j] = raw;
-        if (!ok && A.d_scores) A.d_scores[j] = -INFINITY;
-        if (ok) {
-          const int slot = atomicAdd(&q_n, 1);
-          sm.q_dv[slot] = dv;
-          sm.q_m0[slot] = log(cost);
-          sm.q_cvi[slot] = static_cast<uint32_t>(pcvi);
-          sm.q_j[slot] = static_cast<uint32_t>(j);
-        }
-      }
-      const unsigned vb = __ballot_sync(0xffffffffu, in && ok);
-      if (lane == 0 && vb) atomicAdd(&valid_cta, static_cast<unsigned long long>(__popc(vb)));
-      named_sync(1, TC_PROD_THREADS);
-      const bool last_tile = tile + gridDim.x >= ntiles;
-      head = 0;
-      while (true) {
-        const int avail = q_n - head;
-        const int n = avail >= TC_ROWS ? TC_ROWS : (last_tile ? avail : 0);
-        if (n <= 0) break;
-        // ---- publish tile t: meta + tile info
-        const int ts_ = t % TC_TI;
-        if (pt < TC_ROWS && pt < n) {
-          sm.m_cvi[ts_ * TC_ROWS + pt] = sm.q_cvi[head + pt];
-          sm.m_j[ts_ * TC_ROWS + pt] = sm.q_j[head + pt];
-          sm.m_m0[ts_ * TC_ROWS + pt] = sm.q_m0[head + pt];
-        }
-        unsigned long long xp[2 * NF4];
-        const bool has = cand < n;
-        {
-          DV cdv;
-          cdv.w[0] = cdv.w[1] = cdv.w[2] = 0;
-          if (has) cdv = sm.q_dv[head + cand];
-#pragma unroll
-          for (int f = 0; f < 4 * NF4; f += 2) {
-            const float a = (has && f < S.d) ? sm.xt[f * VMAX + dv_get(cdv, f)] : 0.f;
-            const float b = (has && f + 1 < S.d) ? sm.xt[(f + 1) * VMAX + dv_get(cdv, f + 1)] : 0.f;
-            xp[f / 2] = f2_pack(a, b);
-          }
-        }
-        named_sync(1, TC_PROD_THREADS);
-        if (pt == 0) {
-          tinfo[ts_] = n;
-          tc::mbar_arrive(t_ready + ts_);
-        }
-        // ---- cross-covariance chunks -> A ring
-        float mu_p = 0.f, sb_p = 0.f, kk_p = 0.f;
-        const uint32_t sO = tc::smem_u32(sm.O), sAl = tc::smem_u32(sm.alpha), sAa = tc::smem_u32(sm.aabs);
-        const uint32_t o0 = tc::kmajor_off(cand, half * 8, TC_KCH / 4), o1 = tc::kmajor_off(cand, half * 8 + 4, TC_KCH / 4);
-        const float hmask = has ? 1.0f : 0.0f;
-        for (int c = 0; c < nch; ++c, ++g) {
-          const int s = g % TC_NA;
-          tc::mbar_wait(a_empty + s, ((g / TC_NA) & 1u) ^ 1u);
-          float kh[8], kl[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int jo = c * TC_KCH + half * 8 + q;           // warp-uniform
-            float kval = 0.f;
-            if (jo < G.M) {
-              unsigned long long acc0 = 0ull, acc1 = 0ull;
-              const uint32_t orow = sO + static_cast<uint32_t>(jo * NF4 * 16);
-#pragma unroll
-              for (int f4 = 0; f4 < NF4; ++f4) {
-                unsigned long long ox, oy;
-                tc::lds_u64x2(orow + 16 * f4, ox, oy);
-                const unsigned long long d0 = f2_sub(xp[2 * f4], ox), d1 = f2_sub(xp[2 * f4 + 1], oy);
-                acc0 = f2_fma(d0, d0, acc0);
-                acc1 = f2_fma(d1, d1, acc1);
-              }
-              const float2 ra = f2_unpack(acc0), rb = f2_unpack(acc1);
-              const float r2 = (ra.x + rb.x) + (ra.y + rb.y);
-              float arg, poly;
-              if (G.kernel == 0) {
-                arg = 2.2360679774997896f * sqrt_approx(r2);
-                poly = fmaf(arg, fmaf(arg, 0.33333333333333333f, 1.0f), 1.0f);
-              } else {
-                arg = 0.5f * r2;
-                poly = 1.0f;
-              }
-              kval = hmask * G.sf2f * poly * __expf(-arg);
-              const float cc = kval * (1.0f + arg);
-              mu_p = fmaf(kval, tc::lds_f32(sAl + 4 * jo), mu_p);
-              sb_p = fmaf(cc, tc::lds_f32(sAa + 4 * jo), sb_p);
-              kk_p = fmaf(cc, cc, kk_p);
-            }
-            tc::split_tf32(kval, kh[q], kl[q]);
-          }
-          const uint32_t ah = tc::smem_u32(sm.Ahi[s]), al = tc::smem_u32(sm.Alo[s]);
-          tc::sts_f32x4(ah + o0, kh[0], kh[1], kh[2], kh[3]);
-          tc::sts_f32x4(ah + o1, kh[4], kh[5], kh[6], kh[7]);
-          tc::sts_f32x4(al + o0, kl[0], kl[1], kl[2], kl[3]);
-          tc::sts_f32x4(al + o1, kl[4], kl[5], kl[6], kl[7]);
-          tc::fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(a_full + s);
-        }
-        float* mp = sm.m_part + ts_ * 6 * TC_ROWS;
-        mp[(0 * 2 + half) * TC_ROWS + cand] = mu_p;
-        mp[(1 * 2 + half) * TC_ROWS + cand] = sb_p;
-        mp[(2 * 2 + half) * TC_ROWS + cand] = kk_p;
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(m_full + ts_);
-        head += n;
-        ++t;
-      }
-      // ---- compact the queue: leftovers (< 128) to the front
-      const int left = q_n - head;
-      named_sync(1, TC_PROD_THREADS);
-      DV mdv;
-      double mm0 = 0;
-      uint32_t mcvi = 0, mj = 0;
-      if (pt < left) {
-        mdv = sm.q_dv[head + pt];
-        mm0 = sm.q_m0[head + pt];
-        mcvi = sm.q_cvi[head + pt];
-        mj = sm.q_j[head + pt];
-      }
-      named_sync(1, TC_PROD_THREADS);
-      if (pt < left) {
-        sm.q_dv[pt] = mdv;
-        sm.q_m0[pt] = mm0;
-        sm.q_cvi[pt] = mcvi;
-        sm.q_j[pt] = mj;
-      }
-      if (pt == 0) q_n = left;
-      named_sync(1, TC_PROD_THREADS);
-    }
-    // ---- end of stream
-    if (pt == 0) {
-      const int ts_ = t % TC_TI;
-      tinfo[ts_] = -1;
-      tc::mbar_arrive(t_ready + ts_);
-    }
-  } else if (warp == TC_MMA_WARP) {
-    // =========================================================== MMA issuer
-    if (lane == 0) {
-      uint32_t ga = 0, gb = 0;
-      for (int t = 0;; ++t) {
-        const int ts_ = t % TC_TI;
-        tc::mbar_wait(t_ready + ts_, (t / TC_TI) & 1);
-        if (tinfo[ts_] < 0) break;
-        const int buf = t & 1;
-        tc::mbar_wait(d_empty + buf, ((t >> 1) & 1) ^ 1);
-        tc::fence_after_sync();
-        const uint32_t dcol = tmem + buf * Mp16;
-        for (int c = 0; c < nch; ++c, ++ga, ++gb) {
-          const int sa = ga % TC_NA, sbb = gb % TC_NB;
-          tc::mbar_wait(a_full + sa, (ga / TC_NA) & 1);
-          tc::mbar_wait(b_full + sbb, (gb / TC_NB) & 1);
-          tc::fence_after_sync();
-          const int N = Mp16 - c * TC_KCH;
-          const uint32_t idesc = tc::idesc_tf32(TC_ROWS, N);
-          const uint32_t a_h = tc::smem_u32(sm.Ahi[sa]), a_l = tc::smem_u32(sm.Alo[sa]);
-          const uint32_t b_h = tc::smem_u32(sm.B[sbb]);
-          const uint32_t b_l = b_h + N * TC_KCH * 4;
-          const uint32_t sbo = (TC_KCH / 4) * 128;
-#pragma unroll
-          for (int ks = 0; ks < TC_KCH / 8; ++ks) {
-            const uint64_t ah = tc::sdesc(a_h + 256 * ks, 128, sbo), al = tc::sdesc(a_l + 256 * ks, 128, sbo);
-            const uint64_t bh = tc::sdesc(b_h + 256 * ks, 128, sbo), bl = tc::sdesc(b_l + 256 * ks, 128, sbo);
-            const uint32_t d = dcol + c * TC_KCH;
-            tc::mma_tf32(d, ah, bh, idesc, (c > 0 || ks > 0) ? 1u : 0u);
-            tc::mma_tf32(d, ah, bl, idesc, 1u);
-            tc::mma_tf32(d, al, bh, idesc, 1u);
-          }
-          tc::mma_commit(a_empty + sa);
-          tc::mma_commit(b_empty + sbb);
-        }
-        tc::mma_commit(d_full + buf);
-      }
-    }
-    __syncwarp();
-  } else if (warp == TC_LOAD_WARP) {
-    // =========================================================== B loader
-    if (lane == 0) {
-      uint32_t gb = 0;
-      for (int t = 0;; ++t) {
-        const int ts_ = t % TC_TI;
-        tc::mbar_wait_backoff(t_ready + ts_, (t / TC_TI) & 1, 1024);
-        if (tinfo[ts_] < 0) break;
-        for (int c = 0; c < nch; ++c, ++gb) {
-          const int s = gb % TC_NB;
-          tc::mbar_wait_backoff(b_empty + s, ((gb / TC_NB) & 1u) ^ 1u, 256);
-          const uint32_t bytes = 2u * (Mp16 - c * TC_KCH) * TC_KCH * 4;
-          tc::mbar_arrive_expect_tx(b_full + s, bytes);
-          tc::bulk_g2s(sm.B[s], TB.chunks + TB.off[c], bytes, b_full + s);
-        }
-      }
-    }
-    __syncwarp();
-  } else {
-    // =========================================================== epilogue (warps 0-3)
-    const int et = tid;                           // 0..127 = TMEM lane = row of the tile
-    double* scratch = TB.scratch + (static_cast<size_t>(blockIdx.x) * TC_EPI_WARPS + warp) * Mp16;
-    for (int t = 0;; ++t) {
-      const int ts_ = t % TC_TI;
-      tc::mbar_wait_backoff(t_ready + ts_, (t / TC_TI) & 1, 2048);
-      const int n = tinfo[ts_];
-      if (n < 0) break;
-      const int buf = t & 1;
-      tc::mbar_wait_backoff(d_full + buf, (t >> 1) & 1, 2048);
+  if (warp < TC_PROD_WARPS) {
+    // =========================================================== producers (+ epilogue)
+    const int pt = tid;                              // 0..511
+    const int cand = pt & (TC_ROWS - 1);             // candidate row of the tile
+    const int jq = pt >> 7;                          // observed-point group of a chunk (warp-uniform)
+    const int quad = warp & 3, cq = warp >> 2;       // TMEM lane quadrant / column quarter (epilogue)
+    const uint32_t sO = tc::smem_u32(sm.O), sAl = tc::smem_u32(sm.alpha), sAa = tc::smem_u32(sm.aabs);
+    const uint32_t a_off = tc::kmajor_off(cand, jq * TC_JPT, TC_KCH / 4);
+    double* scratch = TB.scratch + (static_cast<size_t>(blockIdx.x) * TC_EPI_WARPS + (warp & 3)) * Mp16;
+
+    // Epilogue of tile u: ||v||^2 from TMEM, then row finalisation + admission (all 512 threads).
+    auto epilogue = [&](int u) {
+      const int us = u % TC_TI, buf = u & 1;
+      tc::mbar_wait(d_full + buf, (u >> 1) & 1);
       tc::fence_after_sync();
       float vsq = 0.f;
-      const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + buf * Mp16;
-      for (int c = 0; c < Mp16; c += 16) {
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(quad * 32) << 16) + buf * Mp16;
+      for (int c = cq * 16; c < Mp16; c += 64) {
         float v[16];
         tc::tmem_ld16(taddr + c, v);
 #pragma unroll
         for (int i = 0; i < 16; ++i) vsq = fmaf(v[i], v[i], vsq);
       }
+      sm.vpart[cq * TC_ROWS + quad * 32 + lane] = vsq;
       tc::fence_before_sync();
-      tc::mbar_arrive(d_empty + buf);
-      tc::mbar_wait_backoff(m_full + ts_, (t / TC_TI) & 1, 512);
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(d_empty + buf);
+      named_sync(1, TC_PROD_THREADS);
+      const int n = tinfo[us];
       uint64_t key = KEY_NONE;
-      const bool has = et < n;
       bool sensitive = false;
-      if (has) {
-        const float* mp = sm.m_part + ts_ * 6 * TC_ROWS;
-        const float mu32 = mp[0 * TC_ROWS + et] + mp[1 * TC_ROWS + et];
-        const float sb = mp[2 * TC_ROWS + et] + mp[3 * TC_ROWS + et];
-        const float kk = mp[4 * TC_ROWS + et] + mp[5 * TC_ROWS + et];
-        const double cm0 = sm.m_m0[ts_ * TC_ROWS + et];
+      if (pt < TC_ROWS && pt < n) {
+        const int row = pt;
+        const float* mp = sm.m_part + us * 3 * TC_JQ * TC_ROWS;
+        float mu32 = 0.f, sb = 0.f, kk = 0.f, vv = 0.f;
+#pragma unroll
+        for (int q = 0; q < TC_JQ; ++q) {
+          mu32 += mp[(0 * TC_JQ + q) * TC_ROWS + row];
+          sb += mp[(1 * TC_JQ + q) * TC_ROWS + row];
+          kk += mp[(2 * TC_JQ + q) * TC_ROWS + row];
+          vv += sm.vpart[q * TC_ROWS + row];
+        }
+        const double cm0 = sm.m_m0[us * TC_ROWS + row];
         const double mu = cm0 + G.b + static_cast<double>(mu32);
-        const double vs = static_cast<double>(vsq);
+        const double vs = static_cast<double>(vv);
         const double s2 = G.sf2 - vs;
         // FP32 SIMT k + 3xTF32 contraction: error coefficient 8x the SIMT one
         const double eps = 8.0 * G.eps;
@@ -471,42 +272,247 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
           }
         }
         if (!sensitive) {
-          if (A.d_scores) A.d_scores[sm.m_j[ts_ * TC_ROWS + et]] = static_cast<float>(sc);
-          if (ub > -INFINITY) key = make_key(__double2float_ru(ub), sm.m_cvi[ts_ * TC_ROWS + et]);
+          if (A.d_scores) A.d_scores[sm.m_j[us * TC_ROWS + row]] = static_cast<float>(sc);
+          if (ub > -INFINITY) key = make_key(__double2float_ru(ub), sm.m_cvi[us * TC_ROWS + row]);
         }
       }
-      // warp-cooperative FP64 posterior for flagged rows of this warp
-      unsigned fl = __ballot_sync(0xffffffffu, sensitive);
-      while (fl) {
-        const int src = __ffs(fl) - 1;
-        fl &= fl - 1;
-        const int row = warp * 32 + src;
-        const uint32_t cvi = sm.m_cvi[ts_ * TC_ROWS + row];
+      if (warp < TC_EPI_WARPS) {
+        // warp-cooperative FP64 posterior for the flagged rows of this warp (d_scores mode only)
+        unsigned fl = __ballot_sync(0xffffffffu, sensitive);
+        while (fl) {
+          const int src = __ffs(fl) - 1;
+          fl &= fl - 1;
+          const int row = warp * 32 + src;
+          const uint32_t cvi = sm.m_cvi[us * TC_ROWS + row];
+          DV dv;
+          uint32_t act;
+          uint64_t raw;
+          decode_dev(S, cvi, dv, act, raw);
+          double kalpha, vq;
+          posterior64_warp(S, G, dv, lane, scratch, kalpha, vq);
+          if (lane == src) {
+            const double cm0 = sm.m_m0[us * TC_ROWS + row];
+            const double sc = acquisition(A.acq, cm0 + G.b + kalpha, G.sf2 - vq, cm0, G.fstar, A.xi, A.kappa);
+            const double ub = sc + 1e-12 * fmax(1.0, fabs(sc));
+            A.d_scores[sm.m_j[us * TC_ROWS + row]] = static_cast<float>(sc);
+            if (ub > -INFINITY) key = make_key(__double2float_ru(ub), cvi);
+          }
+        }
+      }
+      group_admit(key, sm.arr, ts, out.KC, pt, TC_PROD_THREADS, 1);
+    };
+
+    const uint64_t ntiles = (A.count + TC_PROD_THREADS - 1) / TC_PROD_THREADS;
+    uint32_t g = 0;                                   // global A-chunk counter
+    int t = 0;                                        // tile counter
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      // ---- phase 0: index -> configuration -> validity -> simulator -> queue
+      const uint64_t j = tile * TC_PROD_THREADS + pt;
+      const bool in = j < A.count;
+      bool ok = false;
+      if (in) {
+        const uint64_t pcvi = (A.mode == 0) ? A.begin + j : feistel_pi(A.fk, A.begin + j);
         DV dv;
         uint32_t act;
         uint64_t raw;
-        decode_dev(S, cvi, dv, act, raw);
-        double kalpha, vq;
-        posterior64_warp(S, G, dv, lane, scratch, kalpha, vq);
-        if (lane == src) {
-          const double cm0 = sm.m_m0[ts_ * TC_ROWS + row];
-          const double sc = acquisition(A.acq, cm0 + G.b + kalpha, G.sf2 - vq, cm0, G.fstar, A.xi, A.kappa);
-          const double ub = sc + 1e-12 * fmax(1.0, fabs(sc));
-          A.d_scores[sm.m_j[ts_ * TC_ROWS + row]] = static_cast<float>(sc);
-          if (ub > -INFINITY) key = make_key(__double2float_ru(ub), cvi);
+        decode_dev_idx(S, sm.cidx, pcvi, dv, act, raw);
+        double cost;
+        sim_dev(S, dv, act, cost, ok);
+        if (A.d_raw) A.d_raw[j] = raw;
+        if (!ok && A.d_scores) A.d_scores[j] = -INFINITY;
+        if (ok) {
+          const int slot = atomicAdd(&q_n, 1);
+          sm.q_dv[slot] = dv;
+          sm.q_m0[slot] = log(cost);
+          sm.q_cvi[slot] = static_cast<uint32_t>(pcvi);
+          sm.q_j[slot] = static_cast<uint32_t>(j);
         }
       }
-      group_admit(key, sm.arr, ts, out.KC, et, TC_EPI_WARPS * 32, 2);
+      const unsigned vb = __ballot_sync(0xffffffffu, in && ok);
+      if (lane == 0 && vb) atomicAdd(&valid_cta, static_cast<unsigned long long>(__popc(vb)));
+      named_sync(1, TC_PROD_THREADS);
+      const bool last_tile = tile + gridDim.x >= ntiles;
+      int head = 0;
+      while (true) {
+        const int avail = q_n - head;
+        const int n = avail >= TC_ROWS ? TC_ROWS : (last_tile ? avail : 0);
+        if (n <= 0) break;
+        // ---- publish tile t: meta + tile info
+        const int ts_ = t % TC_TI;
+        if (pt < n) {
+          sm.m_cvi[ts_ * TC_ROWS + pt] = sm.q_cvi[head + pt];
+          sm.m_j[ts_ * TC_ROWS + pt] = sm.q_j[head + pt];
+          sm.m_m0[ts_ * TC_ROWS + pt] = sm.q_m0[head + pt];
+        }
+        unsigned long long xp[2 * NF4];
+        const bool has = cand < n;
+        {
+          DV cdv;
+          cdv.w[0] = cdv.w[1] = cdv.w[2] = 0;
+          if (has) cdv = sm.q_dv[head + cand];
+#pragma unroll
+          for (int f = 0; f < 4 * NF4; f += 2) {
+            const float a = (has && f < S.d) ? sm.xt[f * VMAX + dv_get(cdv, f)] : 0.f;
+            const float b = (has && f + 1 < S.d) ? sm.xt[(f + 1) * VMAX + dv_get(cdv, f + 1)] : 0.f;
+            xp[f / 2] = f2_pack(a, b);
+          }
+        }
+        named_sync(1, TC_PROD_THREADS);
+        if (pt == 0) {
+          tinfo[ts_] = n;
+          tc::mbar_arrive(t_ready + ts_);
+        }
+        // ---- cross-covariance chunks -> A ring
+        float mu_p = 0.f, sb_p = 0.f, kk_p = 0.f;
+        const float hmask = has ? G.sf2f : 0.0f;
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int s = g % TC_NA;
+          tc::mbar_wait(a_empty + s, ((g / TC_NA) & 1u) ^ 1u);
+          float kh[TC_JPT], kl[TC_JPT];
+#pragma unroll
+          for (int q = 0; q < TC_JPT; ++q) {
+            const int jo = c * TC_KCH + jq * TC_JPT + q;      // warp-uniform; rows >= M are zero padded
+            unsigned long long acc0 = 0ull, acc1 = 0ull;
+            const uint32_t orow = sO + static_cast<uint32_t>(jo * NF4 * 16);
+#pragma unroll
+            for (int f4 = 0; f4 < NF4; ++f4) {
+              unsigned long long ox, oy;
+              tc::lds_u64x2(orow + 16 * f4, ox, oy);
+              const unsigned long long d0 = f2_sub(xp[2 * f4], ox), d1 = f2_sub(xp[2 * f4 + 1], oy);
+              acc0 = f2_fma(d0, d0, acc0);
+              acc1 = f2_fma(d1, d1, acc1);
+            }
+            const float2 ra = f2_unpack(acc0), rb = f2_unpack(acc1);
+            const float r2 = (ra.x + rb.x) + (ra.y + rb.y);
+            float arg, poly;
+            if (G.kernel == 0) {
+              arg = 2.2360679774997896f * tc::sqrt_approx_ftz(r2);
+              poly = fmaf(arg, fmaf(arg, 0.33333333333333333f, 1.0f), 1.0f);
+            } else {
+              arg = 0.5f * r2;
+              poly = 1.0f;
+            }
+            const float kval = hmask * poly * tc::ex2_approx(-1.4426950408889634f * arg);
+            const float cc = kval * (1.0f + arg);
+            const float jm = jo < G.M ? 1.0f : 0.0f;
+            mu_p = fmaf(kval, tc::lds_f32(sAl + 4 * jo), mu_p);
+            sb_p = fmaf(cc, tc::lds_f32(sAa + 4 * jo), sb_p);
+            kk_p = fmaf(jm * cc, cc, kk_p);
+            tc::split_tf32(kval, kh[q], kl[q]);
+          }
+          tc::sts_f32x4(tc::smem_u32(sm.Ahi[s]) + a_off, kh[0], kh[1], kh[2], kh[3]);
+          tc::sts_f32x4(tc::smem_u32(sm.Alo[s]) + a_off, kl[0], kl[1], kl[2], kl[3]);
+          tc::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(a_full + s);
+        }
+        float* mp = sm.m_part + ts_ * 3 * TC_JQ * TC_ROWS;
+        mp[(0 * TC_JQ + jq) * TC_ROWS + cand] = mu_p;
+        mp[(1 * TC_JQ + jq) * TC_ROWS + cand] = sb_p;
+        mp[(2 * TC_JQ + jq) * TC_ROWS + cand] = kk_p;
+        // ---- epilogue of the previous tile (its accumulator is complete by now)
+        if (t > 0) epilogue(t - 1);
+        named_sync(1, TC_PROD_THREADS);
+        head += n;
+        ++t;
+      }
+      // ---- compact the queue: leftovers (< 128) to the front
+      const int left = q_n - head;
+      named_sync(1, TC_PROD_THREADS);
+      DV mdv;
+      double mm0 = 0;
+      uint32_t mcvi = 0, mj = 0;
+      if (pt < left) {
+        mdv = sm.q_dv[head + pt];
+        mm0 = sm.q_m0[head + pt];
+        mcvi = sm.q_cvi[head + pt];
+        mj = sm.q_j[head + pt];
+      }
+      named_sync(1, TC_PROD_THREADS);
+      if (pt < left) {
+        sm.q_dv[pt] = mdv;
+        sm.q_m0[pt] = mm0;
+        sm.q_cvi[pt] = mcvi;
+        sm.q_j[pt] = mj;
+      }
+      if (pt == 0) q_n = left;
+      named_sync(1, TC_PROD_THREADS);
+    }
+    if (t > 0) epilogue(t - 1);
+    // ---- end of stream
+    if (pt == 0) {
+      const int ts_ = t % TC_TI;
+      tinfo[ts_] = -1;
+      tc::mbar_arrive(t_ready + ts_);
     }
     // ---- CTA list
-    named_sync(2, TC_EPI_WARPS * 32);
+    named_sync(1, TC_PROD_THREADS);
     const int n = ts.n_list;
     uint64_t* dst = out.lists + static_cast<size_t>(blockIdx.x) * out.KC;
-    for (int i = et; i < n; i += TC_EPI_WARPS * 32) dst[i] = sm.arr[i];
-    if (et == 0) {
+    for (int i = pt; i < n; i += TC_PROD_THREADS) dst[i] = sm.arr[i];
+    if (pt == 0) {
       out.counts[blockIdx.x] = n;
       out.drop[blockIdx.x] = ts.drop;
     }
+  } else {
+    // =========================================================== MMA issuer + B loader
+    if (lane == 0) {
+      uint32_t g = 0, gl = 0;                        // consumed chunks, loaded chunks (global counters)
+      auto load_next = [&]() {
+        const int s = gl % TC_NB;
+        tc::mbar_wait(b_empty + s, ((gl / TC_NB) & 1u) ^ 1u);
+        const int c = gl % nch;
+        const uint32_t bytes = 2u * (Mp16 - c * TC_KCH) * TC_KCH * 4;
+        tc::mbar_arrive_expect_tx(b_full + s, bytes);
+        tc::bulk_g2s(sm.B[s], TB.chunks + TB.off[c], bytes, b_full + s);
+        ++gl;
+      };
+      bool primed = false;
+      for (int t = 0;; ++t) {
+        const int ts_ = t % TC_TI;
+        tc::mbar_wait(t_ready + ts_, (t / TC_TI) & 1);
+        if (tinfo[ts_] < 0) break;
+        if (!primed) {
+          for (int i = 0; i < TC_NB - 1; ++i) load_next();
+          primed = true;
+        }
+        const int buf = t & 1;
+        tc::mbar_wait(d_empty + buf, ((t >> 1) & 1) ^ 1);
+        tc::fence_after_sync();
+        const uint32_t dcol = tmem + buf * Mp16;
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int sa = g % TC_NA, sbb = g % TC_NB;
+          tc::mbar_wait(a_full + sa, (g / TC_NA) & 1);
+          tc::mbar_wait(b_full + sbb, (g / TC_NB) & 1);
+          tc::fence_after_sync();
+          const int N = Mp16 - c * TC_KCH;
+          const uint32_t idesc = tc::idesc_tf32(TC_ROWS, N);
+          const uint32_t a_h = tc::smem_u32(sm.Ahi[sa]), a_l = tc::smem_u32(sm.Alo[sa]);
+          const uint32_t b_h = tc::smem_u32(sm.B[sbb]);
+          const uint32_t b_l = b_h + N * TC_KCH * 4;
+          const uint32_t sbo = (TC_KCH / 4) * 128;
+#pragma unroll
+          for (int ks = 0; ks < TC_KCH / 8; ++ks) {
+            const uint64_t ah = tc::sdesc(a_h + 256 * ks, 128, sbo), al = tc::sdesc(a_l + 256 * ks, 128, sbo);
+            const uint64_t bh = tc::sdesc(b_h + 256 * ks, 128, sbo), bl = tc::sdesc(b_l + 256 * ks, 128, sbo);
+            const uint32_t d = dcol + c * TC_KCH;
+            tc::mma_tf32(d, ah, bh, idesc, (c > 0 || ks > 0) ? 1u : 0u);
+            tc::mma_tf32(d, ah, bl, idesc, 1u);
+            tc::mma_tf32(d, al, bh, idesc, 1u);
+          }
+          tc::mma_commit(a_empty + sa);
+          tc::mma_commit(b_empty + sbb);
+          load_next();                               // refill the slot of chunk g-1, 2 chunks ahead
+        }
+        tc::mma_commit(d_full + buf);
+      }
+      // drain bulk copies still in flight before the CTA exits
+      while (g < gl) {
+        tc::mbar_wait(b_full + (g % TC_NB), (g / TC_NB) & 1);
+        ++g;
+      }
+    }
+    __syncwarp();
   }
   // ---- teardown
   tc::fence_before_sync();
