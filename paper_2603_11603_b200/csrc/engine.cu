@@ -65,8 +65,8 @@ size_t score_smem_bytes(int Mp, int DP, int d, int P) {
 size_t tc_smem_bytes(int Mp16, int DP, int d, int P) {
   auto r128 = [](size_t b) { return (b + 127) & ~size_t(127); };
   size_t s = 0;
-  s += 2 * TC_NA * r128(static_cast<size_t>(TC_ROWS) * TC_KCH * 4);
-  s += TC_NB * r128(2ull * Mp16 * TC_KCH * 4);
+  s += r128(2ull * TC_NA * TC_ROWS * TC_KCH * 4);
+  s += r128(static_cast<size_t>(TC_NB) * 2ull * Mp16 * TC_KCH * 4);
   s += r128(sizeof(float) * Mp16 * DP);
   s += 2 * r128(sizeof(float) * Mp16);
   s += r128(sizeof(float) * d * VMAX);

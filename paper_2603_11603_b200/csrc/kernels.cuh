@@ -251,6 +251,40 @@ __device__ __forceinline__ void posterior64_warp(const DevSpace& S, const DevGP&
   vsq = vs;
 }
 
+// ---- FP32 acquisition for the screen (the upper bound adds acq32_margin; the refine is FP64)
+__device__ __forceinline__ float lnh_f(float z) {
+  if (z >= -10.0f) {
+    const float phi = __expf(-0.5f * z * z) * 0.3989422804014327f;
+    const float Phi = 0.5f * erfcf(-z * 0.7071067811865476f);
+    return logf(fmaf(z, Phi, phi));
+  }
+  const float iz2 = 1.0f / (z * z);
+  return -0.5f * z * z - 0.9189385332046727f - 2.0f * logf(-z) +
+         log1pf(iz2 * (-3.0f + iz2 * (15.0f + iz2 * (-105.0f + 945.0f * iz2))));
+}
+__device__ __forceinline__ float acquisition32(int acq, float mu, float s2, float m0, float fstar, float xi,
+                                               float kappa, float& margin) {
+  if (acq == 2) {
+    margin = 1e-6f * (1.0f + fabsf(m0));
+    return -m0;
+  }
+  const float sigma = sqrtf(fmaxf(s2, 0.0f));
+  if (acq == 1) {
+    margin = 1e-6f * (1.0f + fabsf(mu) + kappa * sigma);
+    return kappa * sigma - mu;
+  }
+  const float u = fstar - mu - xi;
+  if (sigma == 0.0f) {
+    margin = 1e-6f * (1.0f + fabsf(u));
+    return u > 0.0f ? logf(u) : -INFINITY;
+  }
+  const float z = u / sigma;
+  const float r = logf(sigma) + lnh_f(z);
+  // FP32 evaluation error: rounding of the terms + cancellation of phi + z Phi (~ u z^2 relative)
+  margin = 2e-6f * (1.0f + fabsf(r)) + (z < -10.0f ? 0.0f : 1e-6f * (1.0f + z * z));
+  return r;
+}
+
 // Bitonic sort of arr[0..n) ascending (n power of two), all threads of the block.
 __device__ __forceinline__ void bitonic_sort(uint64_t* arr, int n) {
   for (int k = 2; k <= n; k <<= 1) {

@@ -90,9 +90,8 @@ __device__ __forceinline__ void group_admit(uint64_t key, uint64_t* arr, TopkSme
 }
 
 struct TcSmem {
-  float* Ahi[TC_NA];
-  float* Alo[TC_NA];
-  float* B[TC_NB];          // hi then lo
+  float* A0;                // A ring: stage s hi at A0 + 2 s a_stage, lo at + a_stage
+  float* B0;                // B ring: stage s at B0 + s b_stage (hi then lo)
   float* O;                 // [Mp16][DP]
   float* alpha;
   float* aabs;
@@ -133,11 +132,9 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
     p += (bytes + 127) & ~size_t(127);
     return r;
   };
-  for (int s = 0; s < TC_NA; ++s) {
-    sm.Ahi[s] = reinterpret_cast<float*>(take(a_stage_bytes));
-    sm.Alo[s] = reinterpret_cast<float*>(take(a_stage_bytes));
-  }
-  for (int s = 0; s < TC_NB; ++s) sm.B[s] = reinterpret_cast<float*>(take(b_stage_bytes));
+  sm.A0 = reinterpret_cast<float*>(take(2ull * TC_NA * a_stage_bytes));
+  sm.B0 = reinterpret_cast<float*>(take(static_cast<size_t>(TC_NB) * b_stage_bytes));
+  const uint32_t sA0 = tc::smem_u32(sm.A0), sB0 = tc::smem_u32(sm.B0);
   sm.O = reinterpret_cast<float*>(take(sizeof(float) * Mp16 * DP));
   sm.alpha = reinterpret_cast<float*>(take(sizeof(float) * Mp16));
   sm.aabs = reinterpret_cast<float*>(take(sizeof(float) * Mp16));
@@ -243,38 +240,45 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
           vv += sm.vpart[q * TC_ROWS + row];
         }
         const double cm0 = sm.m_m0[us * TC_ROWS + row];
-        const double mu = cm0 + G.b + static_cast<double>(mu32);
-        const double vs = static_cast<double>(vv);
-        const double s2 = G.sf2 - vs;
+        const float mu = static_cast<float>(cm0 + G.b) + mu32;
+        const float vs = vv;
+        const float s2 = static_cast<float>(G.sf2) - vs;
         // FP32 SIMT k + 3xTF32 contraction: error coefficient 8x the SIMT one
-        const double eps = 8.0 * G.eps;
-        const double d_mu = eps * static_cast<double>(sb) + 1e-13 * fabs(mu);
-        const double ew = eps * G.w_fro;
-        const double kn = sqrt(static_cast<double>(kk));
-        const double d_s2 = 2.5 * ew * sqrt(vs) * kn + ew * ew * static_cast<double>(kk) + eps * vs +
-                            4.0 * static_cast<double>(U32) * G.sf2;
-        const double sc = acquisition(A.acq, mu, s2, cm0, G.fstar, A.xi, A.kappa);
-        double ub = acquisition(A.acq, mu - d_mu, s2 + d_s2, cm0, G.fstar, A.xi, A.kappa);
-        ub += 1e-12 * fmax(1.0, fabs(ub));
-        if (A.d_scores && A.acq == 0) {
-          if (s2 > 0.0) {
-            const double sg = sqrt(s2), z = (G.fstar - mu - A.xi) / sg;
-            if (z >= -3.2) {
-              const double Phi = 0.5 * erfc(-z * INV_SQRT2);
-              const double h = exp(-0.5 * z * z) * INV_SQRT_2PI + z * Phi;
-              const double uu = static_cast<double>(U32);
-              const double e_s = (1.0 - z * Phi / h) / (2.0 * s2) * 160.0 * uu * vs +
-                                 Phi / (sg * h) * uu * (1.0 + static_cast<double>(sb));
-              sensitive = e_s > 5e-6;
+        const float eps = 8.0f * static_cast<float>(G.eps);
+        const float d_mu = eps * sb + 2e-7f * (1.0f + fabsf(mu));
+        const float ew = eps * static_cast<float>(G.w_fro);
+        const float d_s2 = 2.5f * ew * sqrtf(vs) * sqrtf(kk) + ew * ew * kk + eps * vs + 8.0f * U32 * G.sf2f;
+        const float fstar = static_cast<float>(G.fstar), m0f = static_cast<float>(cm0);
+        float m1, m2;
+        const float sc = acquisition32(A.acq, mu, s2, m0f, fstar, static_cast<float>(A.xi), static_cast<float>(A.kappa), m1);
+        float ub = acquisition32(A.acq, mu - d_mu, s2 + d_s2, m0f, fstar, static_cast<float>(A.xi),
+                                 static_cast<float>(A.kappa), m2);
+        ub += m2;
+        if (A.d_scores) {
+          // per-candidate output: FP64 acquisition (and FP64 posterior where FP32 is too sensitive)
+          const double mud = cm0 + G.b + static_cast<double>(mu32);
+          const double s2d = G.sf2 - static_cast<double>(vv);
+          if (A.acq == 0) {
+            if (s2d > 0.0) {
+              const double sg = sqrt(s2d), z = (G.fstar - mud - A.xi) / sg;
+              if (z >= -3.2) {
+                const double Phi = 0.5 * erfc(-z * INV_SQRT2);
+                const double h = exp(-0.5 * z * z) * INV_SQRT_2PI + z * Phi;
+                const double uu = static_cast<double>(U32);
+                const double e_s = (1.0 - z * Phi / h) / (2.0 * s2d) * 160.0 * uu * static_cast<double>(vv) +
+                                   Phi / (sg * h) * uu * (1.0 + static_cast<double>(sb));
+                sensitive = e_s > 5e-6;
+              }
+            } else {
+              sensitive = true;
             }
-          } else {
-            sensitive = true;
           }
+          if (!sensitive)
+            A.d_scores[sm.m_j[us * TC_ROWS + row]] =
+                static_cast<float>(acquisition(A.acq, mud, s2d, cm0, G.fstar, A.xi, A.kappa));
         }
-        if (!sensitive) {
-          if (A.d_scores) A.d_scores[sm.m_j[us * TC_ROWS + row]] = static_cast<float>(sc);
-          if (ub > -INFINITY) key = make_key(__double2float_ru(ub), sm.m_cvi[us * TC_ROWS + row]);
-        }
+        if (!sensitive && ub > -INFINITY) key = make_key(ub, sm.m_cvi[us * TC_ROWS + row]);
+        (void)sc;
       }
       if (warp < TC_EPI_WARPS) {
         // warp-cooperative FP64 posterior for the flagged rows of this warp (d_scores mode only)
@@ -400,8 +404,9 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
             kk_p = fmaf(jm * cc, cc, kk_p);
             tc::split_tf32(kval, kh[q], kl[q]);
           }
-          tc::sts_f32x4(tc::smem_u32(sm.Ahi[s]) + a_off, kh[0], kh[1], kh[2], kh[3]);
-          tc::sts_f32x4(tc::smem_u32(sm.Alo[s]) + a_off, kl[0], kl[1], kl[2], kl[3]);
+          const uint32_t ahs = sA0 + 2u * s * a_stage_bytes;
+          tc::sts_f32x4(ahs + a_off, kh[0], kh[1], kh[2], kh[3]);
+          tc::sts_f32x4(ahs + a_stage_bytes + a_off, kl[0], kl[1], kl[2], kl[3]);
           tc::fence_proxy_async();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(a_full + s);
@@ -464,7 +469,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
         const int c = gl % nch;
         const uint32_t bytes = 2u * (Mp16 - c * TC_KCH) * TC_KCH * 4;
         tc::mbar_arrive_expect_tx(b_full + s, bytes);
-        tc::bulk_g2s(sm.B[s], TB.chunks + TB.off[c], bytes, b_full + s);
+        tc::bulk_g2s(sm.B0 + static_cast<size_t>(s) * (b_stage_bytes / 4), TB.chunks + TB.off[c], bytes, b_full + s);
         ++gl;
       };
       bool primed = false;
@@ -487,8 +492,8 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
           tc::fence_after_sync();
           const int N = Mp16 - c * TC_KCH;
           const uint32_t idesc = tc::idesc_tf32(TC_ROWS, N);
-          const uint32_t a_h = tc::smem_u32(sm.Ahi[sa]), a_l = tc::smem_u32(sm.Alo[sa]);
-          const uint32_t b_h = tc::smem_u32(sm.B[sbb]);
+          const uint32_t a_h = sA0 + 2u * sa * a_stage_bytes, a_l = a_h + a_stage_bytes;
+          const uint32_t b_h = sB0 + sbb * b_stage_bytes;
           const uint32_t b_l = b_h + N * TC_KCH * 4;
           const uint32_t sbo = (TC_KCH / 4) * 128;
 #pragma unroll
