@@ -75,7 +75,7 @@ size_t tc_smem_bytes(int Mp16, int DP, int d, int P) {
   s += 2 * r128(sizeof(uint32_t) * TC_QCAP);
   s += 2 * r128(sizeof(uint32_t) * TC_TI * TC_ROWS);
   s += r128(sizeof(double) * TC_TI * TC_ROWS);
-  s += r128(sizeof(float) * TC_TI * 3 * TC_JQ * TC_ROWS);
+  s += r128(sizeof(float) * TC_TI * 3 * TC_ROWS);
   s += r128(sizeof(float) * 4 * TC_ROWS);
   s += r128(sizeof(uint64_t) * P);
   s += r128(sizeof(uint64_t) * 32);

@@ -28,7 +28,7 @@ constexpr int TC_ROWS = 128;                 // candidates per tile = TMEM lanes
 constexpr int TC_KCH = 16;                   // observed points per K-chunk
 constexpr int TC_JQ = TC_PROD_THREADS / TC_ROWS;   // producer threads per candidate (4)
 constexpr int TC_JPT = TC_KCH / TC_JQ;       // observed points per thread per chunk (4)
-constexpr int TC_NA = 3;                     // A ring stages
+constexpr int TC_NA = 4;                     // A ring stages
 constexpr int TC_NB = 3;                     // B ring stages
 constexpr int TC_TI = 2;                     // tile-info / meta slots
 constexpr int TC_QCAP = TC_ROWS - 1 + TC_PROD_THREADS;
@@ -103,7 +103,7 @@ struct TcSmem {
   uint32_t* m_cvi;          // [TI][128]
   uint32_t* m_j;
   double* m_m0;
-  float* m_part;            // [TI][3][JQ][128]  mu, sb, kk partials of the JQ observed-point groups
+  float* m_part;            // [TI][3][128]  mu, sb, kk sums (atomically reduced over the JQ groups)
   float* vpart;             // [4][128] ||v||^2 partials of the 4 column quarters
   uint64_t* arr;            // top-k' [P]
   uint64_t* bars;           // mbarriers
@@ -146,7 +146,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
   sm.m_cvi = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_TI * TC_ROWS));
   sm.m_j = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_TI * TC_ROWS));
   sm.m_m0 = reinterpret_cast<double*>(take(sizeof(double) * TC_TI * TC_ROWS));
-  sm.m_part = reinterpret_cast<float*>(take(sizeof(float) * TC_TI * 3 * TC_JQ * TC_ROWS));
+  sm.m_part = reinterpret_cast<float*>(take(sizeof(float) * TC_TI * 3 * TC_ROWS));
   sm.vpart = reinterpret_cast<float*>(take(sizeof(float) * 4 * TC_ROWS));
   sm.arr = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * out.P));
   sm.bars = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 32));
@@ -230,15 +230,11 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
       bool sensitive = false;
       if (pt < TC_ROWS && pt < n) {
         const int row = pt;
-        const float* mp = sm.m_part + us * 3 * TC_JQ * TC_ROWS;
-        float mu32 = 0.f, sb = 0.f, kk = 0.f, vv = 0.f;
+        const float* mp = sm.m_part + us * 3 * TC_ROWS;
+        const float mu32 = mp[0 * TC_ROWS + row], sb = mp[1 * TC_ROWS + row], kk = mp[2 * TC_ROWS + row];
+        float vv = 0.f;
 #pragma unroll
-        for (int q = 0; q < TC_JQ; ++q) {
-          mu32 += mp[(0 * TC_JQ + q) * TC_ROWS + row];
-          sb += mp[(1 * TC_JQ + q) * TC_ROWS + row];
-          kk += mp[(2 * TC_JQ + q) * TC_ROWS + row];
-          vv += sm.vpart[q * TC_ROWS + row];
-        }
+        for (int q = 0; q < 4; ++q) vv += sm.vpart[q * TC_ROWS + row];
         const double cm0 = sm.m_m0[us * TC_ROWS + row];
         const float mu = static_cast<float>(cm0 + G.b) + mu32;
         const float vs = vv;
@@ -343,6 +339,12 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
         if (n <= 0) break;
         // ---- publish tile t: meta + tile info
         const int ts_ = t % TC_TI;
+        if (pt < TC_ROWS) {
+          float* mz = sm.m_part + ts_ * 3 * TC_ROWS;
+          mz[pt] = 0.f;
+          mz[TC_ROWS + pt] = 0.f;
+          mz[2 * TC_ROWS + pt] = 0.f;
+        }
         if (pt < n) {
           sm.m_cvi[ts_ * TC_ROWS + pt] = sm.q_cvi[head + pt];
           sm.m_j[ts_ * TC_ROWS + pt] = sm.q_j[head + pt];
@@ -371,7 +373,8 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
         const float hmask = has ? G.sf2f : 0.0f;
         for (int c = 0; c < nch; ++c, ++g) {
           const int s = g % TC_NA;
-          tc::mbar_wait(a_empty + s, ((g / TC_NA) & 1u) ^ 1u);
+          const uint32_t a_par = ((g / TC_NA) & 1u) ^ 1u;
+          const bool a_ready = tc::mbar_test(a_empty + s, a_par);   // result consumed after the math
           float kh[TC_JPT], kl[TC_JPT];
 #pragma unroll
           for (int q = 0; q < TC_JPT; ++q) {
@@ -404,6 +407,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
             kk_p = fmaf(jm * cc, cc, kk_p);
             tc::split_tf32(kval, kh[q], kl[q]);
           }
+          if (!a_ready) tc::mbar_wait(a_empty + s, a_par);
           const uint32_t ahs = sA0 + 2u * s * a_stage_bytes;
           tc::sts_f32x4(ahs + a_off, kh[0], kh[1], kh[2], kh[3]);
           tc::sts_f32x4(ahs + a_stage_bytes + a_off, kl[0], kl[1], kl[2], kl[3]);
@@ -411,10 +415,10 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(a_full + s);
         }
-        float* mp = sm.m_part + ts_ * 3 * TC_JQ * TC_ROWS;
-        mp[(0 * TC_JQ + jq) * TC_ROWS + cand] = mu_p;
-        mp[(1 * TC_JQ + jq) * TC_ROWS + cand] = sb_p;
-        mp[(2 * TC_JQ + jq) * TC_ROWS + cand] = kk_p;
+        float* mp = sm.m_part + ts_ * 3 * TC_ROWS;
+        atomicAdd(mp + cand, mu_p);
+        atomicAdd(mp + TC_ROWS + cand, sb_p);
+        atomicAdd(mp + 2 * TC_ROWS + cand, kk_p);
         // ---- epilogue of the previous tile (its accumulator is complete by now)
         if (t > 0) epilogue(t - 1);
         named_sync(1, TC_PROD_THREADS);
