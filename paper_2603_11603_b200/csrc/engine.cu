@@ -68,7 +68,8 @@ size_t tc_smem_bytes(int Mp16, int DP, int d, int P) {
   s += r128(2ull * TC_NA * TC_ROWS * TC_KCH * 4);
   s += r128(static_cast<size_t>(TC_NB) * 2ull * Mp16 * TC_KCH * 4);
   s += r128(sizeof(float) * Mp16 * DP);
-  s += 2 * r128(sizeof(float) * Mp16);
+  s += r128(sizeof(float) * 2 * Mp16);
+  s += r128(0);
   s += r128(sizeof(float) * d * VMAX);
   s += r128(sizeof(DV) * TC_QCAP);
   s += r128(sizeof(double) * TC_QCAP);

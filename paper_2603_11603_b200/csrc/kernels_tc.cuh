@@ -136,8 +136,8 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
   sm.B0 = reinterpret_cast<float*>(take(static_cast<size_t>(TC_NB) * b_stage_bytes));
   const uint32_t sA0 = tc::smem_u32(sm.A0), sB0 = tc::smem_u32(sm.B0);
   sm.O = reinterpret_cast<float*>(take(sizeof(float) * Mp16 * DP));
-  sm.alpha = reinterpret_cast<float*>(take(sizeof(float) * Mp16));
-  sm.aabs = reinterpret_cast<float*>(take(sizeof(float) * Mp16));
+  sm.alpha = reinterpret_cast<float*>(take(sizeof(float) * 2 * Mp16));   // (alpha_j, |alpha_j|) pairs
+  sm.aabs = nullptr;
   sm.xt = reinterpret_cast<float*>(take(sizeof(float) * S.d * VMAX));
   sm.q_dv = reinterpret_cast<DV*>(take(sizeof(DV) * TC_QCAP));
   sm.q_m0 = reinterpret_cast<double*>(take(sizeof(double) * TC_QCAP));
@@ -162,8 +162,8 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
   // ---- setup: stage observed set + tables, init barriers, allocate TMEM
   for (int i = tid; i < Mp16 * DP; i += TC_THREADS) sm.O[i] = (i < G.Mp * DP) ? __ldg(G.O + i) : 0.f;
   for (int i = tid; i < Mp16; i += TC_THREADS) {
-    sm.alpha[i] = i < G.Mp ? __ldg(G.alpha + i) : 0.f;
-    sm.aabs[i] = i < G.Mp ? __ldg(G.aabs + i) : 0.f;
+    sm.alpha[2 * i] = i < G.Mp ? __ldg(G.alpha + i) : 0.f;
+    sm.alpha[2 * i + 1] = i < G.Mp ? __ldg(G.aabs + i) : 0.f;
   }
   for (int i = tid; i < S.d * VMAX; i += TC_THREADS) sm.xt[i] = __ldg(S.xt32 + i);
   for (int i = tid; i < out.P; i += TC_THREADS) sm.arr[i] = KEY_NONE;
@@ -203,7 +203,10 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
     const int cand = pt & (TC_ROWS - 1);             // candidate row of the tile
     const int jq = pt >> 7;                          // observed-point group of a chunk (warp-uniform)
     const int quad = warp & 3, cq = warp >> 2;       // TMEM lane quadrant / column quarter (epilogue)
-    const uint32_t sO = tc::smem_u32(sm.O), sAl = tc::smem_u32(sm.alpha), sAa = tc::smem_u32(sm.aabs);
+    const uint32_t sO = tc::smem_u32(sm.O), sAl = tc::smem_u32(sm.alpha);
+    // k = sf2 poly(a) exp(-a):  exp2 argument folds ln(sf2):  -a log2(e) + log2(sf2)
+    const float ex_c1 = (G.kernel == 0) ? -2.2360679774997896f * 1.4426950408889634f : -0.5f * 1.4426950408889634f;
+    const float ex_c0 = log2f(G.sf2f);
     const uint32_t a_off = tc::kmajor_off(cand, jq * TC_JPT, TC_KCH / 4);
     double* scratch = TB.scratch + (static_cast<size_t>(blockIdx.x) * TC_EPI_WARPS + (warp & 3)) * Mp16;
 
@@ -370,7 +373,6 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
         }
         // ---- cross-covariance chunks -> A ring
         float mu_p = 0.f, sb_p = 0.f, kk_p = 0.f;
-        const float hmask = has ? G.sf2f : 0.0f;
         for (int c = 0; c < nch; ++c, ++g) {
           const int s = g % TC_NA;
           const uint32_t a_par = ((g / TC_NA) & 1u) ^ 1u;
@@ -378,7 +380,9 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
           float kh[TC_JPT], kl[TC_JPT];
 #pragma unroll
           for (int q = 0; q < TC_JPT; ++q) {
-            const int jo = c * TC_KCH + jq * TC_JPT + q;      // warp-uniform; rows >= M are zero padded
+            // rows >= M of the observed set are zero padded with alpha = 0 and L^-1 columns = 0; rows of
+            // an incomplete tile (cand >= n) compute finite values that are never read back
+            const int jo = c * TC_KCH + jq * TC_JPT + q;      // warp-uniform
             unsigned long long acc0 = 0ull, acc1 = 0ull;
             const uint32_t orow = sO + static_cast<uint32_t>(jo * NF4 * 16);
 #pragma unroll
@@ -389,23 +393,27 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
               acc0 = f2_fma(d0, d0, acc0);
               acc1 = f2_fma(d1, d1, acc1);
             }
-            const float2 ra = f2_unpack(acc0), rb = f2_unpack(acc1);
-            const float r2 = (ra.x + rb.x) + (ra.y + rb.y);
-            float arg, poly;
+            const float2 rs = f2_unpack(f2_add(acc0, acc1));
+            const float r2 = rs.x + rs.y;
+            float arg, poly, ex;
             if (G.kernel == 0) {
-              arg = 2.2360679774997896f * tc::sqrt_approx_ftz(r2);
+              const float r = tc::sqrt_approx_ftz(r2);
+              arg = 2.2360679774997896f * r;
               poly = fmaf(arg, fmaf(arg, 0.33333333333333333f, 1.0f), 1.0f);
+              ex = tc::ex2_approx(fmaf(r, ex_c1, ex_c0));
             } else {
               arg = 0.5f * r2;
               poly = 1.0f;
+              ex = tc::ex2_approx(fmaf(r2, ex_c1, ex_c0));
             }
-            const float kval = hmask * poly * tc::ex2_approx(-1.4426950408889634f * arg);
-            const float cc = kval * (1.0f + arg);
-            const float jm = jo < G.M ? 1.0f : 0.0f;
-            mu_p = fmaf(kval, tc::lds_f32(sAl + 4 * jo), mu_p);
-            sb_p = fmaf(cc, tc::lds_f32(sAa + 4 * jo), sb_p);
-            kk_p = fmaf(jm * cc, cc, kk_p);
-            tc::split_tf32(kval, kh[q], kl[q]);
+            const float kval = poly * ex;
+            const float cc = fmaf(kval, arg, kval);           // k (1 + a)
+            float al, aa;
+            tc::lds_f32x2(sAl + 8 * jo, al, aa);
+            mu_p = fmaf(kval, al, mu_p);
+            sb_p = fmaf(cc, aa, sb_p);
+            kk_p = fmaf(cc, cc, kk_p);
+            tc::split_tf32_fast(kval, kh[q], kl[q]);
           }
           if (!a_ready) tc::mbar_wait(a_empty + s, a_par);
           const uint32_t ahs = sA0 + 2u * s * a_stage_bytes;

@@ -159,6 +159,17 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   lo = __uint_as_float(l);
 }
 
+// Cheap 3xTF32 split: hi = x rounded to nearest on the 10 TF32 mantissa bits (integer add + mask),
+// lo = x - hi exactly (|lo| <= 2^-11 |x|); the tensor core truncates lo to TF32 itself
+// (relative error of hi + lo <= 2^-21, inside the 8x FP32 error coefficient of DESIGN.md §5.6).
+__device__ __forceinline__ void split_tf32_fast(float x, float& hi, float& lo) {
+  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+  lo = x - hi;
+}
+__device__ __forceinline__ void lds_f32x2(uint32_t a, float& x, float& y) {
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x), "=f"(y) : "r"(a));
+}
+
 // byte offset of element (row, k) in a K-major no-swizzle tile with 8-row groups of `kcore`
 // 16-byte core-matrix columns: core (row/8, k/4) at (row/8)*SBO + (k/4)*128, SBO = kcore*128.
 __host__ __device__ __forceinline__ uint32_t kmajor_off(uint32_t row, uint32_t k, uint32_t kcore) {
