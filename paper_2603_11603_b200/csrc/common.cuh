@@ -276,11 +276,13 @@ AS_HD uint64_t splitmix64(uint64_t z) {
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
+// SAMPLE-mode permutation (R3): 4-round Feistel on b = max(2, ceil(log2 n)) bits with
+// alternating unbalanced halves (|L| = ceil(b/2), |R| = floor(b/2)), round function
+// fmix32(R ^ k_r) masked to |L|, cycle-walked into [0, n).  n < 2^32.
 struct FeistelKey {
-  uint64_t k[4];
+  uint32_t k[4];
   uint64_t n;
-  uint32_t h;
-  uint64_t mask;
+  uint32_t a, c;   // |L|, |R| of the input layout
 };
 inline FeistelKey feistel_make(uint64_t n, uint64_t seed) {
   FeistelKey f;
@@ -288,24 +290,35 @@ inline FeistelKey feistel_make(uint64_t n, uint64_t seed) {
   uint32_t b = 0;
   while ((1ull << b) < n) ++b;  // ceil(log2 n)
   if (b < 2) b = 2;
-  if (b & 1u) ++b;
-  f.h = b / 2;
-  f.mask = (1ull << f.h) - 1ull;
-  for (int r = 0; r < 4; ++r) f.k[r] = splitmix64(seed ^ (GOLDEN * static_cast<uint64_t>(r + 1)));
+  f.a = (b + 1) / 2;
+  f.c = b / 2;
+  for (int r = 0; r < 4; ++r) f.k[r] = static_cast<uint32_t>(splitmix64(seed ^ (GOLDEN * static_cast<uint64_t>(r + 1))));
   return f;
 }
-AS_HD uint64_t feistel_E(const FeistelKey& f, uint64_t x) {
-  uint64_t L = x >> f.h, R = x & f.mask;
+AS_HD uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85EBCA6Bu;
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  h ^= h >> 16;
+  return h;
+}
+AS_HD uint32_t feistel_E(const FeistelKey& f, uint32_t x) {
+  uint32_t a = f.a, c = f.c;
+  uint32_t L = x >> c, R = x & ((1u << c) - 1u);
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
-    uint64_t nl = R;
-    R = L ^ (splitmix64(R ^ f.k[r]) & f.mask);
+    const uint32_t nl = R;
+    R = L ^ (fmix32(R ^ f.k[r]) & ((1u << a) - 1u));
     L = nl;
+    const uint32_t t = a;
+    a = c;
+    c = t;
   }
-  return (L << f.h) | R;
+  return (L << c) | R;
 }
 AS_HD uint64_t feistel_pi(const FeistelKey& f, uint64_t j) {
-  uint64_t x = feistel_E(f, j);
+  uint32_t x = feistel_E(f, static_cast<uint32_t>(j));
   while (x >= f.n) x = feistel_E(f, x);
   return x;
 }
