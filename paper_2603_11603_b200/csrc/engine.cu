@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -85,16 +86,26 @@ size_t tc_smem_bytes(int Mp16, int DP, int d, int P) {
 }
 
 using TcKernelFn = void (*)(DevSpace, DevGP, BatchArgs, CtaOut, TcB);
-TcKernelFn tc_kernel_for(int DP) {
+template <int PW>
+TcKernelFn tc_kernel_pw(int DP) {
   switch (DP / 4) {
-    case 1: return score_tc_kernel<1>;
-    case 2: return score_tc_kernel<2>;
-    case 3: return score_tc_kernel<3>;
-    case 4: return score_tc_kernel<4>;
-    case 5: return score_tc_kernel<5>;
-    default: return score_tc_kernel<6>;
+    case 1: return score_tc_kernel<1, PW>;
+    case 2: return score_tc_kernel<2, PW>;
+    case 3: return score_tc_kernel<3, PW>;
+    case 4: return score_tc_kernel<4, PW>;
+    case 5: return score_tc_kernel<5, PW>;
+    default: return score_tc_kernel<6, PW>;
   }
 }
+// producer warps of the tensor-core kernel: 16 (default) or 8 (AUTOSCOUT_TC_WARPS=8, for A/B profiling)
+int tc_warps() {
+  static int w = [] {
+    const char* e = std::getenv("AUTOSCOUT_TC_WARPS");
+    return (e && std::atoi(e) == 8) ? 8 : 16;
+  }();
+  return w;
+}
+TcKernelFn tc_kernel_for(int DP) { return tc_warps() == 8 ? tc_kernel_pw<8>(DP) : tc_kernel_pw<16>(DP); }
 
 // TF32 round-to-nearest (ties away), as cvt.rna.tf32.f32
 float tf32_rna(float x) {
@@ -357,7 +368,7 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
     if (use_tc) {
       TcB tb = s->tb;
       tb.scratch = s->d_scratch;
-      tc_kernel_for(s->G.DP)<<<grid, TC_THREADS, smem, st>>>(s->D, G, A, out, tb);
+      tc_kernel_for(s->G.DP)<<<grid, tc_warps() * 32 + 32, smem, st>>>(s->D, G, A, out, tb);
     } else if (gp) {
       score_kernel<true><<<grid, SCORE_THREADS, smem, st>>>(s->D, G, A, out);
     } else {

@@ -20,18 +20,13 @@
 
 namespace as {
 
-constexpr int TC_PROD_WARPS = 16;
-constexpr int TC_PROD_THREADS = TC_PROD_WARPS * 32;
-constexpr int TC_THREADS = TC_PROD_THREADS + 32;
-constexpr int TC_MMA_WARP = TC_PROD_WARPS;
 constexpr int TC_ROWS = 128;                 // candidates per tile = TMEM lanes
 constexpr int TC_KCH = 16;                   // observed points per K-chunk
-constexpr int TC_JQ = TC_PROD_THREADS / TC_ROWS;   // producer threads per candidate (4)
-constexpr int TC_JPT = TC_KCH / TC_JQ;       // observed points per thread per chunk (4)
 constexpr int TC_NA = 4;                     // A ring stages
 constexpr int TC_NB = 3;                     // B ring stages
 constexpr int TC_TI = 2;                     // tile-info / meta slots
-constexpr int TC_QCAP = TC_ROWS - 1 + TC_PROD_THREADS;
+constexpr int TC_PW_MAX = 16;                // producer warps (template parameter PW in {8, 16})
+constexpr int TC_QCAP = TC_ROWS - 1 + TC_PW_MAX * 32;
 constexpr int TC_MAXCH = MMAX / TC_KCH;
 constexpr int TC_EPI_WARPS = 4;              // warps that finalise rows (rows 0..127)
 
@@ -104,16 +99,25 @@ struct TcSmem {
   uint32_t* m_j;
   double* m_m0;
   float* m_part;            // [TI][3][128]  mu, sb, kk sums (atomically reduced over the JQ groups)
-  float* vpart;             // [4][128] ||v||^2 partials of the 4 column quarters
+  float* vpart;             // [PW/4][128] ||v||^2 partials of the column groups
   uint64_t* arr;            // top-k' [P]
   uint64_t* bars;           // mbarriers
   uint64_t* cidx;           // coarse structure index [CI]
 };
 
 // NF4 = feature width in float4 units (d padded to 4); compile-time so the r^2 loop has no guards.
-template <int NF4>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+// PW = producer warps (8 or 16): PW*32/128 threads share a candidate, each computes TC_KCH*128/(PW*32)
+// observed points per K-chunk.
+template <int NF4, int PW>
+__global__ void __launch_bounds__(PW * 32 + 32, 1)
 score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
+  constexpr int TC_PROD_WARPS = PW;
+  constexpr int TC_PROD_THREADS = PW * 32;
+  constexpr int TC_THREADS = TC_PROD_THREADS + 32;
+  constexpr int TC_MMA_WARP = PW;
+  constexpr int TC_JQ = TC_PROD_THREADS / TC_ROWS;   // producer threads per candidate
+  constexpr int TC_JPT = TC_KCH / TC_JQ;             // observed points per thread per chunk
+  constexpr int NCQ = PW / 4;                        // TMEM column groups in the epilogue
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ TopkSmem ts;
   __shared__ int q_n;
@@ -147,7 +151,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
   sm.m_j = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_TI * TC_ROWS));
   sm.m_m0 = reinterpret_cast<double*>(take(sizeof(double) * TC_TI * TC_ROWS));
   sm.m_part = reinterpret_cast<float*>(take(sizeof(float) * TC_TI * 3 * TC_ROWS));
-  sm.vpart = reinterpret_cast<float*>(take(sizeof(float) * 4 * TC_ROWS));
+  sm.vpart = reinterpret_cast<float*>(take(sizeof(float) * 4 * TC_ROWS));   // sized for NCQ <= 4
   sm.arr = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * out.P));
   sm.bars = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 32));
   sm.cidx = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * CI));
@@ -207,7 +211,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
     // k = sf2 poly(a) exp(-a):  exp2 argument folds ln(sf2):  -a log2(e) + log2(sf2)
     const float ex_c1 = (G.kernel == 0) ? -2.2360679774997896f * 1.4426950408889634f : -0.5f * 1.4426950408889634f;
     const float ex_c0 = log2f(G.sf2f);
-    const uint32_t a_off = tc::kmajor_off(cand, jq * TC_JPT, TC_KCH / 4);
+    const uint32_t a_off = tc::kmajor_off(cand, jq * TC_JPT, TC_KCH / 4);   // + 128 B per further 4 points
     double* scratch = TB.scratch + (static_cast<size_t>(blockIdx.x) * TC_EPI_WARPS + (warp & 3)) * Mp16;
 
     // Epilogue of tile u: ||v||^2 from TMEM, then row finalisation + admission (all 512 threads).
@@ -217,7 +221,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
       tc::fence_after_sync();
       float vsq = 0.f;
       const uint32_t taddr = tmem + (static_cast<uint32_t>(quad * 32) << 16) + buf * Mp16;
-      for (int c = cq * 16; c < Mp16; c += 64) {
+      for (int c = cq * 16; c < Mp16; c += 16 * NCQ) {
         float v[16];
         tc::tmem_ld16(taddr + c, v);
 #pragma unroll
@@ -237,7 +241,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
         const float mu32 = mp[0 * TC_ROWS + row], sb = mp[1 * TC_ROWS + row], kk = mp[2 * TC_ROWS + row];
         float vv = 0.f;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) vv += sm.vpart[q * TC_ROWS + row];
+        for (int q = 0; q < NCQ; ++q) vv += sm.vpart[q * TC_ROWS + row];
         const double cm0 = sm.m_m0[us * TC_ROWS + row];
         const float mu = static_cast<float>(cm0 + G.b) + mu32;
         const float vs = vv;
@@ -417,8 +421,12 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
           }
           if (!a_ready) tc::mbar_wait(a_empty + s, a_par);
           const uint32_t ahs = sA0 + 2u * s * a_stage_bytes;
-          tc::sts_f32x4(ahs + a_off, kh[0], kh[1], kh[2], kh[3]);
-          tc::sts_f32x4(ahs + a_stage_bytes + a_off, kl[0], kl[1], kl[2], kl[3]);
+#pragma unroll
+          for (int v4 = 0; v4 < TC_JPT / 4; ++v4) {
+            tc::sts_f32x4(ahs + a_off + 128 * v4, kh[4 * v4], kh[4 * v4 + 1], kh[4 * v4 + 2], kh[4 * v4 + 3]);
+            tc::sts_f32x4(ahs + a_stage_bytes + a_off + 128 * v4, kl[4 * v4], kl[4 * v4 + 1], kl[4 * v4 + 2],
+                          kl[4 * v4 + 3]);
+          }
           tc::fence_proxy_async();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(a_full + s);
