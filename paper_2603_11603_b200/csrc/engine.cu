@@ -66,7 +66,6 @@ size_t score_smem_bytes(int Mp, int DP, int d, int P) {
 size_t tc_smem_bytes(int Mp16, int DP, int d, int P) {
   auto r128 = [](size_t b) { return (b + 127) & ~size_t(127); };
   size_t s = 0;
-  s += r128(2ull * TC_NA * TC_ROWS * TC_KCH * 4);
   s += r128(static_cast<size_t>(TC_NB) * 2ull * Mp16 * TC_KCH * 4);
   s += r128(sizeof(float) * Mp16 * DP);
   s += r128(sizeof(float) * 2 * Mp16);
@@ -86,26 +85,19 @@ size_t tc_smem_bytes(int Mp16, int DP, int d, int P) {
 }
 
 using TcKernelFn = void (*)(DevSpace, DevGP, BatchArgs, CtaOut, TcB);
-template <int PW>
-TcKernelFn tc_kernel_pw(int DP) {
+template <int KT>
+TcKernelFn tc_kernel_kt(int DP) {
   switch (DP / 4) {
-    case 1: return score_tc_kernel<1, PW>;
-    case 2: return score_tc_kernel<2, PW>;
-    case 3: return score_tc_kernel<3, PW>;
-    case 4: return score_tc_kernel<4, PW>;
-    case 5: return score_tc_kernel<5, PW>;
-    default: return score_tc_kernel<6, PW>;
+    case 1: return score_tc_kernel<1, 16, KT>;
+    case 2: return score_tc_kernel<2, 16, KT>;
+    case 3: return score_tc_kernel<3, 16, KT>;
+    case 4: return score_tc_kernel<4, 16, KT>;
+    case 5: return score_tc_kernel<5, 16, KT>;
+    default: return score_tc_kernel<6, 16, KT>;
   }
 }
-// producer warps of the tensor-core kernel: 16 (default) or 8 (AUTOSCOUT_TC_WARPS=8, for A/B profiling)
-int tc_warps() {
-  static int w = [] {
-    const char* e = std::getenv("AUTOSCOUT_TC_WARPS");
-    return (e && std::atoi(e) == 8) ? 8 : 16;
-  }();
-  return w;
-}
-TcKernelFn tc_kernel_for(int DP) { return tc_warps() == 8 ? tc_kernel_pw<8>(DP) : tc_kernel_pw<16>(DP); }
+constexpr int TC_WARPS = 16;   // producer warps of the tensor-core kernel (A/B-tested against 8)
+TcKernelFn tc_kernel_for(int DP, int kernel) { return kernel == 0 ? tc_kernel_kt<0>(DP) : tc_kernel_kt<1>(DP); }
 
 // TF32 round-to-nearest (ties away), as cvt.rna.tf32.f32
 float tf32_rna(float x) {
@@ -239,6 +231,12 @@ as_status upload_gp(as_space* s, cudaStream_t st) {
   s->tb = TcB{};
   s->tb.Mp16 = Mp16;
   s->tb.nch = nch;
+  s->tb.ndb = (2 * Mp16 + 32 * TC_NA <= 512) ? 2 : 1;
+  {
+    uint32_t need = static_cast<uint32_t>(s->tb.ndb * Mp16 + 32 * TC_NA), cols = 32;
+    while (cols < need) cols <<= 1;
+    s->tb.tmem_cols = cols;
+  }
   for (int c = 0; c < nch; ++c) {
     const int N = Mp16 - c * TC_KCH;
     s->tb.off[c] = static_cast<uint32_t>(s->h_Bch.size());
@@ -326,7 +324,7 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
   if (a.count > 0) {
     int occ = 1;
     if (use_tc) {
-      CUDA_TRY(cudaFuncSetAttribute(tc_kernel_for(s->G.DP), cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CUDA_TRY(cudaFuncSetAttribute(tc_kernel_for(s->G.DP, s->G.kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
       occ = 1;
     } else if (gp) {
@@ -368,7 +366,7 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
     if (use_tc) {
       TcB tb = s->tb;
       tb.scratch = s->d_scratch;
-      tc_kernel_for(s->G.DP)<<<grid, tc_warps() * 32 + 32, smem, st>>>(s->D, G, A, out, tb);
+      tc_kernel_for(s->G.DP, s->G.kernel)<<<grid, TC_WARPS * 32 + 32, smem, st>>>(s->D, G, A, out, tb);
     } else if (gp) {
       score_kernel<true><<<grid, SCORE_THREADS, smem, st>>>(s->D, G, A, out);
     } else {

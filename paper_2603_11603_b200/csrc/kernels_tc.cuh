@@ -5,10 +5,13 @@
 // Warp roles (544 threads, 1 CTA per SM):
 //   warps 0-15  producers: decode + mask + simulator -> queue of valid candidates -> per tile of
 //               128: k(x_c, o_j) in K-chunks of 16 observed points (4 per thread), split into
-//               TF32 hi/lo and written in the K-major core-matrix layout of the A operand
-//               (3-stage ring); then the epilogue of the PREVIOUS tile (whose accumulator is
-//               complete by then): tcgen05.ld of their TMEM lane quadrant (warp % 4) and column
-//               quarter (warp / 4) -> ||v||^2 -> mu, FP64 acquisition + bound -> CTA top-k'.
+//               TF32 hi/lo and stored with tcgen05.st straight into a 4-stage A ring in TMEM (each
+//               warp writes its own lane quadrant = its 32 candidates); then the epilogue of a
+//               finished tile: tcgen05.ld of their TMEM lane quadrant (warp % 4) and column
+//               quarter (warp / 4) -> ||v||^2 -> mu, FP32 acquisition + bound -> CTA top-k'.
+//               TMEM = D accumulator(s) [NDB x Mp16 columns] + A ring [4 x 32 columns]; D is
+//               double-buffered when it fits (M <= 192: epilogue of tile t-1 after producing t),
+//               else single (epilogue of tile t right after producing it).
 //   warp 16     MMA issuer + B loader (one thread): per K-chunk c, 3 MMAs x 2 k-steps into
 //               D[:, 16c : Mp16) (triangular skipping: L^-1 has no entries above the diagonal);
 //               bulk async copies of the host-pre-laid-out L^-1^T hi/lo chunks, 2 chunks ahead.
@@ -35,6 +38,8 @@ struct TcB {
   uint32_t off[TC_MAXCH];       // float offset of chunk c
   int nch;                      // Mp16 / 16
   int Mp16;                     // M padded to 16
+  int ndb;                      // TMEM accumulator buffers (2 if 2*Mp16 + 32*NA <= 512, else 1)
+  uint32_t tmem_cols;           // allocation (power of two >= ndb*Mp16 + 32*NA)
   double* scratch;              // [grid][4][Mp16] FP64 scratch of the sensitive-output fallback
 };
 
@@ -85,7 +90,6 @@ __device__ __forceinline__ void group_admit(uint64_t key, uint64_t* arr, TopkSme
 }
 
 struct TcSmem {
-  float* A0;                // A ring: stage s hi at A0 + 2 s a_stage, lo at + a_stage
   float* B0;                // B ring: stage s at B0 + s b_stage (hi then lo)
   float* O;                 // [Mp16][DP]
   float* alpha;
@@ -108,7 +112,7 @@ struct TcSmem {
 // NF4 = feature width in float4 units (d padded to 4); compile-time so the r^2 loop has no guards.
 // PW = producer warps (8 or 16): PW*32/128 threads share a candidate, each computes TC_KCH*128/(PW*32)
 // observed points per K-chunk.
-template <int NF4, int PW>
+template <int NF4, int PW, int KT>
 __global__ void __launch_bounds__(PW * 32 + 32, 1)
 score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
   constexpr int TC_PROD_WARPS = PW;
@@ -127,7 +131,8 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int Mp16 = TB.Mp16, DP = G.DP, nch = TB.nch;
-  const uint32_t a_stage_bytes = TC_ROWS * TC_KCH * 4;          // per split
+  const int NDB = TB.ndb;
+  const uint32_t A0col = static_cast<uint32_t>(NDB * Mp16);      // TMEM column of A stage 0
   const uint32_t b_stage_bytes = 2u * Mp16 * TC_KCH * 4;         // hi + lo at the widest chunk
   TcSmem sm;
   unsigned char* p = smem_raw;
@@ -136,9 +141,8 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
     p += (bytes + 127) & ~size_t(127);
     return r;
   };
-  sm.A0 = reinterpret_cast<float*>(take(2ull * TC_NA * a_stage_bytes));
   sm.B0 = reinterpret_cast<float*>(take(static_cast<size_t>(TC_NB) * b_stage_bytes));
-  const uint32_t sA0 = tc::smem_u32(sm.A0), sB0 = tc::smem_u32(sm.B0);
+  const uint32_t sB0 = tc::smem_u32(sm.B0);
   sm.O = reinterpret_cast<float*>(take(sizeof(float) * Mp16 * DP));
   sm.alpha = reinterpret_cast<float*>(take(sizeof(float) * 2 * Mp16));   // (alpha_j, |alpha_j|) pairs
   sm.aabs = nullptr;
@@ -194,7 +198,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
     q_n = 0;
     valid_cta = 0;
   }
-  const uint32_t tmem_cols = (2 * Mp16 <= 256) ? 256u : 512u;
+  const uint32_t tmem_cols = TB.tmem_cols;
   if (warp == 0) tc::tmem_alloc(&tmem_base, tmem_cols);
   tc::fence_before_sync();
   __syncthreads();
@@ -209,15 +213,15 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
     const int quad = warp & 3, cq = warp >> 2;       // TMEM lane quadrant / column quarter (epilogue)
     const uint32_t sO = tc::smem_u32(sm.O), sAl = tc::smem_u32(sm.alpha);
     // k = sf2 poly(a) exp(-a):  exp2 argument folds ln(sf2):  -a log2(e) + log2(sf2)
-    const float ex_c1 = (G.kernel == 0) ? -2.2360679774997896f * 1.4426950408889634f : -0.5f * 1.4426950408889634f;
+    const float ex_c1 = (KT == 0) ? -2.2360679774997896f * 1.4426950408889634f : -0.5f * 1.4426950408889634f;
     const float ex_c0 = log2f(G.sf2f);
     const uint32_t a_off = tc::kmajor_off(cand, jq * TC_JPT, TC_KCH / 4);   // + 128 B per further 4 points
     double* scratch = TB.scratch + (static_cast<size_t>(blockIdx.x) * TC_EPI_WARPS + (warp & 3)) * Mp16;
 
     // Epilogue of tile u: ||v||^2 from TMEM, then row finalisation + admission (all 512 threads).
     auto epilogue = [&](int u) {
-      const int us = u % TC_TI, buf = u & 1;
-      tc::mbar_wait(d_full + buf, (u >> 1) & 1);
+      const int us = u % TC_TI, buf = u % NDB;
+      tc::mbar_wait(d_full + buf, (u / NDB) & 1);
       tc::fence_after_sync();
       float vsq = 0.f;
       const uint32_t taddr = tmem + (static_cast<uint32_t>(quad * 32) << 16) + buf * Mp16;
@@ -400,7 +404,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
             const float2 rs = f2_unpack(f2_add(acc0, acc1));
             const float r2 = rs.x + rs.y;
             float arg, poly, ex;
-            if (G.kernel == 0) {
+            if (KT == 0) {
               const float r = tc::sqrt_approx_ftz(r2);
               arg = 2.2360679774997896f * r;
               poly = fmaf(arg, fmaf(arg, 0.33333333333333333f, 1.0f), 1.0f);
@@ -420,14 +424,15 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
             tc::split_tf32_fast(kval, kh[q], kl[q]);
           }
           if (!a_ready) tc::mbar_wait(a_empty + s, a_par);
-          const uint32_t ahs = sA0 + 2u * s * a_stage_bytes;
+          tc::fence_after_sync();
+          const uint32_t acol = tmem + (static_cast<uint32_t>(quad * 32) << 16) + A0col + 32u * s + jq * TC_JPT;
 #pragma unroll
           for (int v4 = 0; v4 < TC_JPT / 4; ++v4) {
-            tc::sts_f32x4(ahs + a_off + 128 * v4, kh[4 * v4], kh[4 * v4 + 1], kh[4 * v4 + 2], kh[4 * v4 + 3]);
-            tc::sts_f32x4(ahs + a_stage_bytes + a_off + 128 * v4, kl[4 * v4], kl[4 * v4 + 1], kl[4 * v4 + 2],
-                          kl[4 * v4 + 3]);
+            tc::tmem_st4(acol + 4 * v4, kh[4 * v4], kh[4 * v4 + 1], kh[4 * v4 + 2], kh[4 * v4 + 3]);
+            tc::tmem_st4(acol + 16 + 4 * v4, kl[4 * v4], kl[4 * v4 + 1], kl[4 * v4 + 2], kl[4 * v4 + 3]);
           }
-          tc::fence_proxy_async();
+          tc::tmem_st_wait();
+          tc::fence_before_sync();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(a_full + s);
         }
@@ -435,8 +440,12 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
         atomicAdd(mp + cand, mu_p);
         atomicAdd(mp + TC_ROWS + cand, sb_p);
         atomicAdd(mp + 2 * TC_ROWS + cand, kk_p);
-        // ---- epilogue of the previous tile (its accumulator is complete by now)
-        if (t > 0) epilogue(t - 1);
+        // ---- epilogue: previous tile with a double-buffered accumulator, this tile otherwise
+        if (NDB == 2) {
+          if (t > 0) epilogue(t - 1);
+        } else {
+          epilogue(t);
+        }
         named_sync(1, TC_PROD_THREADS);
         head += n;
         ++t;
@@ -463,7 +472,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
       if (pt == 0) q_n = left;
       named_sync(1, TC_PROD_THREADS);
     }
-    if (t > 0) epilogue(t - 1);
+    if (NDB == 2 && t > 0) epilogue(t - 1);
     // ---- end of stream
     if (pt == 0) {
       const int ts_ = t % TC_TI;
@@ -501,8 +510,8 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
           for (int i = 0; i < TC_NB - 1; ++i) load_next();
           primed = true;
         }
-        const int buf = t & 1;
-        tc::mbar_wait(d_empty + buf, ((t >> 1) & 1) ^ 1);
+        const int buf = t % NDB;
+        tc::mbar_wait(d_empty + buf, ((t / NDB) & 1) ^ 1);
         tc::fence_after_sync();
         const uint32_t dcol = tmem + buf * Mp16;
         for (int c = 0; c < nch; ++c, ++g) {
@@ -512,18 +521,17 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
           tc::fence_after_sync();
           const int N = Mp16 - c * TC_KCH;
           const uint32_t idesc = tc::idesc_tf32(TC_ROWS, N);
-          const uint32_t a_h = sA0 + 2u * sa * a_stage_bytes, a_l = a_h + a_stage_bytes;
+          const uint32_t a_h = tmem + A0col + 32u * sa, a_l = a_h + 16;
           const uint32_t b_h = sB0 + sbb * b_stage_bytes;
           const uint32_t b_l = b_h + N * TC_KCH * 4;
           const uint32_t sbo = (TC_KCH / 4) * 128;
 #pragma unroll
           for (int ks = 0; ks < TC_KCH / 8; ++ks) {
-            const uint64_t ah = tc::sdesc(a_h + 256 * ks, 128, sbo), al = tc::sdesc(a_l + 256 * ks, 128, sbo);
             const uint64_t bh = tc::sdesc(b_h + 256 * ks, 128, sbo), bl = tc::sdesc(b_l + 256 * ks, 128, sbo);
             const uint32_t d = dcol + c * TC_KCH;
-            tc::mma_tf32(d, ah, bh, idesc, (c > 0 || ks > 0) ? 1u : 0u);
-            tc::mma_tf32(d, ah, bl, idesc, 1u);
-            tc::mma_tf32(d, al, bh, idesc, 1u);
+            tc::mma_tf32_ts(d, a_h + 8 * ks, bh, idesc, (c > 0 || ks > 0) ? 1u : 0u);
+            tc::mma_tf32_ts(d, a_h + 8 * ks, bl, idesc, 1u);
+            tc::mma_tf32_ts(d, a_l + 8 * ks, bh, idesc, 1u);
           }
           tc::mma_commit(a_empty + sa);
           tc::mma_commit(b_empty + sbb);
