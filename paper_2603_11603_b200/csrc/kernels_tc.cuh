@@ -316,34 +316,9 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
     const uint64_t ntiles = (A.count + TC_PROD_THREADS - 1) / TC_PROD_THREADS;
     uint32_t g = 0;                                   // global A-chunk counter
     int t = 0;                                        // tile counter
-    uint64_t ptile = blockIdx.x;                      // next block of TC_PROD_THREADS positions
-    int head = 0;                                     // first unconsumed queue entry
-    // ---- phase 0 on the next TC_PROD_THREADS positions: index -> configuration -> validity ->
-    //      simulator -> queue (after moving the unconsumed entries to the front)
-    auto phase0_step = [&]() {
-      const int left = q_n - head;
-      if (head > 0) {
-        DV mdv;
-        double mm0 = 0;
-        uint32_t mcvi = 0, mj = 0;
-        if (pt < left) {
-          mdv = sm.q_dv[head + pt];
-          mm0 = sm.q_m0[head + pt];
-          mcvi = sm.q_cvi[head + pt];
-          mj = sm.q_j[head + pt];
-        }
-        named_sync(1, TC_PROD_THREADS);
-        if (pt < left) {
-          sm.q_dv[pt] = mdv;
-          sm.q_m0[pt] = mm0;
-          sm.q_cvi[pt] = mcvi;
-          sm.q_j[pt] = mj;
-        }
-        if (pt == 0) q_n = left;
-        head = 0;
-        named_sync(1, TC_PROD_THREADS);
-      }
-      const uint64_t j = ptile * TC_PROD_THREADS + pt;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      // ---- phase 0: index -> configuration -> validity -> simulator -> queue
+      const uint64_t j = tile * TC_PROD_THREADS + pt;
       const bool in = j < A.count;
       bool ok = false;
       if (in) {
@@ -366,117 +341,136 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
       }
       const unsigned vb = __ballot_sync(0xffffffffu, in && ok);
       if (lane == 0 && vb) atomicAdd(&valid_cta, static_cast<unsigned long long>(__popc(vb)));
-      ptile += gridDim.x;
       named_sync(1, TC_PROD_THREADS);
-    };
-    for (;;) {
-      while (q_n - head < TC_ROWS && ptile < ntiles) phase0_step();
-      const int avail = q_n - head;
-      const int n = avail < TC_ROWS ? avail : TC_ROWS;
-      if (n <= 0) break;
-      // ---- publish tile t: meta + tile info (queue entries are copied out and then consumed)
-      const int ts_ = t % TC_TI;
-      if (pt < TC_ROWS) {
-        float* mz = sm.m_part + ts_ * 3 * TC_ROWS;
-        mz[pt] = 0.f;
-        mz[TC_ROWS + pt] = 0.f;
-        mz[2 * TC_ROWS + pt] = 0.f;
-      }
-      if (pt < n) {
-        sm.m_cvi[ts_ * TC_ROWS + pt] = sm.q_cvi[head + pt];
-        sm.m_j[ts_ * TC_ROWS + pt] = sm.q_j[head + pt];
-        sm.m_m0[ts_ * TC_ROWS + pt] = sm.q_m0[head + pt];
-      }
-      unsigned long long xp[2 * NF4];
-      const bool has = cand < n;
-      {
-        DV cdv;
-        cdv.w[0] = cdv.w[1] = cdv.w[2] = 0;
-        if (has) cdv = sm.q_dv[head + cand];
-#pragma unroll
-        for (int f = 0; f < 4 * NF4; f += 2) {
-          const float a = (has && f < S.d) ? sm.xt[f * VMAX + dv_get(cdv, f)] : 0.f;
-          const float b = (has && f + 1 < S.d) ? sm.xt[(f + 1) * VMAX + dv_get(cdv, f + 1)] : 0.f;
-          xp[f / 2] = f2_pack(a, b);
+      const bool last_tile = tile + gridDim.x >= ntiles;
+      int head = 0;
+      while (true) {
+        const int avail = q_n - head;
+        const int n = avail >= TC_ROWS ? TC_ROWS : (last_tile ? avail : 0);
+        if (n <= 0) break;
+        // ---- publish tile t: meta + tile info
+        const int ts_ = t % TC_TI;
+        if (pt < TC_ROWS) {
+          float* mz = sm.m_part + ts_ * 3 * TC_ROWS;
+          mz[pt] = 0.f;
+          mz[TC_ROWS + pt] = 0.f;
+          mz[2 * TC_ROWS + pt] = 0.f;
         }
-      }
-      named_sync(1, TC_PROD_THREADS);
-      if (pt == 0) {
-        tinfo[ts_] = n;
-        tc::mbar_arrive(t_ready + ts_);
-      }
-      head += n;
-      // ---- cross-covariance chunks -> A ring (TMEM)
-      float mu_p = 0.f, sb_p = 0.f, kk_p = 0.f;
-      for (int c = 0; c < nch; ++c, ++g) {
-        const int s = g % TC_NA;
-        const uint32_t a_par = ((g / TC_NA) & 1u) ^ 1u;
-        const bool a_ready = tc::mbar_test(a_empty + s, a_par);   // result consumed after the math
-        float kh[TC_JPT], kl[TC_JPT];
+        if (pt < n) {
+          sm.m_cvi[ts_ * TC_ROWS + pt] = sm.q_cvi[head + pt];
+          sm.m_j[ts_ * TC_ROWS + pt] = sm.q_j[head + pt];
+          sm.m_m0[ts_ * TC_ROWS + pt] = sm.q_m0[head + pt];
+        }
+        unsigned long long xp[2 * NF4];
+        const bool has = cand < n;
+        {
+          DV cdv;
+          cdv.w[0] = cdv.w[1] = cdv.w[2] = 0;
+          if (has) cdv = sm.q_dv[head + cand];
 #pragma unroll
-        for (int q = 0; q < TC_JPT; ++q) {
-          // rows >= M of the observed set are zero padded with alpha = 0 and L^-1 columns = 0; rows of
-          // an incomplete tile (cand >= n) compute finite values that are never read back
-          const int jo = c * TC_KCH + jq * TC_JPT + q;      // warp-uniform
-          unsigned long long acc0 = 0ull, acc1 = 0ull;
-          const uint32_t orow = sO + static_cast<uint32_t>(jo * NF4 * 16);
-#pragma unroll
-          for (int f4 = 0; f4 < NF4; ++f4) {
-            unsigned long long ox, oy;
-            tc::lds_u64x2(orow + 16 * f4, ox, oy);
-            const unsigned long long d0 = f2_sub(xp[2 * f4], ox), d1 = f2_sub(xp[2 * f4 + 1], oy);
-            acc0 = f2_fma(d0, d0, acc0);
-            acc1 = f2_fma(d1, d1, acc1);
+          for (int f = 0; f < 4 * NF4; f += 2) {
+            const float a = (has && f < S.d) ? sm.xt[f * VMAX + dv_get(cdv, f)] : 0.f;
+            const float b = (has && f + 1 < S.d) ? sm.xt[(f + 1) * VMAX + dv_get(cdv, f + 1)] : 0.f;
+            xp[f / 2] = f2_pack(a, b);
           }
-          const float2 rs = f2_unpack(f2_add(acc0, acc1));
-          const float r2 = rs.x + rs.y;
-          float arg, poly, ex;
-          if (KT == 0) {
-            const float r = tc::sqrt_approx_ftz(r2);
-            arg = 2.2360679774997896f * r;
-            poly = fmaf(arg, fmaf(arg, 0.33333333333333333f, 1.0f), 1.0f);
-            ex = tc::ex2_approx(fmaf(r, ex_c1, ex_c0));
-          } else {
-            arg = 0.5f * r2;
-            poly = 1.0f;
-            ex = tc::ex2_approx(fmaf(r2, ex_c1, ex_c0));
-          }
-          const float kval = poly * ex;
-          const float cc = fmaf(kval, arg, kval);           // k (1 + a)
-          float al, aa;
-          tc::lds_f32x2(sAl + 8 * jo, al, aa);
-          mu_p = fmaf(kval, al, mu_p);
-          sb_p = fmaf(cc, aa, sb_p);
-          kk_p = fmaf(cc, cc, kk_p);
-          tc::split_tf32_fast(kval, kh[q], kl[q]);
         }
-        if (!a_ready) tc::mbar_wait(a_empty + s, a_par);
-        tc::fence_after_sync();
-        const uint32_t acol = tmem + (static_cast<uint32_t>(quad * 32) << 16) + A0col + 32u * s + jq * TC_JPT;
+        named_sync(1, TC_PROD_THREADS);
+        if (pt == 0) {
+          tinfo[ts_] = n;
+          tc::mbar_arrive(t_ready + ts_);
+        }
+        // ---- cross-covariance chunks -> A ring
+        float mu_p = 0.f, sb_p = 0.f, kk_p = 0.f;
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int s = g % TC_NA;
+          const uint32_t a_par = ((g / TC_NA) & 1u) ^ 1u;
+          const bool a_ready = tc::mbar_test(a_empty + s, a_par);   // result consumed after the math
+          float kh[TC_JPT], kl[TC_JPT];
 #pragma unroll
-        for (int v4 = 0; v4 < TC_JPT / 4; ++v4) {
-          tc::tmem_st4(acol + 4 * v4, kh[4 * v4], kh[4 * v4 + 1], kh[4 * v4 + 2], kh[4 * v4 + 3]);
-          tc::tmem_st4(acol + 16 + 4 * v4, kl[4 * v4], kl[4 * v4 + 1], kl[4 * v4 + 2], kl[4 * v4 + 3]);
+          for (int q = 0; q < TC_JPT; ++q) {
+            // rows >= M of the observed set are zero padded with alpha = 0 and L^-1 columns = 0; rows of
+            // an incomplete tile (cand >= n) compute finite values that are never read back
+            const int jo = c * TC_KCH + jq * TC_JPT + q;      // warp-uniform
+            unsigned long long acc0 = 0ull, acc1 = 0ull;
+            const uint32_t orow = sO + static_cast<uint32_t>(jo * NF4 * 16);
+#pragma unroll
+            for (int f4 = 0; f4 < NF4; ++f4) {
+              unsigned long long ox, oy;
+              tc::lds_u64x2(orow + 16 * f4, ox, oy);
+              const unsigned long long d0 = f2_sub(xp[2 * f4], ox), d1 = f2_sub(xp[2 * f4 + 1], oy);
+              acc0 = f2_fma(d0, d0, acc0);
+              acc1 = f2_fma(d1, d1, acc1);
+            }
+            const float2 rs = f2_unpack(f2_add(acc0, acc1));
+            const float r2 = rs.x + rs.y;
+            float arg, poly, ex;
+            if (KT == 0) {
+              const float r = tc::sqrt_approx_ftz(r2);
+              arg = 2.2360679774997896f * r;
+              poly = fmaf(arg, fmaf(arg, 0.33333333333333333f, 1.0f), 1.0f);
+              ex = tc::ex2_approx(fmaf(r, ex_c1, ex_c0));
+            } else {
+              arg = 0.5f * r2;
+              poly = 1.0f;
+              ex = tc::ex2_approx(fmaf(r2, ex_c1, ex_c0));
+            }
+            const float kval = poly * ex;
+            const float cc = fmaf(kval, arg, kval);           // k (1 + a)
+            float al, aa;
+            tc::lds_f32x2(sAl + 8 * jo, al, aa);
+            mu_p = fmaf(kval, al, mu_p);
+            sb_p = fmaf(cc, aa, sb_p);
+            kk_p = fmaf(cc, cc, kk_p);
+            tc::split_tf32_fast(kval, kh[q], kl[q]);
+          }
+          if (!a_ready) tc::mbar_wait(a_empty + s, a_par);
+          tc::fence_after_sync();
+          const uint32_t acol = tmem + (static_cast<uint32_t>(quad * 32) << 16) + A0col + 32u * s + jq * TC_JPT;
+#pragma unroll
+          for (int v4 = 0; v4 < TC_JPT / 4; ++v4) {
+            tc::tmem_st4(acol + 4 * v4, kh[4 * v4], kh[4 * v4 + 1], kh[4 * v4 + 2], kh[4 * v4 + 3]);
+            tc::tmem_st4(acol + 16 + 4 * v4, kl[4 * v4], kl[4 * v4 + 1], kl[4 * v4 + 2], kl[4 * v4 + 3]);
+          }
+          tc::tmem_st_wait();
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(a_full + s);
         }
-        tc::tmem_st_wait();
-        tc::fence_before_sync();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(a_full + s);
+        float* mp = sm.m_part + ts_ * 3 * TC_ROWS;
+        atomicAdd(mp + cand, mu_p);
+        atomicAdd(mp + TC_ROWS + cand, sb_p);
+        atomicAdd(mp + 2 * TC_ROWS + cand, kk_p);
+        // ---- epilogue: previous tile with a double-buffered accumulator, this tile otherwise
+        if (NDB == 2) {
+          if (t > 0) epilogue(t - 1);
+        } else {
+          epilogue(t);
+        }
+        named_sync(1, TC_PROD_THREADS);
+        head += n;
+        ++t;
       }
-      float* mp = sm.m_part + ts_ * 3 * TC_ROWS;
-      atomicAdd(mp + cand, mu_p);
-      atomicAdd(mp + TC_ROWS + cand, sb_p);
-      atomicAdd(mp + 2 * TC_ROWS + cand, kk_p);
-      if (NDB == 2) {
-        // double-buffered accumulator: finish the previous tile while the MMA works on this one
-        if (t > 0) epilogue(t - 1);
-      } else {
-        // single accumulator: overlap the MMA tail of this tile with the next phase-0 step
-        if (q_n - head < TC_ROWS && ptile < ntiles) phase0_step();
-        epilogue(t);
+      // ---- compact the queue: leftovers (< 128) to the front
+      const int left = q_n - head;
+      named_sync(1, TC_PROD_THREADS);
+      DV mdv;
+      double mm0 = 0;
+      uint32_t mcvi = 0, mj = 0;
+      if (pt < left) {
+        mdv = sm.q_dv[head + pt];
+        mm0 = sm.q_m0[head + pt];
+        mcvi = sm.q_cvi[head + pt];
+        mj = sm.q_j[head + pt];
       }
       named_sync(1, TC_PROD_THREADS);
-      ++t;
+      if (pt < left) {
+        sm.q_dv[pt] = mdv;
+        sm.q_m0[pt] = mm0;
+        sm.q_cvi[pt] = mcvi;
+        sm.q_j[pt] = mj;
+      }
+      if (pt == 0) q_n = left;
+      named_sync(1, TC_PROD_THREADS);
     }
     if (NDB == 2 && t > 0) epilogue(t - 1);
     // ---- end of stream
