@@ -103,7 +103,7 @@ struct TcSmem {
   uint32_t* m_j;
   double* m_m0;
   float* m_part;            // [TI][3][128]  mu, sb, kk sums (atomically reduced over the JQ groups)
-  float* vpart;             // [PW/4][128] ||v||^2 partials of the column groups
+  float* vpart;             // [JQ][128] ||v||^2 partials of the column groups
   uint64_t* arr;            // top-k' [P]
   uint64_t* bars;           // mbarriers
   uint64_t* cidx;           // coarse structure index [CI]
@@ -121,7 +121,6 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
   constexpr int TC_MMA_WARP = PW;
   constexpr int TC_JQ = TC_PROD_THREADS / TC_ROWS;   // producer threads per candidate
   constexpr int TC_JPT = TC_KCH / TC_JQ;             // observed points per thread per chunk
-  constexpr int NCQ = PW / 4;                        // TMEM column groups in the epilogue
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ TopkSmem ts;
   __shared__ int q_n;
@@ -155,7 +154,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
   sm.m_j = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_TI * TC_ROWS));
   sm.m_m0 = reinterpret_cast<double*>(take(sizeof(double) * TC_TI * TC_ROWS));
   sm.m_part = reinterpret_cast<float*>(take(sizeof(float) * TC_TI * 3 * TC_ROWS));
-  sm.vpart = reinterpret_cast<float*>(take(sizeof(float) * 4 * TC_ROWS));   // sized for NCQ <= 4
+  sm.vpart = reinterpret_cast<float*>(take(sizeof(float) * 4 * TC_ROWS));   // sized for TC_JQ <= 4
   sm.arr = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * out.P));
   sm.bars = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 32));
   sm.cidx = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * CI));
@@ -210,7 +209,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
     const int pt = tid;                              // 0..511
     const int cand = pt & (TC_ROWS - 1);             // candidate row of the tile
     const int jq = pt >> 7;                          // observed-point group of a chunk (warp-uniform)
-    const int quad = warp & 3, cq = warp >> 2;       // TMEM lane quadrant / column quarter (epilogue)
+    const int quad = warp & 3;                       // TMEM lane quadrant of this warp
     const uint32_t sO = tc::smem_u32(sm.O), sAl = tc::smem_u32(sm.alpha);
     // k = sf2 poly(a) exp(-a):  exp2 argument folds ln(sf2):  -a log2(e) + log2(sf2)
     const float ex_c1 = (KT == 0) ? -2.2360679774997896f * 1.4426950408889634f : -0.5f * 1.4426950408889634f;
@@ -218,20 +217,25 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
     const uint32_t a_off = tc::kmajor_off(cand, jq * TC_JPT, TC_KCH / 4);   // + 128 B per further 4 points
     double* scratch = TB.scratch + (static_cast<size_t>(blockIdx.x) * TC_EPI_WARPS + (warp & 3)) * Mp16;
 
-    // Epilogue of tile u: ||v||^2 from TMEM, then row finalisation + admission (all 512 threads).
-    auto epilogue = [&](int u) {
+    // Epilogue of tile u.  Column block b = [16b, 16b+16) of the accumulator is final once chunk b's
+    // MMAs completed (triangular: later chunks only write columns >= 16(b+1)); the producers already
+    // read blocks b < nch - NA during the chunk loop (vsq_run), so only the last NA blocks wait for
+    // the tile's final commit.
+    auto epilogue = [&](int u, float vsq_run) {
       const int us = u % TC_TI, buf = u % NDB;
       tc::mbar_wait(d_full + buf, (u / NDB) & 1);
       tc::fence_after_sync();
-      float vsq = 0.f;
-      const uint32_t taddr = tmem + (static_cast<uint32_t>(quad * 32) << 16) + buf * Mp16;
-      for (int c = cq * 16; c < Mp16; c += 16 * NCQ) {
-        float v[16];
-        tc::tmem_ld16(taddr + c, v);
+      float vsq = vsq_run;
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(quad * 32) << 16) + buf * Mp16 + TC_JPT * jq;
+      for (int b = (nch > TC_NA ? nch - TC_NA : 0); b < nch; ++b) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) vsq = fmaf(v[i], v[i], vsq);
+        for (int h = 0; h < TC_JPT; h += 4) {
+          float v[4];
+          tc::tmem_ld4(taddr + 16 * b + h, v);
+          vsq = fmaf(v[0], v[0], fmaf(v[1], v[1], fmaf(v[2], v[2], fmaf(v[3], v[3], vsq))));
+        }
       }
-      sm.vpart[cq * TC_ROWS + quad * 32 + lane] = vsq;
+      sm.vpart[jq * TC_ROWS + quad * 32 + lane] = vsq;
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(d_empty + buf);
@@ -245,7 +249,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
         const float mu32 = mp[0 * TC_ROWS + row], sb = mp[1 * TC_ROWS + row], kk = mp[2 * TC_ROWS + row];
         float vv = 0.f;
 #pragma unroll
-        for (int q = 0; q < NCQ; ++q) vv += sm.vpart[q * TC_ROWS + row];
+        for (int q = 0; q < TC_JQ; ++q) vv += sm.vpart[q * TC_ROWS + row];
         const double cm0 = sm.m_m0[us * TC_ROWS + row];
         const float mu = static_cast<float>(cm0 + G.b) + mu32;
         const float vs = vv;
@@ -380,7 +384,8 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
           tc::mbar_arrive(t_ready + ts_);
         }
         // ---- cross-covariance chunks -> A ring
-        float mu_p = 0.f, sb_p = 0.f, kk_p = 0.f;
+        float mu_p = 0.f, sb_p = 0.f, kk_p = 0.f, vsq_run = 0.f;
+        const uint32_t dq = tmem + (static_cast<uint32_t>(quad * 32) << 16) + (t % NDB) * Mp16 + TC_JPT * jq;
         for (int c = 0; c < nch; ++c, ++g) {
           const int s = g % TC_NA;
           const uint32_t a_par = ((g / TC_NA) & 1u) ^ 1u;
@@ -425,6 +430,15 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
           }
           if (!a_ready) tc::mbar_wait(a_empty + s, a_par);
           tc::fence_after_sync();
+          if (c >= TC_NA) {
+            // chunk c - NA of this tile completed (its A stage was released): its column block is final
+#pragma unroll
+            for (int h = 0; h < TC_JPT; h += 4) {
+              float v[4];
+              tc::tmem_ld4(dq + 16 * (c - TC_NA) + h, v);
+              vsq_run = fmaf(v[0], v[0], fmaf(v[1], v[1], fmaf(v[2], v[2], fmaf(v[3], v[3], vsq_run))));
+            }
+          }
           const uint32_t acol = tmem + (static_cast<uint32_t>(quad * 32) << 16) + A0col + 32u * s + jq * TC_JPT;
 #pragma unroll
           for (int v4 = 0; v4 < TC_JPT / 4; ++v4) {
@@ -440,12 +454,8 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
         atomicAdd(mp + cand, mu_p);
         atomicAdd(mp + TC_ROWS + cand, sb_p);
         atomicAdd(mp + 2 * TC_ROWS + cand, kk_p);
-        // ---- epilogue: previous tile with a double-buffered accumulator, this tile otherwise
-        if (NDB == 2) {
-          if (t > 0) epilogue(t - 1);
-        } else {
-          epilogue(t);
-        }
+        // ---- epilogue of this tile (only the last NA column blocks still wait for the MMAs)
+        epilogue(t, vsq_run);
         named_sync(1, TC_PROD_THREADS);
         head += n;
         ++t;
@@ -472,7 +482,6 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
       if (pt == 0) q_n = left;
       named_sync(1, TC_PROD_THREADS);
     }
-    if (NDB == 2 && t > 0) epilogue(t - 1);
     // ---- end of stream
     if (pt == 0) {
       const int ts_ = t % TC_TI;
