@@ -242,8 +242,9 @@ class Space:
                                          _stream_ptr(stream)))
 
     def set_path(self, path):
-        """0 auto, 1 SIMT, 2 tensor cores (or 'auto' / 'simt' / 'tc')."""
-        path = {"auto": 0, "simt": 1, "tc": 2}.get(path, path)
+        """0 auto, 1 SIMT, 2 tensor cores (SIMT r^2), 3 tensor cores (one-hot r^2 on the tensor cores);
+        or 'auto' / 'simt' / 'tc' / 'tc2'."""
+        path = {"auto": 0, "simt": 1, "tc": 2, "tc2": 3}.get(path, path)
         _check(_LIB.autoscout_set_path(self.h, int(path)))
 
     def set_timing(self, enable=True):

@@ -1,5 +1,6 @@
 // extern "C" boundary of libautoscout.so (include/autoscout.h): host orchestration of the
 // sm_100a kernels in kernels.cuh.  No torch types; plain pointers and sizes.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -12,6 +13,7 @@
 #include "../../include/autoscout.h"
 #include "kernels.cuh"
 #include "kernels_tc.cuh"
+#include "kernels_tc2.cuh"
 #include "space.hpp"
 
 using namespace as;
@@ -83,6 +85,37 @@ size_t tc_smem_bytes(int Mp16, int DP, int d, int P) {
   s += r128(sizeof(uint64_t) * CI);
   return s;
 }
+
+// one-hot R2 kernel (kernels_tc2.cuh): B ring (2) + T ring (3) + E (2) + the common state
+size_t tc2_smem_bytes(int Mp16, int Kp, int nh, int P) {
+  auto r128 = [](size_t b) { return (b + 127) & ~size_t(127); };
+  const int nh1 = nh > 0 ? nh : 1;
+  size_t s = 0;
+  s += r128(static_cast<size_t>(TC2_NB) * 2ull * Mp16 * TC_KCH * 4);
+  s += r128(static_cast<size_t>(TC2_NT) * 2ull * (TC2_RG * TC_KCH) * Kp * 2);
+  s += r128(2ull * TC_ROWS * Kp * 2);
+  s += r128(sizeof(float) * 2 * Mp16);
+  s += r128(sizeof(float) * nh1 * Mp16);
+  s += r128(sizeof(float) * nh1 * VMAX);
+  s += r128(sizeof(float) * nh1 * TC_TI * TC_ROWS);
+  s += r128(sizeof(DV) * TC_QCAP);
+  s += r128(sizeof(double) * TC_QCAP);
+  s += 2 * r128(sizeof(uint32_t) * TC_QCAP);
+  s += 2 * r128(sizeof(uint32_t) * TC_TI * TC_ROWS);
+  s += r128(sizeof(double) * TC_TI * TC_ROWS);
+  s += r128(sizeof(float) * TC_TI * 3 * TC_ROWS);
+  s += r128(sizeof(float) * 4 * TC_ROWS);
+  s += r128(sizeof(uint64_t) * P);
+  s += r128(sizeof(uint64_t) * 64);
+  s += r128(sizeof(uint64_t) * CI);
+  return s;
+}
+using Tc2KernelFn = void (*)(DevSpace, DevGP, BatchArgs, CtaOut, TcB, Tc2B);
+template <int KT>
+Tc2KernelFn tc2_kernel_kt(int nh) {
+  return nh == 0 ? score_tc2_kernel<16, KT, 0> : (nh == 2 ? score_tc2_kernel<16, KT, 2> : score_tc2_kernel<16, KT, 4>);
+}
+Tc2KernelFn tc2_kernel_for(int kernel, int nh) { return kernel == 0 ? tc2_kernel_kt<0>(nh) : tc2_kernel_kt<1>(nh); }
 
 using TcKernelFn = void (*)(DevSpace, DevGP, BatchArgs, CtaOut, TcB);
 template <int KT>
@@ -164,10 +197,16 @@ struct as_space {
   double *d_O64 = nullptr, *d_alpha64 = nullptr, *d_W64 = nullptr;
   std::vector<float> h_O, h_alpha, h_aabs, h_Wblk, h_Bch;
   float* d_Bch = nullptr;          // L^-1^T hi/lo chunks for the tensor-core path
+  std::vector<uint16_t> h_Tch;     // one-hot R2 operand T (FP16 hi/lo groups, kernels_tc2.cuh)
+  std::vector<float> h_xh, h_oh;   // SIMT features of the one-hot kernel (scaled)
+  uint16_t* d_Tch = nullptr;
+  float *d_xh = nullptr, *d_oh = nullptr;
+  Tc2B t2{};
+  bool tc2_auto = false;           // auto path prefers the one-hot kernel (set once it is the faster one)
   double* d_scratch = nullptr;     // FP64 scratch of the sensitive-output fallback (TC path)
   size_t scratch_cap = 0;
   TcB tb{};
-  int path = 0;                    // 0 auto (tensor cores for M >= 64), 1 SIMT, 2 tensor cores
+  int path = 0;                    // 0 auto, 1 SIMT, 2 tensor cores (SIMT r^2), 3 tensor cores (one-hot r^2)
   std::vector<double> h_O64, h_alpha64, h_W64;
   // pool state
   int KC = 0;
@@ -253,6 +292,69 @@ as_status upload_gp(as_space* s, cudaStream_t st) {
         s->h_Bch[base + static_cast<size_t>(N) * TC_KCH + off] = lo;
       }
   }
+  // T operand of the one-hot R2 contraction (kernels_tc2.cuh): group g = observed points
+  // [64g, 64g+64) x one-hot columns (f, v); T = 2^s (xt_f[v] - o_jf)^2 in FP64, split hi + lo FP16.
+  // SIMT features: 2^(s/2) xt and 2^(s/2) o in FP32.
+  {
+    Tc2B& t2 = s->t2;
+    const int Kp = t2.Kp, nh = t2.nh, GR = TC2_RG * TC_KCH;
+    const int ngr = (nch + TC2_RG - 1) / TC2_RG;
+    s->h_Tch.assign(static_cast<size_t>(ngr) * 2 * GR * Kp, 0);
+    double tmax = 0.0;
+    for (int f = 0; f < d; ++f) {
+      if (t2.eoff[f] < 0) continue;
+      for (int v = 0; v < H.feat[f].n; ++v)
+        for (int w = 0; w < H.feat[f].n; ++w) {
+          const double q = H.xt64[f * VMAX + v] - H.xt64[f * VMAX + w];
+          tmax = std::max(tmax, q * q);
+        }
+    }
+    int sc = 0;   // even, largest one-hot entry in (2^13, 2^15]
+    if (tmax > 0.0) {
+      while (tmax * std::ldexp(1.0, sc) > 32768.0) sc -= 2;
+      while (tmax * std::ldexp(1.0, sc + 2) <= 32768.0) sc += 2;
+    }
+    t2.r2_scale = static_cast<float>(std::ldexp(1.0, -sc));
+    t2.r_scale = static_cast<float>(std::ldexp(1.0, -sc / 2));
+    auto h16 = [](double x) {
+      const __half h = __double2half(x);
+      uint16_t u;
+      std::memcpy(&u, &h, 2);
+      return u;
+    };
+    auto v16 = [](uint16_t u) {
+      __half h;
+      std::memcpy(&h, &u, 2);
+      return static_cast<double>(__half2float(h));
+    };
+    for (int gi = 0; gi < ngr; ++gi) {
+      uint16_t* base = s->h_Tch.data() + static_cast<size_t>(gi) * 2 * GR * Kp;
+      for (int n = 0; n < GR; ++n) {
+        const int j = gi * GR + n;
+        if (j >= M) continue;
+        for (int f = 0; f < d; ++f) {
+          if (t2.eoff[f] < 0) continue;
+          for (int v = 0; v < H.feat[f].n; ++v) {
+            const double q = H.xt64[f * VMAX + v] - F.X[static_cast<size_t>(j) * d + f];
+            const double x = std::ldexp(q * q, sc);
+            const uint16_t hi = h16(x);
+            const uint32_t o = tc::kmajor_off16(n, t2.eoff[f] + v, Kp / 8) / 2;
+            base[o] = hi;
+            base[static_cast<size_t>(GR) * Kp + o] = h16(x - v16(hi));
+          }
+        }
+      }
+    }
+    const double hs = std::ldexp(1.0, sc / 2);
+    s->h_xh.assign(static_cast<size_t>(4) * VMAX, 0.f);
+    s->h_oh.assign(static_cast<size_t>(std::max(Mp16, 1)) * 4, 0.f);
+    for (int h = 0; h < nh; ++h) {
+      const int f = t2.hf[h];
+      if (f < 0) continue;
+      for (int v = 0; v < H.feat[f].n; ++v) s->h_xh[h * VMAX + v] = static_cast<float>(H.xt64[f * VMAX + v] * hs);
+      for (int j = 0; j < M; ++j) s->h_oh[j * nh + h] = static_cast<float>(F.X[static_cast<size_t>(j) * d + f] * hs);
+    }
+  }
   DevGP& G = s->G;
   G.M = M;
   G.Mp = Mp;
@@ -278,6 +380,12 @@ as_status upload_gp(as_space* s, cudaStream_t st) {
   if ((r = cp(s->d_alpha64, s->h_alpha64.data(), s->h_alpha64.size() * 8)) != AS_OK) return r;
   if ((r = cp(s->d_W64, s->h_W64.data(), s->h_W64.size() * 8)) != AS_OK) return r;
   if ((r = cp(s->d_Bch, s->h_Bch.data(), s->h_Bch.size() * 4)) != AS_OK) return r;
+  if ((r = cp(s->d_Tch, s->h_Tch.data(), s->h_Tch.size() * 2)) != AS_OK) return r;
+  if ((r = cp(s->d_xh, s->h_xh.data(), s->h_xh.size() * 4)) != AS_OK) return r;
+  if ((r = cp(s->d_oh, s->h_oh.data(), s->h_oh.size() * 4)) != AS_OK) return r;
+  s->t2.tch = s->d_Tch;
+  s->t2.xh = s->d_xh;
+  s->t2.oh = s->d_oh;
   s->tb.chunks = s->d_Bch;
   CUDA_TRY(cudaStreamSynchronize(st));  // staging vectors may be reused by the next observe()
   G.O = s->d_O;
@@ -309,10 +417,14 @@ as_status ensure_lists(as_space* s, int grid) {
 
 as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStream_t st) {
   const bool gp = (a.acq != AS_ACQ_SIM) && s->G.M > 0;
-  const bool use_tc = gp && (s->path == 2 || (s->path == 0 && s->G.M >= 64));
   const int P = next_pow2_h(s->KC + SCORE_THREADS);
+  const bool tc2_fits = tc2_smem_bytes(s->tb.Mp16, s->t2.Kp, s->t2.nh, P) <= static_cast<size_t>(s->smem_optin);
+  const bool use_tc2 = gp && (s->path == 3 || (s->path == 0 && s->G.M >= 64 && tc2_fits && s->tc2_auto));
+  const bool use_tc = !use_tc2 && gp && (s->path == 2 || (s->path == 0 && s->G.M >= 64));
   size_t smem = 0;
-  if (use_tc) {
+  if (use_tc2) {
+    smem = tc2_smem_bytes(s->tb.Mp16, s->t2.Kp, s->t2.nh, P);
+  } else if (use_tc) {
     smem = tc_smem_bytes(s->tb.Mp16, s->G.DP, s->H.d, P);
   } else {
     smem = score_smem_bytes(gp ? s->G.Mp : 0, gp ? s->G.DP : 0, s->H.d, P);
@@ -323,7 +435,11 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
   int grid = 0;
   if (a.count > 0) {
     int occ = 1;
-    if (use_tc) {
+    if (use_tc2) {
+      CUDA_TRY(cudaFuncSetAttribute(tc2_kernel_for(s->G.kernel, s->t2.nh), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+      occ = 1;
+    } else if (use_tc) {
       CUDA_TRY(cudaFuncSetAttribute(tc_kernel_for(s->G.DP, s->G.kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
       occ = 1;
@@ -340,7 +456,7 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
   }
   as_status r = ensure_lists(s, std::max(grid, 1));
   if (r != AS_OK) return r;
-  if (use_tc && a.d_scores && a.acq == AS_ACQ_EI) {
+  if ((use_tc || use_tc2) && a.d_scores && a.acq == AS_ACQ_EI) {
     const size_t need = static_cast<size_t>(std::max(grid, 1)) * TC_EPI_WARPS * std::max(s->tb.Mp16, 1);
     if (need > s->scratch_cap) {
       if (s->d_scratch) cudaFree(s->d_scratch);
@@ -363,7 +479,11 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
   DevGP G = s->G;
   if (s->timing) CUDA_TRY(cudaEventRecord(s->ev[0], st));
   if (grid > 0) {
-    if (use_tc) {
+    if (use_tc2) {
+      TcB tb = s->tb;
+      tb.scratch = s->d_scratch;
+      tc2_kernel_for(s->G.kernel, s->t2.nh)<<<grid, TC_WARPS * 32 + 32, smem, st>>>(s->D, G, A, out, tb, s->t2);
+    } else if (use_tc) {
       TcB tb = s->tb;
       tb.scratch = s->d_scratch;
       tc_kernel_for(s->G.DP, s->G.kernel)<<<grid, TC_WARPS * 32 + 32, smem, st>>>(s->D, G, A, out, tb);
@@ -464,6 +584,34 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
     return fail(static_cast<as_status>(st.code), st.msg);
   }
   s->device = cuda_device;
+  {
+    // one-hot layout of the R2 contraction (kernels_tc2.cuh): column of (f, v) = eoff[f] + v.
+    // The widest features move to the SIMT side (at most 4) while the one-hot width exceeds
+    // TC2_KPMAX; their count is padded to 0 / 2 / 4 with a zero feature (hf = -1).
+    Tc2B& t2 = s->t2;
+    const int d = s->H.d;
+    std::vector<bool> simt(d, false);
+    int K = 0;
+    for (int f = 0; f < d; ++f) K += s->H.feat[f].n;
+    int nh = 0;
+    for (int f = 0; f < 4; ++f) t2.hf[f] = -1;
+    while (K > TC2_KPMAX && nh < 4) {
+      int best = -1;
+      for (int f = 0; f < d; ++f)
+        if (!simt[f] && (best < 0 || s->H.feat[f].n > s->H.feat[best].n)) best = f;
+      if (best < 0) break;
+      simt[best] = true;
+      t2.hf[nh++] = best;
+      K -= s->H.feat[best].n;
+    }
+    t2.nh = nh == 0 ? 0 : (nh <= 2 ? 2 : 4);
+    K = 0;
+    for (int f = 0; f < DMAX; ++f) {
+      t2.eoff[f] = (f < d && simt[f]) ? -1 : K;
+      if (f < d && !simt[f]) K += s->H.feat[f].n;
+    }
+    t2.Kp = std::max(16, ((K + 15) / 16) * 16);
+  }
   // GP fit with no observations (prior only)
   gp_fit(s->H, {}, {}, {}, {}, s->fit);
   s->G = DevGP{};
@@ -538,6 +686,9 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
     if ((r = dalloc(&s->d_Bch, static_cast<size_t>(2) * TC_KCH * (Mc / TC_KCH) * (Mc / TC_KCH + 1) / 2 * TC_KCH,
                     s->owned)) != AS_OK)
       return cleanup(r);
+    if ((r = dalloc(&s->d_Tch, static_cast<size_t>(Mc) * 2 * s->t2.Kp, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = dalloc(&s->d_xh, static_cast<size_t>(4) * VMAX, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = dalloc(&s->d_oh, static_cast<size_t>(Mc) * 4, s->owned)) != AS_OK) return cleanup(r);
     // pool buffers at capacity
     s->KC_max = KC_CAP;
     if ((r = dalloc(&s->d_pool, KC_CAP, s->owned)) != AS_OK) return cleanup(r);
@@ -816,7 +967,8 @@ as_status autoscout_mask_range(as_space* s, uint64_t raw_begin, uint64_t count, 
 }
 
 as_status autoscout_set_path(as_space* s, int32_t path) {
-  if (!s || path < 0 || path > 2) return fail(AS_ERR_INVALID_ARG, "path must be 0 (auto), 1 (SIMT) or 2 (tensor cores)");
+  if (!s || path < 0 || path > 3)
+    return fail(AS_ERR_INVALID_ARG, "path must be 0 (auto), 1 (SIMT), 2 (tensor cores) or 3 (tensor cores, one-hot r^2)");
   s->path = path;
   return AS_OK;
 }

@@ -1,0 +1,609 @@
+// Tensor-core score kernel, second generation: both contractions of the posterior
+// on tcgen05 —
+//   (1) squared distances  R2 = E T^T  (kind::f16, FP32 accumulate): E is the one-hot digit encoding
+//       of the 128 candidates of a tile (exact in FP16), T[j][(f,v)] = 2^s (xt_f[v] - o_jf)^2 split
+//       into two FP16 pieces on the host.  All products are exact and every term is >= 0, so R2 has
+//       FP32-accumulation error only (no cancellation); rows of E are built by the producers.
+//       Features with many values (NH <= 4 of them, chosen on the host to keep the one-hot width
+//       Kp <= 64) are added on the SIMT pipes instead: (x_f - o_jf)^2 in FP32, same 2^s scale.
+//       One R2 MMA group covers 4 K-chunks (N = 64): per-instruction cost is flat below N = 64
+//       (tools/mma_bench.cu), so wide groups are what keeps the tensor pipe and the issuing warp free.
+//   (2) v = L^-1 k  (kind::tf32, 3xTF32 split) exactly as score_tc_kernel (kernels_tc.cuh).
+// The producers therefore no longer evaluate sum_f (x_f - o_jf)^2 on the FP32 pipe (2 d FP32 ops
+// per candidate x observed pair); they read R2 from TMEM and evaluate k(r) only.
+//
+// Warp roles (544 threads, 1 CTA per SM):
+//   warps 0-15  producers: phase 0 (decode + mask + simulator -> queue), publish tile t+1 (meta +
+//               E rows) BEFORE the chunk loop of tile t, so the R2 MMAs of t+1 overlap tile t;
+//               chunk loop: R2 chunk from TMEM -> k -> TF32 hi/lo -> A ring (TMEM); epilogue.
+//   warp 16     MMA issuer + loader (warp-converged, one elected lane issues): R2 chunks RR ahead
+//               of the L^-1 chunks in one instruction stream; bulk copies of the L^-1 and T chunks.
+// TMEM: D [Mp16] | A ring [4 x 32] | R2 ring [2 groups x 64]  (Mp16 <= 256 -> <= 512 columns).
+#pragma once
+#include "kernels_tc.cuh"
+
+namespace as {
+
+constexpr int TC2_RG = 4;                    // K-chunks per R2 group (N = 64)
+constexpr int TC2_RS = 2;                    // R2 group slots in TMEM
+constexpr int TC2_NB = 2;                    // L^-1 chunk ring stages
+constexpr int TC2_NT = 3;                    // T group ring stages
+constexpr int TC2_KPMAX = 64;                // one-hot width the host aims for (features beyond go SIMT)
+
+struct Tc2B {
+  const uint16_t* tch;          // T groups: [ng][2 pieces][64 x Kp] FP16, kmajor_off16 layout
+  const float* xh;              // [NH][VMAX] 2^(s/2) xt of the SIMT features
+  const float* oh;              // [Mp16][NH] 2^(s/2) o of the SIMT features (0 beyond M)
+  int Kp;                       // one-hot width (sum of n_f over one-hot features) padded to 16
+  int nh;                       // SIMT features (0, 2 or 4 after padding with a zero feature)
+  int hf[4];                    // their feature indices (-1 = padding)
+  float r2_scale;               // 2^-s    (R2 in TMEM is 2^s r^2)
+  float r_scale;                // 2^-s/2
+  int eoff[DMAX];               // one-hot column of digit 0 of feature f (-1: SIMT feature)
+};
+
+template <int PW, int KT, int NH>
+__global__ void __launch_bounds__(PW * 32 + 32, 1)
+score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2) {
+  constexpr int TC_PROD_WARPS = PW;
+  constexpr int TC_PROD_THREADS = PW * 32;
+  constexpr int TC_THREADS = TC_PROD_THREADS + 32;
+  constexpr int TC_JQ = TC_PROD_THREADS / TC_ROWS;   // producer threads per candidate
+  constexpr int TC_JPT = TC_KCH / TC_JQ;             // observed points per thread per chunk
+  static_assert(TC_JPT % 4 == 0, "R2 / D reads are 32x32b.x4");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ TopkSmem ts;
+  __shared__ int q_n;
+  __shared__ int tinfo[TC_TI];
+  __shared__ uint32_t tmem_base;
+  __shared__ unsigned long long valid_cta;
+  __shared__ int eoff_s[DMAX];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int Mp16 = TB.Mp16, nch = TB.nch, Kp = T2.Kp;
+  const int ng = (nch + TC2_RG - 1) / TC2_RG;                         // R2 groups per tile
+  const uint32_t A0col = static_cast<uint32_t>(Mp16);                 // TMEM column of A stage 0
+  const uint32_t R0col = A0col + 32u * TC_NA;                         // TMEM column of R2 stage 0
+  const uint32_t b_stage_bytes = 2u * Mp16 * TC_KCH * 4;              // L^-1 hi + lo at the widest chunk
+  const uint32_t t_stage_bytes = 2u * (TC2_RG * TC_KCH) * Kp * 2;     // T: 2 FP16 pieces x 64 points
+  const uint32_t e_bytes = static_cast<uint32_t>(TC_ROWS) * Kp * 2;   // E: 128 rows x Kp FP16
+  unsigned char* p = smem_raw;
+  auto take = [&](size_t bytes) {
+    unsigned char* r = p;
+    p += (bytes + 127) & ~size_t(127);
+    return r;
+  };
+  unsigned char* B0 = take(static_cast<size_t>(TC2_NB) * b_stage_bytes);
+  unsigned char* T0 = take(static_cast<size_t>(TC2_NT) * t_stage_bytes);
+  unsigned char* E0 = take(2ull * e_bytes);
+  float* alpha_s = reinterpret_cast<float*>(take(sizeof(float) * 2 * Mp16));   // (alpha_j, |alpha_j|)
+  float* oh_s = reinterpret_cast<float*>(take(sizeof(float) * (NH > 0 ? NH : 1) * Mp16));
+  float* xh_s = reinterpret_cast<float*>(take(sizeof(float) * (NH > 0 ? NH : 1) * VMAX));
+  float* m_xh = reinterpret_cast<float*>(take(sizeof(float) * (NH > 0 ? NH : 1) * TC_TI * TC_ROWS));
+  DV* q_dv = reinterpret_cast<DV*>(take(sizeof(DV) * TC_QCAP));
+  double* q_m0 = reinterpret_cast<double*>(take(sizeof(double) * TC_QCAP));
+  uint32_t* q_cvi = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_QCAP));
+  uint32_t* q_j = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_QCAP));
+  uint32_t* m_cvi = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_TI * TC_ROWS));
+  uint32_t* m_j = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_TI * TC_ROWS));
+  double* m_m0 = reinterpret_cast<double*>(take(sizeof(double) * TC_TI * TC_ROWS));
+  float* m_part = reinterpret_cast<float*>(take(sizeof(float) * TC_TI * 3 * TC_ROWS));
+  float* vpart = reinterpret_cast<float*>(take(sizeof(float) * 4 * TC_ROWS));
+  uint64_t* arr = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * out.P));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 64));
+  uint64_t* cidx = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * CI));
+  const uint32_t sB0 = tc::smem_u32(B0), sT0 = tc::smem_u32(T0), sE0 = tc::smem_u32(E0);
+  uint64_t* a_full = bars;                     // [NA] count PW
+  uint64_t* a_empty = a_full + TC_NA;          // [NA] commit
+  uint64_t* b_full = a_empty + TC_NA;          // [NB] 1 + tx
+  uint64_t* b_empty = b_full + TC2_NB;         // [NB] commit
+  uint64_t* d_full = b_empty + TC2_NB;         // [1]  commit
+  uint64_t* d_empty = d_full + 1;              // [1]  count PW
+  uint64_t* t_ready = d_empty + 1;             // [TI] count 1 (tile meta + E rows published)
+  uint64_t* r_full = t_ready + TC_TI;          // [RS] commit
+  uint64_t* r_empty = r_full + TC2_RS;         // [RS] count PW
+  uint64_t* x_full = r_empty + TC2_RS;         // [NT] 1 + tx  (T group loaded)
+  uint64_t* x_empty = x_full + TC2_NT;         // [NT] commit
+
+  // ---- setup
+  for (int i = tid; i < Mp16; i += TC_THREADS) {
+    alpha_s[2 * i] = i < G.Mp ? __ldg(G.alpha + i) : 0.f;
+    alpha_s[2 * i + 1] = i < G.Mp ? __ldg(G.aabs + i) : 0.f;
+  }
+  for (int i = tid; i < out.P; i += TC_THREADS) arr[i] = KEY_NONE;
+  if (tid < DMAX) eoff_s[tid] = T2.eoff[tid];
+  for (int i = tid; i < NH * Mp16; i += TC_THREADS) oh_s[i] = __ldg(T2.oh + i);
+  for (int i = tid; i < NH * VMAX; i += TC_THREADS) xh_s[i] = __ldg(T2.xh + i);
+  load_cidx(S, cidx, tid, TC_THREADS);
+  if (tid == 0) {
+    for (int s = 0; s < TC_NA; ++s) {
+      tc::mbar_init(a_full + s, TC_PROD_WARPS);
+      tc::mbar_init(a_empty + s, 1);
+    }
+    for (int s = 0; s < TC2_NB; ++s) {
+      tc::mbar_init(b_full + s, 1);
+      tc::mbar_init(b_empty + s, 1);
+    }
+    tc::mbar_init(d_full, 1);
+    tc::mbar_init(d_empty, TC_PROD_WARPS);
+    for (int s = 0; s < TC_TI; ++s) tc::mbar_init(t_ready + s, 1);
+    for (int s = 0; s < TC2_RS; ++s) {
+      tc::mbar_init(r_full + s, 1);
+      tc::mbar_init(r_empty + s, TC_PROD_WARPS);
+    }
+    for (int s = 0; s < TC2_NT; ++s) {
+      tc::mbar_init(x_full + s, 1);
+      tc::mbar_init(x_empty + s, 1);
+    }
+    tc::mbar_fence_init();
+    ts.n_list = 0;
+    ts.n_add = 0;
+    ts.tau = KEY_NONE;
+    ts.drop = KEY_NONE;
+    q_n = 0;
+    valid_cta = 0;
+  }
+  const uint32_t tmem_cols = 512;
+  if (warp == 0) tc::tmem_alloc(&tmem_base, tmem_cols);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = tmem_base;
+
+  if (warp < TC_PROD_WARPS) {
+    // =========================================================== producers (+ epilogue)
+    const int pt = tid;
+    const int cand = pt & (TC_ROWS - 1);
+    const int jq = pt >> 7;
+    const int quad = warp & 3;
+    const uint32_t sAl = tc::smem_u32(alpha_s);
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+    // k = sf2 poly(a) exp(-a) from R2 = 2^s r^2:  a = sqrt5 r = (sqrt5 2^-s/2) sqrt(R2)  (Matern 5/2),
+    // a = r^2 / 2 = (2^-s / 2) R2 (RBF); exp2 argument folds ln(sf2).
+    const float c_arg = (KT == 0) ? 2.2360679774997896f * T2.r_scale : 0.5f * T2.r2_scale;
+    const float ex_c1 = -c_arg * 1.4426950408889634f;
+    const float ex_c0 = log2f(G.sf2f);
+    double* scratch = TB.scratch + (static_cast<size_t>(blockIdx.x) * TC_EPI_WARPS + (warp & 3)) * Mp16;
+
+    // ---- epilogue of tile u (column blocks < nch - NA were accumulated during the chunk loop)
+    auto epilogue = [&](int u, float vsq_run) {
+      const int us = u % TC_TI;
+      tc::mbar_wait(d_full, u & 1);
+      tc::fence_after_sync();
+      float vsq = vsq_run;
+      const uint32_t taddr = lane_base + TC_JPT * jq;
+      for (int b = (nch > TC_NA ? nch - TC_NA : 0); b < nch; ++b) {
+#pragma unroll
+        for (int h = 0; h < TC_JPT; h += 4) {
+          float v[4];
+          tc::tmem_ld4(taddr + 16 * b + h, v);
+          vsq = fmaf(v[0], v[0], fmaf(v[1], v[1], fmaf(v[2], v[2], fmaf(v[3], v[3], vsq))));
+        }
+      }
+      vpart[jq * TC_ROWS + quad * 32 + lane] = vsq;
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(d_empty);
+      named_sync(1, TC_PROD_THREADS);
+      const int n = tinfo[us];
+      uint64_t key = KEY_NONE;
+      bool sensitive = false;
+      if (pt < TC_ROWS && pt < n) {
+        const int row = pt;
+        const float* mp = m_part + us * 3 * TC_ROWS;
+        const float mu32 = mp[0 * TC_ROWS + row], sb = mp[1 * TC_ROWS + row], kk = mp[2 * TC_ROWS + row];
+        float vv = 0.f;
+#pragma unroll
+        for (int q = 0; q < TC_JQ; ++q) vv += vpart[q * TC_ROWS + row];
+        const double cm0 = m_m0[us * TC_ROWS + row];
+        const float mu = static_cast<float>(cm0 + G.b) + mu32;
+        const float vs = vv;
+        const float s2 = static_cast<float>(G.sf2) - vs;
+        // FP32 k + 3xTF32 contraction: error coefficient 8x the SIMT one
+        const float eps = 8.0f * static_cast<float>(G.eps);
+        const float d_mu = eps * sb + 2e-7f * (1.0f + fabsf(mu));
+        const float ew = eps * static_cast<float>(G.w_fro);
+        const float d_s2 = 2.5f * ew * sqrtf(vs) * sqrtf(kk) + ew * ew * kk + eps * vs + 8.0f * U32 * G.sf2f;
+        const float fstar = static_cast<float>(G.fstar), m0f = static_cast<float>(cm0);
+        float m2;
+        float ub = acquisition32(A.acq, mu - d_mu, s2 + d_s2, m0f, fstar, static_cast<float>(A.xi),
+                                 static_cast<float>(A.kappa), m2);
+        ub += m2;
+        if (A.d_scores) {
+          const double mud = cm0 + G.b + static_cast<double>(mu32);
+          const double s2d = G.sf2 - static_cast<double>(vv);
+          if (A.acq == 0) {
+            if (s2d > 0.0) {
+              const double sg = sqrt(s2d), z = (G.fstar - mud - A.xi) / sg;
+              if (z >= -3.2) {
+                const double Phi = 0.5 * erfc(-z * INV_SQRT2);
+                const double h = exp(-0.5 * z * z) * INV_SQRT_2PI + z * Phi;
+                const double uu = static_cast<double>(U32);
+                // R2 from the tensor cores: mu error model 4u(1 + sb)
+                const double e_s = (1.0 - z * Phi / h) / (2.0 * s2d) * 160.0 * uu * static_cast<double>(vv) +
+                                   Phi / (sg * h) * 4.0 * uu * (1.0 + static_cast<double>(sb));
+                sensitive = e_s > 5e-6;
+              }
+            } else {
+              sensitive = true;
+            }
+          }
+          if (!sensitive)
+            A.d_scores[m_j[us * TC_ROWS + row]] =
+                static_cast<float>(acquisition(A.acq, mud, s2d, cm0, G.fstar, A.xi, A.kappa));
+        }
+        if (!sensitive && ub > -INFINITY) key = make_key(ub, m_cvi[us * TC_ROWS + row]);
+      }
+      if (warp < TC_EPI_WARPS) {
+        unsigned fl = __ballot_sync(0xffffffffu, sensitive);
+        while (fl) {
+          const int src = __ffs(fl) - 1;
+          fl &= fl - 1;
+          const int row = warp * 32 + src;
+          const uint32_t cvi = m_cvi[us * TC_ROWS + row];
+          DV dv;
+          uint32_t act;
+          uint64_t raw;
+          decode_dev(S, cvi, dv, act, raw);
+          double kalpha, vq;
+          posterior64_warp(S, G, dv, lane, scratch, kalpha, vq);
+          if (lane == src) {
+            const double cm0 = m_m0[us * TC_ROWS + row];
+            const double sc = acquisition(A.acq, cm0 + G.b + kalpha, G.sf2 - vq, cm0, G.fstar, A.xi, A.kappa);
+            const double ub = sc + 1e-12 * fmax(1.0, fabs(sc));
+            A.d_scores[m_j[us * TC_ROWS + row]] = static_cast<float>(sc);
+            if (ub > -INFINITY) key = make_key(__double2float_ru(ub), cvi);
+          }
+        }
+      }
+      group_admit(key, arr, ts, out.KC, pt, TC_PROD_THREADS, 1);
+    };
+
+    // ---- phase 0 of one input tile: index -> configuration -> validity -> simulator -> queue
+    const uint64_t ntiles = (A.count + TC_PROD_THREADS - 1) / TC_PROD_THREADS;
+    uint64_t tile_in = blockIdx.x;
+    int head = 0;
+    auto phase0 = [&](uint64_t tile) {
+      const uint64_t j = tile * TC_PROD_THREADS + pt;
+      const bool in = j < A.count;
+      bool ok = false;
+      if (in) {
+        const uint64_t pcvi = (A.mode == 0) ? A.begin + j : feistel_pi(A.fk, A.begin + j);
+        DV dv;
+        uint32_t act;
+        uint64_t raw;
+        decode_dev_idx(S, cidx, pcvi, dv, act, raw);
+        double cost;
+        sim_dev(S, dv, act, cost, ok);
+        if (A.d_raw) A.d_raw[j] = raw;
+        if (!ok && A.d_scores) A.d_scores[j] = -INFINITY;
+        if (ok) {
+          const int slot = atomicAdd(&q_n, 1);
+          q_dv[slot] = dv;
+          q_m0[slot] = log(cost);
+          q_cvi[slot] = static_cast<uint32_t>(pcvi);
+          q_j[slot] = static_cast<uint32_t>(j);
+        }
+      }
+      const unsigned vb = __ballot_sync(0xffffffffu, in && ok);
+      if (lane == 0 && vb) atomicAdd(&valid_cta, static_cast<unsigned long long>(__popc(vb)));
+    };
+    // make at least `need` queued candidates available (or exhaust the input)
+    auto fill = [&](int need) {
+      while (q_n - head < need && tile_in < ntiles) {
+        const int left = q_n - head;
+        if (head > 0) {
+          DV mdv;
+          double mm0 = 0;
+          uint32_t mcvi = 0, mj = 0;
+          if (pt < left) {
+            mdv = q_dv[head + pt];
+            mm0 = q_m0[head + pt];
+            mcvi = q_cvi[head + pt];
+            mj = q_j[head + pt];
+          }
+          named_sync(1, TC_PROD_THREADS);
+          if (pt < left) {
+            q_dv[pt] = mdv;
+            q_m0[pt] = mm0;
+            q_cvi[pt] = mcvi;
+            q_j[pt] = mj;
+          }
+          if (pt == 0) q_n = left;
+          head = 0;
+          named_sync(1, TC_PROD_THREADS);
+        }
+        phase0(tile_in);
+        tile_in += gridDim.x;
+        named_sync(1, TC_PROD_THREADS);
+      }
+    };
+    // publish tile u: meta rows, zeroed partial sums, one-hot rows E[u & 1]; returns n (0 = end)
+    auto publish = [&](int u) -> int {
+      const int avail = q_n - head;
+      const int n = avail >= TC_ROWS ? TC_ROWS : avail;
+      const int us = u % TC_TI;
+      if (n > 0) {
+        if (pt < TC_ROWS) {
+          float* mz = m_part + us * 3 * TC_ROWS;
+          mz[pt] = 0.f;
+          mz[TC_ROWS + pt] = 0.f;
+          mz[2 * TC_ROWS + pt] = 0.f;
+        }
+        if (pt < n) {
+          m_cvi[us * TC_ROWS + pt] = q_cvi[head + pt];
+          m_j[us * TC_ROWS + pt] = q_j[head + pt];
+          m_m0[us * TC_ROWS + pt] = q_m0[head + pt];
+        }
+        unsigned char* E = E0 + (u & 1) * e_bytes;
+        for (uint32_t i = pt; i < e_bytes / 16; i += TC_PROD_THREADS)
+          *reinterpret_cast<uint4*>(E + 16 * i) = make_uint4(0u, 0u, 0u, 0u);
+        named_sync(1, TC_PROD_THREADS);
+        if (cand < n) {
+          const DV cdv = q_dv[head + cand];
+          for (int f = jq; f < S.d; f += TC_JQ) {
+            if (eoff_s[f] < 0) continue;
+            const uint32_t col = static_cast<uint32_t>(eoff_s[f]) + dv_get(cdv, f);
+            *reinterpret_cast<uint16_t*>(E + tc::kmajor_off16(cand, col, Kp / 8)) = 0x3C00;   // FP16 1.0
+          }
+          if (jq < NH) {
+            const int f = T2.hf[jq];
+            m_xh[(us * TC_ROWS + cand) * (NH > 0 ? NH : 1) + jq] = f >= 0 ? xh_s[jq * VMAX + dv_get(cdv, f)] : 0.f;
+          }
+        }
+        tc::fence_proxy_async();   // generic-proxy stores -> visible to the tensor core (async proxy)
+      }
+      named_sync(1, TC_PROD_THREADS);
+      if (pt == 0) {
+        tinfo[us] = n > 0 ? n : -1;
+        tc::mbar_arrive(t_ready + us);
+      }
+      head += n;
+      return n;
+    };
+
+    fill(TC_ROWS);
+    int n_cur = publish(0);
+    uint32_t g = 0;                                   // global chunk counter (A ring)
+    uint32_t gr = 0;                                  // global R2 group counter
+    const uint32_t sOH = tc::smem_u32(oh_s);
+    for (int t = 0; n_cur > 0; ++t) {
+      fill(TC_ROWS);
+      const int n_next = publish(t + 1);
+      // ---- chunk loop: R2 (+ SIMT features) -> k -> A ring
+      float mu_p = 0.f, sb_p = 0.f, kk_p = 0.f, vsq_run = 0.f;
+      const uint32_t dq = lane_base + TC_JPT * jq;
+      unsigned long long xhp[NH > 0 ? NH / 2 : 1];
+#pragma unroll
+      for (int h = 0; h < NH / 2; ++h) {
+        const float* xq = m_xh + ((t % TC_TI) * TC_ROWS + cand) * (NH > 0 ? NH : 1) + 2 * h;
+        xhp[h] = f2_pack(xq[0], xq[1]);
+      }
+      for (int c = 0; c < nch; ++c, ++g) {
+        const int s = g % TC_NA, rs = gr % TC2_RS, cg = c % TC2_RG;
+        const uint32_t a_par = ((g / TC_NA) & 1u) ^ 1u;
+        float rv[TC_JPT];
+        if (cg == 0) tc::mbar_wait(r_full + rs, (gr / TC2_RS) & 1u);
+        tc::fence_after_sync();
+#pragma unroll
+        for (int h = 0; h < TC_JPT; h += 4)
+          tc::tmem_ld4(lane_base + R0col + 64u * rs + 16u * cg + TC_JPT * jq + h, rv + h);
+        if (cg == TC2_RG - 1 || c == nch - 1) {       // R2 group consumed
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(r_empty + rs);
+          ++gr;
+        }
+        const bool a_ready = tc::mbar_test(a_empty + s, a_par);
+        float kh[TC_JPT], kl[TC_JPT];
+#pragma unroll
+        for (int q = 0; q < TC_JPT; ++q) {
+          const int jo = c * TC_KCH + jq * TC_JPT + q;
+          float r2s = rv[q];
+          if (NH > 0) {
+            unsigned long long acc = 0ull;
+#pragma unroll
+            for (int h = 0; h < NH / 2; ++h) {
+              unsigned long long o2;
+              asm volatile("ld.shared.b64 %0, [%1];" : "=l"(o2) : "r"(sOH + 4u * (jo * NH + 2 * h)));
+              const unsigned long long dd = f2_sub(xhp[h], o2);
+              acc = f2_fma(dd, dd, acc);
+            }
+            const float2 a2 = f2_unpack(acc);
+            r2s += a2.x + a2.y;
+          }
+          const float r2 = fmaxf(r2s, 0.f);
+          float arg, poly, ex;
+          if (KT == 0) {
+            const float r = tc::sqrt_approx_ftz(r2);
+            arg = c_arg * r;
+            poly = fmaf(arg, fmaf(arg, 0.33333333333333333f, 1.0f), 1.0f);
+            ex = tc::ex2_approx(fmaf(r, ex_c1, ex_c0));
+          } else {
+            arg = c_arg * r2;
+            poly = 1.0f;
+            ex = tc::ex2_approx(fmaf(r2, ex_c1, ex_c0));
+          }
+          const float kval = poly * ex;
+          const float cc = fmaf(kval, arg, kval);
+          float al, aa;
+          tc::lds_f32x2(sAl + 8 * jo, al, aa);
+          mu_p = fmaf(kval, al, mu_p);
+          sb_p = fmaf(cc, aa, sb_p);
+          kk_p = fmaf(cc, cc, kk_p);
+          tc::split_tf32_fast(kval, kh[q], kl[q]);
+        }
+        if (!a_ready) tc::mbar_wait(a_empty + s, a_par);
+        tc::fence_after_sync();
+        if (c >= TC_NA) {
+#pragma unroll
+          for (int h = 0; h < TC_JPT; h += 4) {
+            float v[4];
+            tc::tmem_ld4(dq + 16 * (c - TC_NA) + h, v);
+            vsq_run = fmaf(v[0], v[0], fmaf(v[1], v[1], fmaf(v[2], v[2], fmaf(v[3], v[3], vsq_run))));
+          }
+        }
+        const uint32_t acol = lane_base + A0col + 32u * s + jq * TC_JPT;
+#pragma unroll
+        for (int v4 = 0; v4 < TC_JPT / 4; ++v4) {
+          tc::tmem_st4(acol + 4 * v4, kh[4 * v4], kh[4 * v4 + 1], kh[4 * v4 + 2], kh[4 * v4 + 3]);
+          tc::tmem_st4(acol + 16 + 4 * v4, kl[4 * v4], kl[4 * v4 + 1], kl[4 * v4 + 2], kl[4 * v4 + 3]);
+        }
+        tc::tmem_st_wait();
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(a_full + s);
+      }
+      float* mp = m_part + (t % TC_TI) * 3 * TC_ROWS;
+      atomicAdd(mp + cand, mu_p);
+      atomicAdd(mp + TC_ROWS + cand, sb_p);
+      atomicAdd(mp + 2 * TC_ROWS + cand, kk_p);
+      epilogue(t, vsq_run);
+      named_sync(1, TC_PROD_THREADS);
+      n_cur = n_next;
+    }
+    // ---- CTA list
+    named_sync(1, TC_PROD_THREADS);
+    const int n = ts.n_list;
+    uint64_t* dst = out.lists + static_cast<size_t>(blockIdx.x) * out.KC;
+    for (int i = pt; i < n; i += TC_PROD_THREADS) dst[i] = arr[i];
+    if (pt == 0) {
+      out.counts[blockIdx.x] = n;
+      out.drop[blockIdx.x] = ts.drop;
+    }
+  } else {
+    // =========================================================== MMA issuer + loader
+    // The whole warp runs this loop in lock-step (warp-uniform state); one elected lane issues the
+    // MMAs / commits (elect.sync inside the asm) and lane 0 the bulk copies.
+    uint32_t g = 0, gl = 0;          // L^-1 chunks consumed / loaded
+    uint32_t x = 0, xl = 0;          // R2 chunks issued / T chunks loaded
+    int lc = 0, xc = 0;              // chunk index of the next L^-1 / T load
+    int ru = 0, rgi = 0;             // tile / group index of the next R2 group
+    int known = 0, end_tile = 0x7fffffff;
+    auto tile_exists = [&](int u) -> bool {
+      while (known <= u && known < end_tile) {
+        tc::mbar_wait(t_ready + (known % TC_TI), (known / TC_TI) & 1);
+        if (tinfo[known % TC_TI] < 0) end_tile = known;
+        ++known;
+      }
+      return u < end_tile;
+    };
+    auto load_L = [&]() {
+      const int s = gl % TC2_NB;
+      tc::mbar_wait(b_empty + s, ((gl / TC2_NB) & 1u) ^ 1u);
+      if (lane == 0) {
+        const uint32_t bytes = 2u * (Mp16 - lc * TC_KCH) * TC_KCH * 4;
+        tc::mbar_arrive_expect_tx(b_full + s, bytes);
+        tc::bulk_g2s(B0 + static_cast<size_t>(s) * b_stage_bytes, TB.chunks + TB.off[lc], bytes, b_full + s);
+      }
+      ++gl;
+      if (++lc == nch) lc = 0;
+    };
+    auto load_T = [&]() {
+      const int s = xl % TC2_NT;
+      tc::mbar_wait(x_empty + s, ((xl / TC2_NT) & 1u) ^ 1u);
+      if (lane == 0) {
+        tc::mbar_arrive_expect_tx(x_full + s, t_stage_bytes);
+        tc::bulk_g2s(T0 + static_cast<size_t>(s) * t_stage_bytes,
+                     T2.tch + static_cast<size_t>(xc) * (t_stage_bytes / 2), t_stage_bytes, x_full + s);
+      }
+      ++xl;
+      if (++xc == ng) xc = 0;
+    };
+    __syncwarp();
+    const uint32_t sbo16 = (Kp / 8) * 128;
+    const uint64_t dE = tc::sdesc(sE0, 128, sbo16), dT = tc::sdesc(sT0, 128, sbo16);
+    const uint64_t dB = tc::sdesc(sB0, 128, (TC_KCH / 4) * 128);
+    const uint32_t piece16 = ((TC2_RG * TC_KCH) * Kp * 2) >> 4;   // descriptor units (16 B)
+    const uint32_t idesc_r = tc::idesc_f16(TC_ROWS, TC2_RG * TC_KCH);
+    const int ksteps_r = Kp / 16;
+    // R2 group x: D_R[x % RS] = E[tile & 1] T_g^T  (N = 64; 2 FP16 pieces x Kp/16 k-steps)
+    auto issue_R = [&]() -> bool {
+      if (!tile_exists(ru)) return false;
+      const int rs = x % TC2_RS, st_ = x % TC2_NT;
+      tc::mbar_wait(r_empty + rs, ((x / TC2_RS) & 1u) ^ 1u);
+      tc::mbar_wait(x_full + st_, (x / TC2_NT) & 1u);
+      tc::fence_after_sync();
+      const uint32_t dR = tmem + R0col + 64u * rs;
+      const uint64_t ad = dE + (((ru & 1) * e_bytes) >> 4), bd = dT + ((st_ * t_stage_bytes) >> 4);
+      for (int ks = 0; ks < ksteps_r; ++ks) {
+        tc::mma_f16_w(dR, ad + 16 * ks, bd + 16 * ks, idesc_r, ks > 0 ? 1u : 0u);
+        tc::mma_f16_w(dR, ad + 16 * ks, bd + piece16 + 16 * ks, idesc_r, 1u);
+      }
+      tc::mma_commit_w(r_full + rs);
+      tc::mma_commit_w(x_empty + st_);
+      ++x;
+      if (++rgi == ng) {
+        rgi = 0;
+        ++ru;
+      }
+      load_T();                                        // refill the slot of group x-2, NT-1 ahead
+      return true;
+    };
+    if (tile_exists(0)) {
+      for (int i = 0; i < TC2_NB - 1; ++i) load_L();
+      for (int i = 0; i < TC2_NT - 1; ++i) load_T();
+    }
+    const uint32_t sbo = (TC_KCH / 4) * 128;
+    (void)sbo;
+    for (int t = 0; tile_exists(t); ++t) {
+      tc::mbar_wait(d_empty, (t & 1) ^ 1);
+      tc::fence_after_sync();
+      for (int c = 0; c < nch; ++c, ++g) {
+        // R2 lookahead: the producers may run NA chunks ahead of M(g), so the group of chunk
+        // c + NA must be issued before M(g); never beyond the next tile (tile t+2 is published
+        // only after the epilogue of tile t, which needs MMAs not issued yet).
+        {
+          const int cn = c + TC_NA;
+          const uint32_t target = cn < nch ? static_cast<uint32_t>(t * ng + cn / TC2_RG)
+                                           : static_cast<uint32_t>((t + 1) * ng + min((cn - nch) / TC2_RG, ng - 1));
+          while (x <= target && issue_R()) {
+          }
+        }
+        const int sa = g % TC_NA, sbb = g % TC2_NB;
+        tc::mbar_wait(a_full + sa, (g / TC_NA) & 1);
+        tc::mbar_wait(b_full + sbb, (g / TC2_NB) & 1);
+        tc::fence_after_sync();
+        const int N = Mp16 - c * TC_KCH;
+        const uint32_t idesc = tc::idesc_tf32(TC_ROWS, N);
+        const uint32_t a_h = tmem + A0col + 32u * sa, a_l = a_h + 16;
+        const uint64_t bh = dB + ((sbb * b_stage_bytes) >> 4);
+        const uint64_t bl = bh + ((N * TC_KCH * 4) >> 4);
+        const uint32_t d = tmem + c * TC_KCH;
+#pragma unroll
+        for (int ks = 0; ks < TC_KCH / 8; ++ks) {
+          tc::mma_tf32_ts_w(d, a_h + 8 * ks, bh + 16 * ks, idesc, (c > 0 || ks > 0) ? 1u : 0u);
+          tc::mma_tf32_ts_w(d, a_h + 8 * ks, bl + 16 * ks, idesc, 1u);
+          tc::mma_tf32_ts_w(d, a_l + 8 * ks, bh + 16 * ks, idesc, 1u);
+        }
+        tc::mma_commit_w(a_empty + sa);
+        tc::mma_commit_w(b_empty + sbb);
+        load_L();
+      }
+      tc::mma_commit_w(d_full);
+    }
+    // drain bulk copies still in flight before the CTA exits
+    while (g < gl) {
+      tc::mbar_wait(b_full + (g % TC2_NB), (g / TC2_NB) & 1);
+      ++g;
+    }
+    while (x < xl) {
+      tc::mbar_wait(x_full + (x % TC2_NT), (x / TC2_NT) & 1);
+      ++x;
+    }
+    __syncwarp();
+  }
+  // ---- teardown
+  tc::fence_before_sync();
+  __syncthreads();
+  if (tid == 0 && valid_cta) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(out.valid), valid_cta);
+    if (A.d_valid_count) atomicAdd(reinterpret_cast<unsigned long long*>(A.d_valid_count), valid_cta);
+  }
+  if (warp == 0) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(tmem, tmem_cols);
+  }
+}
+
+}  // namespace as

@@ -85,7 +85,7 @@ def test_full_space_sim_mask_raw(name, M):
     check_topk(top, oracle_topk(rec, ref, 32))
 
 
-@pytest.mark.parametrize("path", ["simt", "tc"])
+@pytest.mark.parametrize("path", ["simt", "tc", "tc2"])
 @pytest.mark.parametrize("name,M", FULL)
 def test_full_space_posterior(name, M, path):
     o, fit, rec, sp, batch = case(name, M, path=path)
@@ -102,7 +102,7 @@ def test_full_space_posterior(name, M, path):
     check_topk(top1, oracle_topk(rec, oracle_scores(o, fit, rec, "lcb", kappa=1.0), 32))
 
 
-@pytest.mark.parametrize("path", ["simt", "tc"])
+@pytest.mark.parametrize("path", ["simt", "tc", "tc2"])
 @pytest.mark.parametrize("name,M", FULL)
 def test_full_space_ei(name, M, path):
     o, fit, rec, sp, batch = case(name, M, path=path)
@@ -117,11 +117,15 @@ def test_full_space_ei(name, M, path):
 @pytest.mark.parametrize("name,M,mode,begin,count,seed,path", [
     ("C4", 256, "sample", 0, 1 << 16, 0, "tc"),         # bench shape (M=256), 65,536 sampled candidates
     ("C4", 256, "sample", 0, 1 << 16, 0, "simt"),       # same inputs, SIMT posterior
+    ("C4", 256, "sample", 0, 1 << 16, 0, "tc2"),        # same inputs, one-hot r^2 on tensor cores
+    ("C4", 65, "range", 100_000_000, 30000, 0, "tc"),   # SIMT-r^2 tensor-core kernel at a ragged M
     ("C4", 64, "sample", 12345, 20000, 7, "auto"),      # M at the 64 boundary (tensor cores)
     ("C4", 65, "range", 100_000_000, 30000, 0, "auto"), # M not a multiple of 16, ragged RANGE window
     ("C5", 128, "range", 1_234_567, 50000, 0, "auto"),  # C5 bench M, RANGE window
     ("C5", 1, "sample", 0, 10000, 3, "auto"),           # M = 1 (SIMT)
     ("C5", 1, "sample", 0, 10000, 3, "tc"),             # M = 1 on tensor cores (one 16-wide chunk)
+    ("C5", 1, "sample", 0, 10000, 3, "tc2"),            # M = 1, one-hot r^2 (R2 lookahead limited to 1 chunk)
+    ("C5", 20, "sample", 77, 30000, 5, "tc2"),          # 2 chunks per tile: R2 lookahead spans tiles
 ])
 def test_large_space_windows(name, M, mode, begin, count, seed, path):
     o, fit, rec, sp, batch = case(name, M, mode, begin, count, seed, path=path)

@@ -11,7 +11,7 @@ for name, M, mode, begin, count in [("C1", 16, "range", 0, 176), ("C2", 64, "ran
     o = oracle_space(name)
     raws, costs = observed(o, M, 0)
     res = {}
-    for path in ("simt", "tc"):
+    for path in ("simt", "tc", "tc2"):
         sp = Space(f"spaces/{name}.json", 0)
         sp.observe(raws, costs)
         sp.set_path(path)
@@ -24,9 +24,11 @@ for name, M, mode, begin, count in [("C1", 16, "range", 0, 176), ("C2", 64, "ran
             res[(path, acq, kap)] = (sc.cpu().numpy().copy(), top, time.time() - t0)
     for acq, kap in (("lcb", 0.0), ("lcb", 1.0), ("ei", None)):
         a, ta, _ = res[("simt", acq, kap)]
-        b, tb, _ = res[("tc", acq, kap)]
-        fin = np.isfinite(a)
-        same_mask = np.array_equal(fin, np.isfinite(b))
-        d = np.abs(a[fin] - b[fin]).max() if fin.any() else 0
-        print(f"{name} M={M} {acq} k={kap}: mask_equal={same_mask} max|simt-tc|={d:.3e} top_equal={[r for r,_ in ta]==[r for r,_ in tb]}", flush=True)
+        for other in ("tc", "tc2"):
+            b, tb, _ = res[(other, acq, kap)]
+            fin = np.isfinite(a)
+            same_mask = np.array_equal(fin, np.isfinite(b))
+            d = np.abs(a[fin] - b[fin]).max() if fin.any() else 0
+            print(f"{name} M={M} {acq} k={kap}: mask_equal={same_mask} max|simt-{other}|={d:.3e} "
+                  f"top_equal={[r for r,_ in ta]==[r for r,_ in tb]}", flush=True)
 print("TC CHECK DONE")
