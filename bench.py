@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--path", default="auto", choices=["auto", "simt", "tc", "tc2"],
+                    help="posterior kernel override (A/B and profiling only; the default is the library's choice)")
     return ap.parse_args()
 
 
@@ -232,6 +234,7 @@ def run_ours(args):
     doc = load_doc(cfg)
     b = doc["bench"]
     sp = Space(os.path.join(ROOT, "spaces", f"{cfg}.json"), local)
+    sp.set_path(args.path)
     M, k, acq, mode = b["M"], b["k"], b["acq"], b["mode"]
     raws, costs = observed_with_library(sp, M, 0)
     sp.observe(raws, costs)

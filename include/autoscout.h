@@ -159,6 +159,11 @@ as_status autoscout_set_path(as_space* s, int32_t path);
  * recorded when `timing` was enabled), for the roofline report in bench.py. */
 as_status autoscout_set_timing(as_space* s, int32_t enable);
 as_status autoscout_last_kernel_ms(as_space* s, double* score_ms, double* merge_ms);
+/* Split of the last timed launch on the one-hot tensor-core path (set_path 3 / auto): device time
+ * of the candidate-generation kernels (decode + mask + simulator -> compact list) and of the
+ * tensor-core score kernels, summed over the batch's slices.  Both are 0 for
+ * the other paths.  AS_ERR_STATE if timing was off. */
+as_status autoscout_last_phase_ms(as_space* s, double* gen_ms, double* score_ms);
 
 const char* autoscout_last_error(void); /* thread-local */
 

@@ -35,7 +35,7 @@ EXPORTS = ["autoscout_space_create", "autoscout_space_destroy", "autoscout_space
            "autoscout_topk_pool", "autoscout_topk_merge", "autoscout_decode", "autoscout_cvi_to_raw",
            "autoscout_sample_to_cvi", "autoscout_simulate", "autoscout_mask_range", "autoscout_set_path",
            "autoscout_set_timing",
-           "autoscout_last_kernel_ms", "autoscout_last_error"]
+           "autoscout_last_kernel_ms", "autoscout_last_phase_ms", "autoscout_last_error"]
 
 
 class SpaceInfo(ctypes.Structure):
@@ -84,6 +84,7 @@ def _load():
         "autoscout_set_path": ([P, I32], I32),
         "autoscout_set_timing": ([P, I32], I32),
         "autoscout_last_kernel_ms": ([P, pD, pD], I32),
+        "autoscout_last_phase_ms": ([P, pD, pD], I32),
         "autoscout_last_error": ([], ctypes.c_char_p),
     }
     for name, (args, res) in sig.items():
@@ -253,6 +254,12 @@ class Space:
     def last_kernel_ms(self):
         a, b = ctypes.c_double(), ctypes.c_double()
         _check(_LIB.autoscout_last_kernel_ms(self.h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def last_phase_ms(self):
+        """(generate kernels ms, tensor-core score kernels ms) of the last timed launch (one-hot path)."""
+        a, b = ctypes.c_double(), ctypes.c_double()
+        _check(_LIB.autoscout_last_phase_ms(self.h, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
 
 

@@ -86,31 +86,9 @@ size_t tc_smem_bytes(int Mp16, int DP, int d, int P) {
   return s;
 }
 
-// one-hot R2 kernel (kernels_tc2.cuh): B ring (2) + T ring (3) + E (2) + the common state
-size_t tc2_smem_bytes(int Mp16, int Kp, int nh, int P) {
-  auto r128 = [](size_t b) { return (b + 127) & ~size_t(127); };
-  const int nh1 = nh > 0 ? nh : 1;
-  size_t s = 0;
-  s += r128(static_cast<size_t>(TC2_NB) * 2ull * Mp16 * TC_KCH * 4);
-  s += r128(static_cast<size_t>(TC2_NT) * 2ull * (TC2_RG * TC_KCH) * Kp * 2);
-  s += r128(2ull * TC_ROWS * Kp * 2);
-  s += r128(sizeof(float) * 2 * Mp16);
-  s += r128(sizeof(float) * nh1 * Mp16);
-  s += r128(sizeof(float) * nh1 * VMAX);
-  s += r128(sizeof(float) * nh1 * TC_TI * TC_ROWS);
-  s += r128(sizeof(DV) * TC_QCAP);
-  s += r128(sizeof(double) * TC_QCAP);
-  s += 2 * r128(sizeof(uint32_t) * TC_QCAP);
-  s += 2 * r128(sizeof(uint32_t) * TC_TI * TC_ROWS);
-  s += r128(sizeof(double) * TC_TI * TC_ROWS);
-  s += r128(sizeof(float) * TC_TI * 3 * TC_ROWS);
-  s += r128(sizeof(float) * 4 * TC_ROWS);
-  s += r128(sizeof(uint64_t) * P);
-  s += r128(sizeof(uint64_t) * 64);
-  s += r128(sizeof(uint64_t) * CI);
-  return s;
-}
-using Tc2KernelFn = void (*)(DevSpace, DevGP, BatchArgs, CtaOut, TcB, Tc2B);
+// one-hot R2 kernel (kernels_tc2.cuh): fixed arrays + B ring + T ring + E (2) + top-k' keys
+size_t tc2_smem_bytes(int Mp16, int Kp, int /*nh*/, int P) { return tc2_smem_total(Mp16, Kp, P); }
+using Tc2KernelFn = void (*)(DevSpace, DevGP, BatchArgs, CtaOut, TcB, Tc2B, CandList);
 template <int KT>
 Tc2KernelFn tc2_kernel_kt(int nh) {
   return nh == 0 ? score_tc2_kernel<16, KT, 0> : (nh == 2 ? score_tc2_kernel<16, KT, 2> : score_tc2_kernel<16, KT, 4>);
@@ -202,7 +180,11 @@ struct as_space {
   uint16_t* d_Tch = nullptr;
   float *d_xh = nullptr, *d_oh = nullptr;
   Tc2B t2{};
-  bool tc2_auto = false;           // auto path prefers the one-hot kernel (set once it is the faster one)
+  CandList list{};                 // compact valid-candidate list of one slice (kernels_gen.cuh)
+  size_t list_cap = 0;
+  std::vector<cudaEvent_t> sev;    // per-slice events: [gen start, gen end / score start, score end]
+  int sev_used = 0;
+  bool tc2_auto = true;            // auto path prefers the one-hot kernel when its shared memory fits
   double* d_scratch = nullptr;     // FP64 scratch of the sensitive-output fallback (TC path)
   size_t scratch_cap = 0;
   TcB tb{};
@@ -338,7 +320,10 @@ as_status upload_gp(as_space* s, cudaStream_t st) {
             const double q = H.xt64[f * VMAX + v] - F.X[static_cast<size_t>(j) * d + f];
             const double x = std::ldexp(q * q, sc);
             const uint16_t hi = h16(x);
-            const uint32_t o = tc::kmajor_off16(n, t2.eoff[f] + v, Kp / 8) / 2;
+            // row order inside the group: producer thread jq reads its 4 points of each of the 4
+            // chunks as 16 contiguous accumulator columns (kernels_tc2.cuh)
+            const int np = 16 * ((n % 16) / 4) + 4 * (n / 16) + (n % 4);
+            const uint32_t o = tc::kmajor_off16(np, t2.eoff[f] + v, Kp / 8) / 2;
             base[o] = hi;
             base[static_cast<size_t>(GR) * Kp + o] = h16(x - v16(hi));
           }
@@ -415,14 +400,98 @@ as_status ensure_lists(as_space* s, int grid) {
   return AS_OK;
 }
 
+// One-hot tensor-core path: the batch is processed in slices of up to 2^25 candidates; per slice
+// the generate kernel writes the compact list of valid candidates and the score kernel consumes
+// it (one CTA per SM), then the pool merge.
+constexpr uint64_t GEN_SLICE = 1ull << 25;
+constexpr int SEV_MAX = 3 * 64;
+
+as_status ensure_cand_list(as_space* s, size_t cap) {
+  if (cap <= s->list_cap) return AS_OK;
+  CandList& L = s->list;
+  void* ptrs[] = {L.cvi, L.j, L.m0, L.dv0, L.dv1, L.dv2, L.count};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  L = CandList{};
+  const size_t n = cap + TC_ROWS;   // padding: the last tile's staging copy is rounded up
+  CUDA_TRY(cudaMalloc(&L.cvi, n * 4));
+  CUDA_TRY(cudaMalloc(&L.j, n * 4));
+  CUDA_TRY(cudaMalloc(&L.m0, n * 8));
+  CUDA_TRY(cudaMalloc(&L.dv0, n * 8));
+  CUDA_TRY(cudaMalloc(&L.dv1, n * 8));
+  CUDA_TRY(cudaMalloc(&L.dv2, n * 8));
+  CUDA_TRY(cudaMalloc(&L.count, sizeof(unsigned long long)));
+  s->list_cap = cap;
+  return AS_OK;
+}
+
+as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, bool reset, cudaStream_t st) {
+  s->sev_used = 0;
+  if (s->timing) CUDA_TRY(cudaEventRecord(s->ev[0], st));
+  const uint64_t count = A.count;
+  const int grid = s->n_sm;
+  as_status r = ensure_lists(s, grid);
+  if (r != AS_OK) return r;
+  out.lists = s->d_lists;            // ensure_lists may have reallocated them
+  out.counts = s->d_counts;
+  out.drop = s->d_drops;
+  if (count > 0) {
+    r = ensure_cand_list(s, static_cast<size_t>(std::min<uint64_t>(count, GEN_SLICE)));
+    if (r != AS_OK) return r;
+  }
+  const int ci_n = std::min(s->H.n_struct, GEN_CI_MAX);
+  int occ = 1;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gen_kernel, GEN_THREADS, ci_n * 8));
+  const int grid_gen = s->n_sm * std::max(occ, 1);
+  auto k2 = tc2_kernel_for(s->G.kernel, s->t2.nh);
+  CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  TcB tb = s->tb;
+  tb.scratch = s->d_scratch;
+  const int P2 = next_pow2_h(s->KC + MERGE_THREADS);
+  CUDA_TRY(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P2 * 8));
+  const uint64_t n_slices = count == 0 ? 1 : (count + GEN_SLICE - 1) / GEN_SLICE;
+  for (uint64_t sl = 0; sl < n_slices; ++sl) {
+    const uint64_t j0 = sl * GEN_SLICE, nj = std::min<uint64_t>(GEN_SLICE, count - j0);
+    const bool ev = s->timing && s->sev_used + 3 <= static_cast<int>(s->sev.size());
+    if (nj > 0) {
+      CUDA_TRY(cudaMemsetAsync(s->list.count, 0, sizeof(unsigned long long), st));
+      if (ev) CUDA_TRY(cudaEventRecord(s->sev[s->sev_used], st));
+      gen_kernel<<<grid_gen, GEN_THREADS, ci_n * 8, st>>>(s->D, A, j0, nj, s->list, ci_n,
+                                                           reinterpret_cast<unsigned long long*>(s->d_valid));
+      CUDA_TRY(cudaGetLastError());
+      ++s->n_launches;
+      if (ev) CUDA_TRY(cudaEventRecord(s->sev[s->sev_used + 1], st));
+      k2<<<grid, TC_WARPS * 32 + 32, smem, st>>>(s->D, s->G, A, out, tb, s->t2, s->list);
+      CUDA_TRY(cudaGetLastError());
+      ++s->n_launches;
+      if (ev) {
+        CUDA_TRY(cudaEventRecord(s->sev[s->sev_used + 2], st));
+        s->sev_used += 3;
+      }
+    }
+    if (sl + 1 == n_slices && s->timing) CUDA_TRY(cudaEventRecord(s->ev[1], st));
+    merge_kernel<<<1, MERGE_THREADS, P2 * 8, st>>>(s->d_lists, s->d_counts, s->d_drops, nj > 0 ? grid : 0, s->KC,
+                                                   s->d_pool, s->d_pool_n, s->d_cut, (reset && sl == 0) ? 1 : 0, P2);
+    CUDA_TRY(cudaGetLastError());
+    ++s->n_launches;
+  }
+  if (s->timing) {
+    CUDA_TRY(cudaEventRecord(s->ev[2], st));
+    s->ev_recorded = true;
+  }
+  return AS_OK;
+}
+
 as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStream_t st) {
   const bool gp = (a.acq != AS_ACQ_SIM) && s->G.M > 0;
-  const int P = next_pow2_h(s->KC + SCORE_THREADS);
-  const bool tc2_fits = tc2_smem_bytes(s->tb.Mp16, s->t2.Kp, s->t2.nh, P) <= static_cast<size_t>(s->smem_optin);
+  int P = next_pow2_h(s->KC + SCORE_THREADS);
+  const int P_tc2 = next_pow2_h(s->KC + TC_ROWS);   // one 128-row tile is admitted at a time
+  const bool tc2_fits = tc2_smem_bytes(s->tb.Mp16, s->t2.Kp, s->t2.nh, P_tc2) <= static_cast<size_t>(s->smem_optin);
   const bool use_tc2 = gp && (s->path == 3 || (s->path == 0 && s->G.M >= 64 && tc2_fits && s->tc2_auto));
   const bool use_tc = !use_tc2 && gp && (s->path == 2 || (s->path == 0 && s->G.M >= 64));
   size_t smem = 0;
   if (use_tc2) {
+    P = P_tc2;
     smem = tc2_smem_bytes(s->tb.Mp16, s->t2.Kp, s->t2.nh, P);
   } else if (use_tc) {
     smem = tc_smem_bytes(s->tb.Mp16, s->G.DP, s->H.d, P);
@@ -454,6 +523,7 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
     const uint64_t g = std::min<uint64_t>(static_cast<uint64_t>(s->n_sm) * occ, ntiles);
     grid = static_cast<int>(g);
   }
+  if (use_tc2) grid = s->n_sm;        // persistent: one CTA per SM over the candidate lists
   as_status r = ensure_lists(s, std::max(grid, 1));
   if (r != AS_OK) return r;
   if ((use_tc || use_tc2) && a.d_scores && a.acq == AS_ACQ_EI) {
@@ -477,13 +547,11 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
   A.d_valid_count = a.d_valid_count;
   CtaOut out{s->d_lists, s->d_counts, s->d_drops, s->d_valid, s->KC, P};
   DevGP G = s->G;
+  if (use_tc2) return launch_tc2(s, A, out, smem, reset, st);
+  s->sev_used = 0;
   if (s->timing) CUDA_TRY(cudaEventRecord(s->ev[0], st));
   if (grid > 0) {
-    if (use_tc2) {
-      TcB tb = s->tb;
-      tb.scratch = s->d_scratch;
-      tc2_kernel_for(s->G.kernel, s->t2.nh)<<<grid, TC_WARPS * 32 + 32, smem, st>>>(s->D, G, A, out, tb, s->t2);
-    } else if (use_tc) {
+    if (use_tc) {
       TcB tb = s->tb;
       tb.scratch = s->d_scratch;
       tc_kernel_for(s->G.DP, s->G.kernel)<<<grid, TC_WARPS * 32 + 32, smem, st>>>(s->D, G, A, out, tb);
@@ -702,6 +770,9 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
     if (e != cudaSuccess) return cleanup(fail(AS_ERR_CUDA, cudaGetErrorString(e)));
     for (int i = 0; i < 4; ++i)
       if (cudaEventCreate(&s->ev[i]) != cudaSuccess) return cleanup(fail(AS_ERR_CUDA, "cudaEventCreate"));
+    s->sev.assign(SEV_MAX, nullptr);
+    for (auto& e : s->sev)
+      if (cudaEventCreate(&e) != cudaSuccess) return cleanup(fail(AS_ERR_CUDA, "cudaEventCreate"));
   }
   *out = s;
   return AS_OK;
@@ -718,6 +789,14 @@ void autoscout_space_destroy(as_space* s) {
     if (s->d_scratch) cudaFree(s->d_scratch);
     for (auto& e : s->ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : s->sev)
+      if (e) cudaEventDestroy(e);
+    {
+      CandList& L = s->list;
+      void* ptrs[] = {L.cvi, L.j, L.m0, L.dv0, L.dv1, L.dv2, L.count};
+      for (void* q : ptrs)
+        if (q) cudaFree(q);
+    }
   }
   delete s;
 }
@@ -977,6 +1056,22 @@ as_status autoscout_set_timing(as_space* s, int32_t enable) {
   if (!s) return fail(AS_ERR_INVALID_ARG, "null argument");
   s->timing = enable != 0 && s->device >= 0;
   s->ev_recorded = false;
+  return AS_OK;
+}
+
+as_status autoscout_last_phase_ms(as_space* s, double* gen_ms, double* score_ms) {
+  if (!s || !s->ev_recorded) return fail(AS_ERR_STATE, "no timed launch recorded");
+  double g = 0, k = 0;
+  for (int i = 0; i + 3 <= s->sev_used; i += 3) {
+    float a = 0, b = 0;
+    CUDA_TRY(cudaEventSynchronize(s->sev[i + 2]));
+    CUDA_TRY(cudaEventElapsedTime(&a, s->sev[i], s->sev[i + 1]));
+    CUDA_TRY(cudaEventElapsedTime(&b, s->sev[i + 1], s->sev[i + 2]));
+    g += a;
+    k += b;
+  }
+  if (gen_ms) *gen_ms = g;
+  if (score_ms) *score_ms = k;
   return AS_OK;
 }
 

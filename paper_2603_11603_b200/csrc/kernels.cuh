@@ -109,12 +109,12 @@ __device__ __forceinline__ void decode_dev(const DevSpace& S, uint64_t p, DV& dv
   }
 }
 
-// Decode with a coarse SMEM index of the structure prefix array: cidx[k] = prefix[k * n_struct / CI]
-// (k < CI) brackets the structure before a short binary search in global memory.
+// Decode with a coarse SMEM index of the structure prefix array: cidx[k] = prefix[k * n_struct / ci_n]
+// (k < ci_n) brackets the structure before a short binary search in global memory; with
+// ci_n == n_struct the whole search runs in shared memory.
 constexpr int CI = 256;
-__device__ __forceinline__ void decode_dev_idx(const DevSpace& S, const uint64_t* cidx, uint64_t p, DV& dv,
-                                               uint32_t& act, uint64_t& raw) {
-  const int ci_n = S.n_struct < CI ? S.n_struct : CI;
+__device__ __forceinline__ void decode_dev_ci(const DevSpace& S, const uint64_t* cidx, int ci_n, uint64_t p, DV& dv,
+                                              uint32_t& act, uint64_t& raw) {
   int a = 0, b = ci_n;                       // largest k with cidx[k] <= p
   while (b - a > 1) {
     const int mid = (a + b) >> 1;
@@ -147,10 +147,16 @@ __device__ __forceinline__ void decode_dev_idx(const DevSpace& S, const uint64_t
     raw += __ldg(&tu->raw);
   }
 }
-__device__ __forceinline__ void load_cidx(const DevSpace& S, uint64_t* cidx, int tid, int nthreads) {
-  const int ci_n = S.n_struct < CI ? S.n_struct : CI;
+__device__ __forceinline__ void decode_dev_idx(const DevSpace& S, const uint64_t* cidx, uint64_t p, DV& dv,
+                                               uint32_t& act, uint64_t& raw) {
+  decode_dev_ci(S, cidx, S.n_struct < CI ? S.n_struct : CI, p, dv, act, raw);
+}
+__device__ __forceinline__ void load_cidx_n(const DevSpace& S, uint64_t* cidx, int ci_n, int tid, int nthreads) {
   for (int k = tid; k < ci_n; k += nthreads)
     cidx[k] = __ldg(S.prefix + static_cast<int>((static_cast<long long>(k) * S.n_struct) / ci_n));
+}
+__device__ __forceinline__ void load_cidx(const DevSpace& S, uint64_t* cidx, int tid, int nthreads) {
+  load_cidx_n(S, cidx, S.n_struct < CI ? S.n_struct : CI, tid, nthreads);
 }
 
 // Packed FP32x2 helpers (FFMA2 / FADD2 on sm_100a): r^2 = sum_f (x_f - o_f)^2 two features at a time.

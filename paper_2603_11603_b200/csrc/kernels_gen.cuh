@@ -1,0 +1,82 @@
+// Candidate generation kernel: index -> configuration -> validity -> simulator,
+// writing the VALID candidates of a slice of the batch as a compact list (SoA) for the
+// tensor-core score kernel.  Decode + simulator are latency-bound integer / FP64 work; run as a
+// separate high-occupancy kernel they no longer stall the producer warps of the score kernel
+// (which has one 544-thread CTA per SM), and the score kernel sees full 128-row tiles only.
+//
+// Per candidate j of the slice [j0, j0 + nj):
+//   p = begin + j (RANGE) or pi_seed(begin + j) (SAMPLE; reading R3)
+//   (dv, act, raw) = CVI decode of p (SMEM structure index)
+//   (cost, ok)     = simulator + FP64 resource check (R7)
+//   d_raw[j] = raw; invalid: d_scores[j] = -inf; valid: append (cvi, j, ln cost, dv) to the list.
+#pragma once
+#include "kernels.cuh"
+
+namespace as {
+
+constexpr int GEN_THREADS = 256;
+constexpr int GEN_CI_MAX = 4096;             // SMEM structure index entries (32 KB)
+
+struct CandList {
+  uint32_t* cvi;                // [cap + 128]
+  uint32_t* j;                  // [cap + 128]   index in the batch (d_scores / d_raw slot)
+  double* m0;                   // [cap + 128]   ln cost (GP prior mean, R9)
+  uint64_t* dv0;                // [cap + 128]   digit vector words
+  uint64_t* dv1;
+  uint64_t* dv2;
+  unsigned long long* count;    // number of records
+};
+
+__global__ void __launch_bounds__(GEN_THREADS)
+gen_kernel(DevSpace S, BatchArgs A, uint64_t j0, uint64_t nj, CandList L, int ci_n, unsigned long long* valid_total) {
+  extern __shared__ __align__(16) uint64_t gen_cidx[];
+  __shared__ unsigned long long blk_valid;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) blk_valid = 0;
+  load_cidx_n(S, gen_cidx, ci_n, tid, GEN_THREADS);
+  __syncthreads();
+  unsigned long long my_valid = 0;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * GEN_THREADS;
+  for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * GEN_THREADS; base < nj; base += stride) {
+    const uint64_t jj = base + tid;
+    const bool in = jj < nj;
+    bool ok = false;
+    DV dv;
+    uint32_t act = 0;
+    uint64_t raw = 0, pcvi = 0;
+    double cost = 1.0;
+    const uint64_t j = j0 + jj;
+    if (in) {
+      pcvi = (A.mode == 0) ? A.begin + j : feistel_pi(A.fk, A.begin + j);
+      decode_dev_ci(S, gen_cidx, ci_n, pcvi, dv, act, raw);
+      sim_dev(S, dv, act, cost, ok);
+      if (A.d_raw) A.d_raw[j] = raw;
+      if (!ok && A.d_scores) A.d_scores[j] = -INFINITY;
+    }
+    // warp-aggregated append of the valid lanes
+    const unsigned vb = __ballot_sync(0xffffffffu, in && ok);
+    if (vb) {
+      unsigned long long wbase = 0;
+      if (lane == 0) wbase = atomicAdd(L.count, static_cast<unsigned long long>(__popc(vb)));
+      wbase = __shfl_sync(0xffffffffu, wbase, 0);
+      if (in && ok) {
+        const uint64_t slot = wbase + __popc(vb & ((1u << lane) - 1u));
+        L.cvi[slot] = static_cast<uint32_t>(pcvi);
+        L.j[slot] = static_cast<uint32_t>(j);
+        L.m0[slot] = log(cost);
+        L.dv0[slot] = dv.w[0];
+        L.dv1[slot] = dv.w[1];
+        L.dv2[slot] = dv.w[2];
+      }
+      if (lane == 0) my_valid += __popc(vb);
+    }
+  }
+  if (lane == 0 && my_valid) atomicAdd(&blk_valid, my_valid);
+  __syncthreads();
+  if (tid == 0 && blk_valid) {
+    atomicAdd(valid_total, blk_valid);
+    if (A.d_valid_count) atomicAdd(reinterpret_cast<unsigned long long*>(A.d_valid_count), blk_valid);
+  }
+}
+
+}  // namespace as

@@ -20,15 +20,40 @@
 //               of the L^-1 chunks in one instruction stream; bulk copies of the L^-1 and T chunks.
 // TMEM: D [Mp16] | A ring [4 x 32] | R2 ring [2 groups x 64]  (Mp16 <= 256 -> <= 512 columns).
 #pragma once
+#include "kernels_gen.cuh"
 #include "kernels_tc.cuh"
 
 namespace as {
 
 constexpr int TC2_RG = 4;                    // K-chunks per R2 group (N = 64)
 constexpr int TC2_RS = 2;                    // R2 group slots in TMEM
-constexpr int TC2_NB = 2;                    // L^-1 chunk ring stages
+constexpr int TC2_NB = 3;                    // L^-1 chunk ring stages (2 chunks prefetched: L2 latency)
 constexpr int TC2_NT = 3;                    // T group ring stages
 constexpr int TC2_KPMAX = 64;                // one-hot width the host aims for (features beyond go SIMT)
+
+// Shared-memory carve-out: the fixed-size arrays first (compile-time offsets, so the hot loop
+// addresses them with immediates), then the rings whose size depends on M and Kp.
+constexpr size_t tc2_r128(size_t b) { return (b + 127) & ~size_t(127); }
+constexpr size_t TC2_O_BARS = 0;
+constexpr size_t TC2_O_ALPHA = TC2_O_BARS + 64 * 8;
+constexpr size_t TC2_O_OH = TC2_O_ALPHA + 2 * MMAX * 4;
+constexpr size_t TC2_O_MXH = TC2_O_OH + 4 * MMAX * 4;
+constexpr size_t TC2_O_MPART = TC2_O_MXH + 4 * TC_TI * TC_ROWS * 4;
+constexpr size_t TC2_O_VPART = TC2_O_MPART + TC_TI * 3 * TC_ROWS * 4;
+constexpr size_t TC2_O_MCVI = TC2_O_VPART + 4 * TC_ROWS * 4;
+constexpr size_t TC2_O_MJ = TC2_O_MCVI + TC_TI * TC_ROWS * 4;
+constexpr size_t TC2_O_MM0 = TC2_O_MJ + TC_TI * TC_ROWS * 4;
+constexpr size_t TC2_O_XH = TC2_O_MM0 + TC_TI * TC_ROWS * 8;
+// staging of one tile of list records (bulk-copied by the loader): cvi | j | m0 | dv0 | dv1 | dv2
+constexpr size_t TC2_STG_CVI = 0, TC2_STG_J = 512, TC2_STG_M0 = 1024, TC2_STG_DV0 = 2048, TC2_STG_DV1 = 3072,
+                 TC2_STG_DV2 = 4096, TC2_STG_BYTES = 5120;
+constexpr size_t TC2_O_STG = TC2_O_XH + 4 * VMAX * 4;
+constexpr size_t TC2_O_VAR = TC2_O_STG + 2 * TC2_STG_BYTES;
+// + NB L^-1 stages (2 Mp16 16 4 B) + NT T stages (2 64 Kp 2 B) + 2 E buffers (128 Kp 2 B) + P keys
+__host__ __device__ constexpr size_t tc2_smem_total(int Mp16, int Kp, int P) {
+  return TC2_O_VAR + static_cast<size_t>(TC2_NB) * 2 * Mp16 * 16 * 4 + static_cast<size_t>(TC2_NT) * 2 * 64 * Kp * 2 +
+         2ull * 128 * Kp * 2 + static_cast<size_t>(P) * 8;
+}
 
 struct Tc2B {
   const uint16_t* tch;          // T groups: [ng][2 pieces][64 x Kp] FP16, kmajor_off16 layout
@@ -44,19 +69,17 @@ struct Tc2B {
 
 template <int PW, int KT, int NH>
 __global__ void __launch_bounds__(PW * 32 + 32, 1)
-score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2) {
+score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, CandList L) {
   constexpr int TC_PROD_WARPS = PW;
   constexpr int TC_PROD_THREADS = PW * 32;
   constexpr int TC_THREADS = TC_PROD_THREADS + 32;
   constexpr int TC_JQ = TC_PROD_THREADS / TC_ROWS;   // producer threads per candidate
   constexpr int TC_JPT = TC_KCH / TC_JQ;             // observed points per thread per chunk
-  static_assert(TC_JPT % 4 == 0, "R2 / D reads are 32x32b.x4");
+  static_assert(TC_JQ == 4 && TC_JPT == 4, "R2 group columns are laid out for 16 producer warps");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ TopkSmem ts;
-  __shared__ int q_n;
   __shared__ int tinfo[TC_TI];
   __shared__ uint32_t tmem_base;
-  __shared__ unsigned long long valid_cta;
   __shared__ int eoff_s[DMAX];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -67,31 +90,26 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2) 
   const uint32_t b_stage_bytes = 2u * Mp16 * TC_KCH * 4;              // L^-1 hi + lo at the widest chunk
   const uint32_t t_stage_bytes = 2u * (TC2_RG * TC_KCH) * Kp * 2;     // T: 2 FP16 pieces x 64 points
   const uint32_t e_bytes = static_cast<uint32_t>(TC_ROWS) * Kp * 2;   // E: 128 rows x Kp FP16
-  unsigned char* p = smem_raw;
-  auto take = [&](size_t bytes) {
-    unsigned char* r = p;
-    p += (bytes + 127) & ~size_t(127);
-    return r;
-  };
-  unsigned char* B0 = take(static_cast<size_t>(TC2_NB) * b_stage_bytes);
-  unsigned char* T0 = take(static_cast<size_t>(TC2_NT) * t_stage_bytes);
-  unsigned char* E0 = take(2ull * e_bytes);
-  float* alpha_s = reinterpret_cast<float*>(take(sizeof(float) * 2 * Mp16));   // (alpha_j, |alpha_j|)
-  float* oh_s = reinterpret_cast<float*>(take(sizeof(float) * (NH > 0 ? NH : 1) * Mp16));
-  float* xh_s = reinterpret_cast<float*>(take(sizeof(float) * (NH > 0 ? NH : 1) * VMAX));
-  float* m_xh = reinterpret_cast<float*>(take(sizeof(float) * (NH > 0 ? NH : 1) * TC_TI * TC_ROWS));
-  DV* q_dv = reinterpret_cast<DV*>(take(sizeof(DV) * TC_QCAP));
-  double* q_m0 = reinterpret_cast<double*>(take(sizeof(double) * TC_QCAP));
-  uint32_t* q_cvi = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_QCAP));
-  uint32_t* q_j = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_QCAP));
-  uint32_t* m_cvi = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_TI * TC_ROWS));
-  uint32_t* m_j = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * TC_TI * TC_ROWS));
-  double* m_m0 = reinterpret_cast<double*>(take(sizeof(double) * TC_TI * TC_ROWS));
-  float* m_part = reinterpret_cast<float*>(take(sizeof(float) * TC_TI * 3 * TC_ROWS));
-  float* vpart = reinterpret_cast<float*>(take(sizeof(float) * 4 * TC_ROWS));
-  uint64_t* arr = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * out.P));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * 64));
-  uint64_t* cidx = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * CI));
+  unsigned char* const sm0 = smem_raw;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm0 + TC2_O_BARS);
+  float* alpha_s = reinterpret_cast<float*>(sm0 + TC2_O_ALPHA);   // (alpha_j, |alpha_j|) pairs
+  float* oh_s = reinterpret_cast<float*>(sm0 + TC2_O_OH);         // [Mp16][NH]
+  float* m_xh = reinterpret_cast<float*>(sm0 + TC2_O_MXH);        // [TI][128][NH]
+  float* m_part = reinterpret_cast<float*>(sm0 + TC2_O_MPART);
+  float* vpart = reinterpret_cast<float*>(sm0 + TC2_O_VPART);
+  uint32_t* m_cvi = reinterpret_cast<uint32_t*>(sm0 + TC2_O_MCVI);
+  uint32_t* m_j = reinterpret_cast<uint32_t*>(sm0 + TC2_O_MJ);
+  double* m_m0 = reinterpret_cast<double*>(sm0 + TC2_O_MM0);
+  float* xh_s = reinterpret_cast<float*>(sm0 + TC2_O_XH);         // [NH][VMAX]
+  unsigned char* stg = sm0 + TC2_O_STG;                           // [2][TC2_STG_BYTES]
+  // this CTA's tiles of the candidate list: blockIdx.x, blockIdx.x + gridDim.x, ...
+  const uint64_t n_list = *L.count;
+  const uint64_t n_tiles = (n_list + TC_ROWS - 1) / TC_ROWS;
+  const int my_tiles = blockIdx.x < n_tiles ? static_cast<int>((n_tiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  unsigned char* B0 = sm0 + TC2_O_VAR;
+  unsigned char* T0 = B0 + static_cast<size_t>(TC2_NB) * b_stage_bytes;
+  unsigned char* E0 = T0 + static_cast<size_t>(TC2_NT) * t_stage_bytes;
+  uint64_t* arr = reinterpret_cast<uint64_t*>(E0 + 2ull * e_bytes);
   const uint32_t sB0 = tc::smem_u32(B0), sT0 = tc::smem_u32(T0), sE0 = tc::smem_u32(E0);
   uint64_t* a_full = bars;                     // [NA] count PW
   uint64_t* a_empty = a_full + TC_NA;          // [NA] commit
@@ -104,6 +122,8 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2) 
   uint64_t* r_empty = r_full + TC2_RS;         // [RS] count PW
   uint64_t* x_full = r_empty + TC2_RS;         // [NT] 1 + tx  (T group loaded)
   uint64_t* x_empty = x_full + TC2_NT;         // [NT] commit
+  uint64_t* s_full = x_empty + TC2_NT;         // [2]  1 + tx  (tile records staged)
+  uint64_t* s_empty = s_full + 2;              // [2]  count PW
 
   // ---- setup
   for (int i = tid; i < Mp16; i += TC_THREADS) {
@@ -114,7 +134,6 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2) 
   if (tid < DMAX) eoff_s[tid] = T2.eoff[tid];
   for (int i = tid; i < NH * Mp16; i += TC_THREADS) oh_s[i] = __ldg(T2.oh + i);
   for (int i = tid; i < NH * VMAX; i += TC_THREADS) xh_s[i] = __ldg(T2.xh + i);
-  load_cidx(S, cidx, tid, TC_THREADS);
   if (tid == 0) {
     for (int s = 0; s < TC_NA; ++s) {
       tc::mbar_init(a_full + s, TC_PROD_WARPS);
@@ -135,13 +154,15 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2) 
       tc::mbar_init(x_full + s, 1);
       tc::mbar_init(x_empty + s, 1);
     }
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(s_full + s, 1);
+      tc::mbar_init(s_empty + s, TC_PROD_WARPS);
+    }
     tc::mbar_fence_init();
     ts.n_list = 0;
     ts.n_add = 0;
     ts.tau = KEY_NONE;
     ts.drop = KEY_NONE;
-    q_n = 0;
-    valid_cta = 0;
   }
   const uint32_t tmem_cols = 512;
   if (warp == 0) tc::tmem_alloc(&tmem_base, tmem_cols);
@@ -259,71 +280,16 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2) 
       group_admit(key, arr, ts, out.KC, pt, TC_PROD_THREADS, 1);
     };
 
-    // ---- phase 0 of one input tile: index -> configuration -> validity -> simulator -> queue
-    const uint64_t ntiles = (A.count + TC_PROD_THREADS - 1) / TC_PROD_THREADS;
-    uint64_t tile_in = blockIdx.x;
-    int head = 0;
-    auto phase0 = [&](uint64_t tile) {
-      const uint64_t j = tile * TC_PROD_THREADS + pt;
-      const bool in = j < A.count;
-      bool ok = false;
-      if (in) {
-        const uint64_t pcvi = (A.mode == 0) ? A.begin + j : feistel_pi(A.fk, A.begin + j);
-        DV dv;
-        uint32_t act;
-        uint64_t raw;
-        decode_dev_idx(S, cidx, pcvi, dv, act, raw);
-        double cost;
-        sim_dev(S, dv, act, cost, ok);
-        if (A.d_raw) A.d_raw[j] = raw;
-        if (!ok && A.d_scores) A.d_scores[j] = -INFINITY;
-        if (ok) {
-          const int slot = atomicAdd(&q_n, 1);
-          q_dv[slot] = dv;
-          q_m0[slot] = log(cost);
-          q_cvi[slot] = static_cast<uint32_t>(pcvi);
-          q_j[slot] = static_cast<uint32_t>(j);
-        }
-      }
-      const unsigned vb = __ballot_sync(0xffffffffu, in && ok);
-      if (lane == 0 && vb) atomicAdd(&valid_cta, static_cast<unsigned long long>(__popc(vb)));
-    };
-    // make at least `need` queued candidates available (or exhaust the input)
-    auto fill = [&](int need) {
-      while (q_n - head < need && tile_in < ntiles) {
-        const int left = q_n - head;
-        if (head > 0) {
-          DV mdv;
-          double mm0 = 0;
-          uint32_t mcvi = 0, mj = 0;
-          if (pt < left) {
-            mdv = q_dv[head + pt];
-            mm0 = q_m0[head + pt];
-            mcvi = q_cvi[head + pt];
-            mj = q_j[head + pt];
-          }
-          named_sync(1, TC_PROD_THREADS);
-          if (pt < left) {
-            q_dv[pt] = mdv;
-            q_m0[pt] = mm0;
-            q_cvi[pt] = mcvi;
-            q_j[pt] = mj;
-          }
-          if (pt == 0) q_n = left;
-          head = 0;
-          named_sync(1, TC_PROD_THREADS);
-        }
-        phase0(tile_in);
-        tile_in += gridDim.x;
-        named_sync(1, TC_PROD_THREADS);
-      }
-    };
-    // publish tile u: meta rows, zeroed partial sums, one-hot rows E[u & 1]; returns n (0 = end)
+    // publish tile u: meta rows, zeroed partial sums, one-hot rows E[u & 1] and the SIMT-feature
+    // values, from the staged list records; returns n (0 = end of this CTA's tiles)
     auto publish = [&](int u) -> int {
-      const int avail = q_n - head;
-      const int n = avail >= TC_ROWS ? TC_ROWS : avail;
+      int n = 0;
       const int us = u % TC_TI;
-      if (n > 0) {
+      if (u < my_tiles) {
+        const uint64_t r0 = (blockIdx.x + static_cast<uint64_t>(u) * gridDim.x) * TC_ROWS;
+        n = static_cast<int>(n_list - r0 < TC_ROWS ? n_list - r0 : TC_ROWS);
+        const unsigned char* sg = stg + (u & 1) * TC2_STG_BYTES;
+        tc::mbar_wait(s_full + (u & 1), (u >> 1) & 1);
         if (pt < TC_ROWS) {
           float* mz = m_part + us * 3 * TC_ROWS;
           mz[pt] = 0.f;
@@ -331,16 +297,19 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2) 
           mz[2 * TC_ROWS + pt] = 0.f;
         }
         if (pt < n) {
-          m_cvi[us * TC_ROWS + pt] = q_cvi[head + pt];
-          m_j[us * TC_ROWS + pt] = q_j[head + pt];
-          m_m0[us * TC_ROWS + pt] = q_m0[head + pt];
+          m_cvi[us * TC_ROWS + pt] = reinterpret_cast<const uint32_t*>(sg + TC2_STG_CVI)[pt];
+          m_j[us * TC_ROWS + pt] = reinterpret_cast<const uint32_t*>(sg + TC2_STG_J)[pt];
+          m_m0[us * TC_ROWS + pt] = reinterpret_cast<const double*>(sg + TC2_STG_M0)[pt];
         }
         unsigned char* E = E0 + (u & 1) * e_bytes;
         for (uint32_t i = pt; i < e_bytes / 16; i += TC_PROD_THREADS)
           *reinterpret_cast<uint4*>(E + 16 * i) = make_uint4(0u, 0u, 0u, 0u);
         named_sync(1, TC_PROD_THREADS);
         if (cand < n) {
-          const DV cdv = q_dv[head + cand];
+          DV cdv;
+          cdv.w[0] = reinterpret_cast<const uint64_t*>(sg + TC2_STG_DV0)[cand];
+          cdv.w[1] = reinterpret_cast<const uint64_t*>(sg + TC2_STG_DV1)[cand];
+          cdv.w[2] = reinterpret_cast<const uint64_t*>(sg + TC2_STG_DV2)[cand];
           for (int f = jq; f < S.d; f += TC_JQ) {
             if (eoff_s[f] < 0) continue;
             const uint32_t col = static_cast<uint32_t>(eoff_s[f]) + dv_get(cdv, f);
@@ -352,23 +321,22 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2) 
           }
         }
         tc::fence_proxy_async();   // generic-proxy stores -> visible to the tensor core (async proxy)
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(s_empty + (u & 1));   // staged records consumed
       }
       named_sync(1, TC_PROD_THREADS);
       if (pt == 0) {
         tinfo[us] = n > 0 ? n : -1;
         tc::mbar_arrive(t_ready + us);
       }
-      head += n;
       return n;
     };
 
-    fill(TC_ROWS);
     int n_cur = publish(0);
     uint32_t g = 0;                                   // global chunk counter (A ring)
     uint32_t gr = 0;                                  // global R2 group counter
     const uint32_t sOH = tc::smem_u32(oh_s);
     for (int t = 0; n_cur > 0; ++t) {
-      fill(TC_ROWS);
       const int n_next = publish(t + 1);
       // ---- chunk loop: R2 (+ SIMT features) -> k -> A ring
       float mu_p = 0.f, sb_p = 0.f, kk_p = 0.f, vsq_run = 0.f;
@@ -379,80 +347,97 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2) 
         const float* xq = m_xh + ((t % TC_TI) * TC_ROWS + cand) * (NH > 0 ? NH : 1) + 2 * h;
         xhp[h] = f2_pack(xq[0], xq[1]);
       }
-      for (int c = 0; c < nch; ++c, ++g) {
-        const int s = g % TC_NA, rs = gr % TC2_RS, cg = c % TC2_RG;
-        const uint32_t a_par = ((g / TC_NA) & 1u) ^ 1u;
-        float rv[TC_JPT];
-        if (cg == 0) tc::mbar_wait(r_full + rs, (gr / TC2_RS) & 1u);
+      for (int c0 = 0; c0 < nch; c0 += TC2_RG) {
+        // ---- one R2 group: the thread's 4 points of each of the 4 chunks are 16 contiguous
+        // columns (T rows are permuted on the host), read with one load
+        const int rs = gr % TC2_RS;
+        float rv[TC2_RG * TC_JPT];
+        tc::mbar_wait(r_full + rs, (gr / TC2_RS) & 1u);
         tc::fence_after_sync();
-#pragma unroll
-        for (int h = 0; h < TC_JPT; h += 4)
-          tc::tmem_ld4(lane_base + R0col + 64u * rs + 16u * cg + TC_JPT * jq + h, rv + h);
-        if (cg == TC2_RG - 1 || c == nch - 1) {       // R2 group consumed
-          tc::fence_before_sync();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(r_empty + rs);
-          ++gr;
-        }
-        const bool a_ready = tc::mbar_test(a_empty + s, a_par);
-        float kh[TC_JPT], kl[TC_JPT];
-#pragma unroll
-        for (int q = 0; q < TC_JPT; ++q) {
-          const int jo = c * TC_KCH + jq * TC_JPT + q;
-          float r2s = rv[q];
-          if (NH > 0) {
-            unsigned long long acc = 0ull;
-#pragma unroll
-            for (int h = 0; h < NH / 2; ++h) {
-              unsigned long long o2;
-              asm volatile("ld.shared.b64 %0, [%1];" : "=l"(o2) : "r"(sOH + 4u * (jo * NH + 2 * h)));
-              const unsigned long long dd = f2_sub(xhp[h], o2);
-              acc = f2_fma(dd, dd, acc);
-            }
-            const float2 a2 = f2_unpack(acc);
-            r2s += a2.x + a2.y;
-          }
-          const float r2 = fmaxf(r2s, 0.f);
-          float arg, poly, ex;
-          if (KT == 0) {
-            const float r = tc::sqrt_approx_ftz(r2);
-            arg = c_arg * r;
-            poly = fmaf(arg, fmaf(arg, 0.33333333333333333f, 1.0f), 1.0f);
-            ex = tc::ex2_approx(fmaf(r, ex_c1, ex_c0));
-          } else {
-            arg = c_arg * r2;
-            poly = 1.0f;
-            ex = tc::ex2_approx(fmaf(r2, ex_c1, ex_c0));
-          }
-          const float kval = poly * ex;
-          const float cc = fmaf(kval, arg, kval);
-          float al, aa;
-          tc::lds_f32x2(sAl + 8 * jo, al, aa);
-          mu_p = fmaf(kval, al, mu_p);
-          sb_p = fmaf(cc, aa, sb_p);
-          kk_p = fmaf(cc, cc, kk_p);
-          tc::split_tf32_fast(kval, kh[q], kl[q]);
-        }
-        if (!a_ready) tc::mbar_wait(a_empty + s, a_par);
-        tc::fence_after_sync();
-        if (c >= TC_NA) {
-#pragma unroll
-          for (int h = 0; h < TC_JPT; h += 4) {
-            float v[4];
-            tc::tmem_ld4(dq + 16 * (c - TC_NA) + h, v);
-            vsq_run = fmaf(v[0], v[0], fmaf(v[1], v[1], fmaf(v[2], v[2], fmaf(v[3], v[3], vsq_run))));
-          }
-        }
-        const uint32_t acol = lane_base + A0col + 32u * s + jq * TC_JPT;
-#pragma unroll
-        for (int v4 = 0; v4 < TC_JPT / 4; ++v4) {
-          tc::tmem_st4(acol + 4 * v4, kh[4 * v4], kh[4 * v4 + 1], kh[4 * v4 + 2], kh[4 * v4 + 3]);
-          tc::tmem_st4(acol + 16 + 4 * v4, kl[4 * v4], kl[4 * v4 + 1], kl[4 * v4 + 2], kl[4 * v4 + 3]);
-        }
-        tc::tmem_st_wait();
+        tc::tmem_ld16(lane_base + R0col + 64u * rs + 16u * jq, rv);
         tc::fence_before_sync();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(a_full + s);
+        if (lane == 0) tc::mbar_arrive(r_empty + rs);
+        ++gr;
+#pragma unroll
+        for (int cg = 0; cg < TC2_RG; ++cg) {
+          const int c = c0 + cg;
+          if (c >= nch) break;
+          const int s = g % TC_NA;
+          const uint32_t a_par = ((g / TC_NA) & 1u) ^ 1u;
+          const bool a_ready = tc::mbar_test(a_empty + s, a_par);
+          float kh[TC_JPT], kl[TC_JPT];
+#pragma unroll
+          for (int q = 0; q < TC_JPT; ++q) {
+            const int jo = c * TC_KCH + jq * TC_JPT + q;
+            float r2s = rv[cg * TC_JPT + q];
+            if (NH > 0) {
+              unsigned long long acc = 0ull;
+#pragma unroll
+              for (int h = 0; h < NH / 2; ++h) {
+                unsigned long long o2;
+                asm volatile("ld.shared.b64 %0, [%1];" : "=l"(o2) : "r"(sOH + 4u * (jo * NH + 2 * h)));
+                const unsigned long long dd = f2_sub(xhp[h], o2);
+                acc = f2_fma(dd, dd, acc);
+              }
+              const float2 a2 = f2_unpack(acc);
+              r2s += a2.x + a2.y;
+            }
+            const float r2 = fmaxf(r2s, 0.f);
+            float arg, poly, ex;
+            if (KT == 0) {
+              const float r = tc::sqrt_approx_ftz(r2);
+              arg = c_arg * r;
+              poly = fmaf(arg, fmaf(arg, 0.33333333333333333f, 1.0f), 1.0f);
+              ex = tc::ex2_approx(fmaf(r, ex_c1, ex_c0));
+            } else {
+              arg = c_arg * r2;
+              poly = 1.0f;
+              ex = tc::ex2_approx(fmaf(r2, ex_c1, ex_c0));
+            }
+            const float kval = poly * ex;
+            const float cc = fmaf(kval, arg, kval);
+            float al, aa;
+            tc::lds_f32x2(sAl + 8 * jo, al, aa);
+            mu_p = fmaf(kval, al, mu_p);
+            sb_p = fmaf(cc, aa, sb_p);
+            kk_p = fmaf(cc, cc, kk_p);
+            tc::split_tf32_fast(kval, kh[q], kl[q]);
+          }
+          if (!a_ready) tc::mbar_wait(a_empty + s, a_par);
+          tc::fence_after_sync();
+          const uint32_t acol = lane_base + A0col + 32u * s + jq * TC_JPT;
+          tc::tmem_st4(acol, kh[0], kh[1], kh[2], kh[3]);
+          tc::tmem_st4(acol + 16, kl[0], kl[1], kl[2], kl[3]);
+          tc::tmem_st_wait();
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(a_full + s);
+          ++g;
+        }
+        // ---- accumulator column blocks made final by this group's a_empty waits:
+        // [c0 - NA, c_last - NA]; one batched read (the last NA blocks are left to the epilogue)
+        {
+          const int c_last = (c0 + TC2_RG < nch ? c0 + TC2_RG : nch) - 1;
+          const int b0 = c0 - TC_NA;
+          if (c_last - TC_NA >= 0) {
+            float v[16];
+            uint32_t ad[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int b = b0 + i;
+              ad[i] = dq + 16u * static_cast<uint32_t>(b >= 0 && b <= c_last - TC_NA ? b : 0);
+            }
+            tc::tmem_ld4x4(ad[0], ad[1], ad[2], ad[3], v);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int b = b0 + i;
+              if (b >= 0 && b <= c_last - TC_NA)
+                vsq_run = fmaf(v[4 * i], v[4 * i],
+                               fmaf(v[4 * i + 1], v[4 * i + 1], fmaf(v[4 * i + 2], v[4 * i + 2], fmaf(v[4 * i + 3], v[4 * i + 3], vsq_run))));
+            }
+          }
+        }
       }
       float* mp = m_part + (t % TC_TI) * 3 * TC_ROWS;
       atomicAdd(mp + cand, mu_p);
@@ -499,6 +484,25 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2) 
       ++gl;
       if (++lc == nch) lc = 0;
     };
+    // stage the list records of this CTA's tile u (rounded up to 16 B; the list is padded)
+    auto load_S = [&](int u) {
+      if (u >= my_tiles) return;
+      tc::mbar_wait(s_empty + (u & 1), ((u >> 1) & 1u) ^ 1u);
+      if (lane == 0) {
+        const uint64_t r0 = (blockIdx.x + static_cast<uint64_t>(u) * gridDim.x) * TC_ROWS;
+        const uint32_t n = static_cast<uint32_t>(n_list - r0 < TC_ROWS ? n_list - r0 : TC_ROWS);
+        const uint32_t b4 = (n * 4 + 15) & ~15u, b8 = (n * 8 + 15) & ~15u;   // bulk sizes: multiples of 16 B
+        unsigned char* sg = stg + (u & 1) * TC2_STG_BYTES;
+        tc::mbar_arrive_expect_tx(s_full + (u & 1), 2 * b4 + 4 * b8);
+        tc::bulk_g2s(sg + TC2_STG_CVI, L.cvi + r0, b4, s_full + (u & 1));
+        tc::bulk_g2s(sg + TC2_STG_J, L.j + r0, b4, s_full + (u & 1));
+        tc::bulk_g2s(sg + TC2_STG_M0, L.m0 + r0, b8, s_full + (u & 1));
+        tc::bulk_g2s(sg + TC2_STG_DV0, L.dv0 + r0, b8, s_full + (u & 1));
+        tc::bulk_g2s(sg + TC2_STG_DV1, L.dv1 + r0, b8, s_full + (u & 1));
+        tc::bulk_g2s(sg + TC2_STG_DV2, L.dv2 + r0, b8, s_full + (u & 1));
+      }
+      __syncwarp();
+    };
     auto load_T = [&]() {
       const int s = xl % TC2_NT;
       tc::mbar_wait(x_empty + s, ((xl / TC2_NT) & 1u) ^ 1u);
@@ -540,6 +544,8 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2) 
       load_T();                                        // refill the slot of group x-2, NT-1 ahead
       return true;
     };
+    load_S(0);
+    load_S(1);
     if (tile_exists(0)) {
       for (int i = 0; i < TC2_NB - 1; ++i) load_L();
       for (int i = 0; i < TC2_NT - 1; ++i) load_T();
@@ -547,6 +553,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2) 
     const uint32_t sbo = (TC_KCH / 4) * 128;
     (void)sbo;
     for (int t = 0; tile_exists(t); ++t) {
+      load_S(t + 2);                                   // slot t % 2 was consumed by publish(t)
       tc::mbar_wait(d_empty, (t & 1) ^ 1);
       tc::fence_after_sync();
       for (int c = 0; c < nch; ++c, ++g) {
@@ -596,10 +603,6 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2) 
   // ---- teardown
   tc::fence_before_sync();
   __syncthreads();
-  if (tid == 0 && valid_cta) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(out.valid), valid_cta);
-    if (A.d_valid_count) atomicAdd(reinterpret_cast<unsigned long long*>(A.d_valid_count), valid_cta);
-  }
   if (warp == 0) {
     tc::fence_after_sync();
     tc::tmem_dealloc(tmem, tmem_cols);
