@@ -69,7 +69,8 @@ typedef struct {
   int32_t n_components;  /* tail gating groups */
   int32_t n_observed;    /* M of the current fit */
   int32_t max_observed;  /* capacity for M */
-  uint64_t n_launches;   /* kernels this handle has launched so far (score, merge, refine, mask) */
+  uint64_t n_launches;   /* kernels this handle has launched so far (generate, score, merge, refine, mask) */
+  uint64_t fit_upload_bytes; /* host->device bytes of the last observe()/observe_clear() GP upload */
 } as_space_info;
 
 typedef struct {

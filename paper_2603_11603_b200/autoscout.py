@@ -41,7 +41,8 @@ EXPORTS = ["autoscout_space_create", "autoscout_space_destroy", "autoscout_space
 class SpaceInfo(ctypes.Structure):
     _fields_ = [("n_raw", ctypes.c_uint64), ("n_cvi", ctypes.c_uint64), ("n_features", ctypes.c_int32),
                 ("n_structures", ctypes.c_int32), ("n_prefix", ctypes.c_int32), ("n_components", ctypes.c_int32),
-                ("n_observed", ctypes.c_int32), ("max_observed", ctypes.c_int32), ("n_launches", ctypes.c_uint64)]
+                ("n_observed", ctypes.c_int32), ("max_observed", ctypes.c_int32), ("n_launches", ctypes.c_uint64),
+                ("fit_upload_bytes", ctypes.c_uint64)]
 
 
 class ScoreArgs(ctypes.Structure):

@@ -177,7 +177,9 @@ struct as_space {
   float* d_Bch = nullptr;          // L^-1^T hi/lo chunks for the tensor-core path
   std::vector<uint16_t> h_Tch;     // one-hot R2 operand T (FP16 hi/lo groups, kernels_tc2.cuh)
   std::vector<float> h_xh, h_oh;   // SIMT features of the one-hot kernel (scaled)
+  std::vector<uint16_t> h_Wch;     // L^-1^T FP16 hi/lo chunks of the one-hot kernel (scaled by 2^ew)
   uint16_t* d_Tch = nullptr;
+  uint16_t* d_Wch = nullptr;
   float *d_xh = nullptr, *d_oh = nullptr;
   Tc2B t2{};
   CandList list{};                 // compact valid-candidate list of one slice (kernels_gen.cuh)
@@ -205,6 +207,7 @@ struct as_space {
   std::vector<as_score_args> batches;
   bool scored = false;
   uint64_t n_launches = 0;
+  uint64_t fit_upload_bytes = 0;   // H2D bytes of the last GP upload (bench e2e accounting)
   // timing
   bool timing = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -330,6 +333,40 @@ as_status upload_gp(as_space* s, cudaStream_t st) {
         }
       }
     }
+    // L^-1^T chunks for the FP16 contraction: chunk c = rows i in [16c, Mp16) x columns j in
+    // [16c, 16c+16), 2^ew L^-1[i][j] split hi + lo FP16 (kmajor_off16); k is scaled by 2^ek in-kernel
+    {
+      double wmax = 0.0;
+      for (double w : F.Wl) wmax = std::max(wmax, std::fabs(w));
+      int ew = 0;
+      if (wmax > 0.0) {
+        while (wmax * std::ldexp(1.0, ew) > 32768.0) --ew;
+        while (wmax * std::ldexp(1.0, ew + 1) <= 32768.0) ++ew;
+      }
+      int ek = 0;
+      while (H.sf2 * std::ldexp(1.0, ek) > 32768.0) --ek;
+      while (H.sf2 * std::ldexp(1.0, ek + 1) <= 32768.0) ++ek;
+      t2.ek = ek;
+      t2.k_unscale = static_cast<float>(std::ldexp(1.0, -ek));
+      t2.vsq_unscale = static_cast<float>(std::ldexp(1.0, -2 * (ek + ew)));
+      s->h_Wch.clear();
+      for (int c = 0; c < nch; ++c) {
+        const int N = Mp16 - c * TC_KCH;
+        t2.woff[c] = static_cast<uint32_t>(s->h_Wch.size());
+        const size_t base = s->h_Wch.size();
+        s->h_Wch.resize(base + 2ull * N * TC_KCH, 0);
+        for (int n = 0; n < N; ++n)
+          for (int k = 0; k < TC_KCH; ++k) {
+            const int i = c * TC_KCH + n, j = c * TC_KCH + k;
+            double w = 0.0;
+            if (i < M && j < M && j <= i) w = std::ldexp(F.Wl[static_cast<size_t>(i) * M + j], ew);
+            const uint16_t hi = h16(w);
+            const uint32_t o = tc::kmajor_off16(n, k, TC_KCH / 8) / 2;
+            s->h_Wch[base + o] = hi;
+            s->h_Wch[base + static_cast<size_t>(N) * TC_KCH + o] = h16(w - v16(hi));
+          }
+      }
+    }
     const double hs = std::ldexp(1.0, sc / 2);
     s->h_xh.assign(static_cast<size_t>(4) * VMAX, 0.f);
     s->h_oh.assign(static_cast<size_t>(std::max(Mp16, 1)) * 4, 0.f);
@@ -354,9 +391,11 @@ as_status upload_gp(as_space* s, cudaStream_t st) {
   if (s->device < 0) return AS_OK;
   auto cp = [&](void* dst, const void* src, size_t bytes) -> as_status {
     if (bytes) CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    s->fit_upload_bytes += bytes;
     return AS_OK;
   };
   as_status r;
+  s->fit_upload_bytes = 0;
   if ((r = cp(s->d_O, s->h_O.data(), s->h_O.size() * 4)) != AS_OK) return r;
   if ((r = cp(s->d_alpha, s->h_alpha.data(), s->h_alpha.size() * 4)) != AS_OK) return r;
   if ((r = cp(s->d_aabs, s->h_aabs.data(), s->h_aabs.size() * 4)) != AS_OK) return r;
@@ -366,6 +405,8 @@ as_status upload_gp(as_space* s, cudaStream_t st) {
   if ((r = cp(s->d_W64, s->h_W64.data(), s->h_W64.size() * 8)) != AS_OK) return r;
   if ((r = cp(s->d_Bch, s->h_Bch.data(), s->h_Bch.size() * 4)) != AS_OK) return r;
   if ((r = cp(s->d_Tch, s->h_Tch.data(), s->h_Tch.size() * 2)) != AS_OK) return r;
+  if ((r = cp(s->d_Wch, s->h_Wch.data(), s->h_Wch.size() * 2)) != AS_OK) return r;
+  s->t2.wch = s->d_Wch;
   if ((r = cp(s->d_xh, s->h_xh.data(), s->h_xh.size() * 4)) != AS_OK) return r;
   if ((r = cp(s->d_oh, s->h_oh.data(), s->h_oh.size() * 4)) != AS_OK) return r;
   s->t2.tch = s->d_Tch;
@@ -756,6 +797,9 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
       return cleanup(r);
     if ((r = dalloc(&s->d_Tch, static_cast<size_t>(Mc) * 2 * s->t2.Kp, s->owned)) != AS_OK) return cleanup(r);
     if ((r = dalloc(&s->d_xh, static_cast<size_t>(4) * VMAX, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = dalloc(&s->d_Wch, static_cast<size_t>(2) * TC_KCH * (Mc / TC_KCH) * (Mc / TC_KCH + 1) / 2 * TC_KCH,
+                    s->owned)) != AS_OK)
+      return cleanup(r);
     if ((r = dalloc(&s->d_oh, static_cast<size_t>(Mc) * 4, s->owned)) != AS_OK) return cleanup(r);
     // pool buffers at capacity
     s->KC_max = KC_CAP;
@@ -812,6 +856,7 @@ as_status autoscout_space_info(const as_space* s, as_space_info* out) {
   out->n_observed = s->fit.M;
   out->max_observed = MMAX;
   out->n_launches = s->n_launches;
+  out->fit_upload_bytes = s->fit_upload_bytes;
   return AS_OK;
 }
 

@@ -27,7 +27,8 @@ namespace as {
 
 constexpr int TC2_RG = 4;                    // K-chunks per R2 group (N = 64)
 constexpr int TC2_RS = 2;                    // R2 group slots in TMEM
-constexpr int TC2_NB = 3;                    // L^-1 chunk ring stages (2 chunks prefetched: L2 latency)
+constexpr int TC2_NA = 8;                    // A ring stages (16 TMEM columns each: FP16 hi | lo)
+constexpr int TC2_NB = 4;                    // L^-1 chunk ring stages (3 chunks prefetched: L2 latency)
 constexpr int TC2_NT = 3;                    // T group ring stages
 constexpr int TC2_KPMAX = 64;                // one-hot width the host aims for (features beyond go SIMT)
 
@@ -51,7 +52,7 @@ constexpr size_t TC2_O_STG = TC2_O_XH + 4 * VMAX * 4;
 constexpr size_t TC2_O_VAR = TC2_O_STG + 2 * TC2_STG_BYTES;
 // + NB L^-1 stages (2 Mp16 16 4 B) + NT T stages (2 64 Kp 2 B) + 2 E buffers (128 Kp 2 B) + P keys
 __host__ __device__ constexpr size_t tc2_smem_total(int Mp16, int Kp, int P) {
-  return TC2_O_VAR + static_cast<size_t>(TC2_NB) * 2 * Mp16 * 16 * 4 + static_cast<size_t>(TC2_NT) * 2 * 64 * Kp * 2 +
+  return TC2_O_VAR + static_cast<size_t>(TC2_NB) * 2 * Mp16 * 16 * 2 + static_cast<size_t>(TC2_NT) * 2 * 64 * Kp * 2 +
          2ull * 128 * Kp * 2 + static_cast<size_t>(P) * 8;
 }
 
@@ -65,6 +66,12 @@ struct Tc2B {
   float r2_scale;               // 2^-s    (R2 in TMEM is 2^s r^2)
   float r_scale;                // 2^-s/2
   int eoff[DMAX];               // one-hot column of digit 0 of feature f (-1: SIMT feature)
+  // v = L^-1 k in kind::f16: k scaled by 2^ek and L^-1 by 2^ew, each split into FP16 hi + lo
+  const uint16_t* wch;          // L^-1^T chunks: chunk c = [hi (N_c x 16)][lo (N_c x 16)], kmajor_off16
+  uint32_t woff[TC_MAXCH];      // element offset of chunk c
+  int ek;                       // k scale exponent (kernel values leave the exp2 already scaled)
+  float k_unscale;              // 2^-ek
+  float vsq_unscale;            // 2^-2(ek + ew)
 };
 
 template <int PW, int KT, int NH>
@@ -86,8 +93,8 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
   const int Mp16 = TB.Mp16, nch = TB.nch, Kp = T2.Kp;
   const int ng = (nch + TC2_RG - 1) / TC2_RG;                         // R2 groups per tile
   const uint32_t A0col = static_cast<uint32_t>(Mp16);                 // TMEM column of A stage 0
-  const uint32_t R0col = A0col + 32u * TC_NA;                         // TMEM column of R2 stage 0
-  const uint32_t b_stage_bytes = 2u * Mp16 * TC_KCH * 4;              // L^-1 hi + lo at the widest chunk
+  const uint32_t R0col = A0col + 16u * TC2_NA;                        // TMEM column of R2 stage 0
+  const uint32_t b_stage_bytes = 2u * Mp16 * TC_KCH * 2;              // L^-1 FP16 hi + lo at the widest chunk
   const uint32_t t_stage_bytes = 2u * (TC2_RG * TC_KCH) * Kp * 2;     // T: 2 FP16 pieces x 64 points
   const uint32_t e_bytes = static_cast<uint32_t>(TC_ROWS) * Kp * 2;   // E: 128 rows x Kp FP16
   unsigned char* const sm0 = smem_raw;
@@ -112,8 +119,8 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
   uint64_t* arr = reinterpret_cast<uint64_t*>(E0 + 2ull * e_bytes);
   const uint32_t sB0 = tc::smem_u32(B0), sT0 = tc::smem_u32(T0), sE0 = tc::smem_u32(E0);
   uint64_t* a_full = bars;                     // [NA] count PW
-  uint64_t* a_empty = a_full + TC_NA;          // [NA] commit
-  uint64_t* b_full = a_empty + TC_NA;          // [NB] 1 + tx
+  uint64_t* a_empty = a_full + TC2_NA;          // [NA] commit
+  uint64_t* b_full = a_empty + TC2_NA;          // [NB] 1 + tx
   uint64_t* b_empty = b_full + TC2_NB;         // [NB] commit
   uint64_t* d_full = b_empty + TC2_NB;         // [1]  commit
   uint64_t* d_empty = d_full + 1;              // [1]  count PW
@@ -135,7 +142,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
   for (int i = tid; i < NH * Mp16; i += TC_THREADS) oh_s[i] = __ldg(T2.oh + i);
   for (int i = tid; i < NH * VMAX; i += TC_THREADS) xh_s[i] = __ldg(T2.xh + i);
   if (tid == 0) {
-    for (int s = 0; s < TC_NA; ++s) {
+    for (int s = 0; s < TC2_NA; ++s) {
       tc::mbar_init(a_full + s, TC_PROD_WARPS);
       tc::mbar_init(a_empty + s, 1);
     }
@@ -183,7 +190,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     // a = r^2 / 2 = (2^-s / 2) R2 (RBF); exp2 argument folds ln(sf2).
     const float c_arg = (KT == 0) ? 2.2360679774997896f * T2.r_scale : 0.5f * T2.r2_scale;
     const float ex_c1 = -c_arg * 1.4426950408889634f;
-    const float ex_c0 = log2f(G.sf2f);
+    const float ex_c0 = log2f(G.sf2f) + static_cast<float>(T2.ek);   // k leaves the exp2 scaled by 2^ek
     double* scratch = TB.scratch + (static_cast<size_t>(blockIdx.x) * TC_EPI_WARPS + (warp & 3)) * Mp16;
 
     // ---- epilogue of tile u (column blocks < nch - NA were accumulated during the chunk loop)
@@ -193,15 +200,20 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       tc::fence_after_sync();
       float vsq = vsq_run;
       const uint32_t taddr = lane_base + TC_JPT * jq;
-      for (int b = (nch > TC_NA ? nch - TC_NA : 0); b < nch; ++b) {
+      const int bfirst = nch > TC2_NA ? nch - TC2_NA : 0;
+      for (int b0 = bfirst; b0 < nch; b0 += 4) {
+        float v[16];
+        uint32_t ad[4];
 #pragma unroll
-        for (int h = 0; h < TC_JPT; h += 4) {
-          float v[4];
-          tc::tmem_ld4(taddr + 16 * b + h, v);
-          vsq = fmaf(v[0], v[0], fmaf(v[1], v[1], fmaf(v[2], v[2], fmaf(v[3], v[3], vsq))));
-        }
+        for (int i = 0; i < 4; ++i) ad[i] = taddr + 16u * static_cast<uint32_t>(b0 + i < nch ? b0 + i : b0);
+        tc::tmem_ld4x4(ad[0], ad[1], ad[2], ad[3], v);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (b0 + i < nch)
+            vsq = fmaf(v[4 * i], v[4 * i],
+                       fmaf(v[4 * i + 1], v[4 * i + 1], fmaf(v[4 * i + 2], v[4 * i + 2], fmaf(v[4 * i + 3], v[4 * i + 3], vsq))));
       }
-      vpart[jq * TC_ROWS + quad * 32 + lane] = vsq;
+      vpart[jq * TC_ROWS + quad * 32 + lane] = vsq * T2.vsq_unscale;
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(d_empty);
@@ -363,10 +375,10 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         for (int cg = 0; cg < TC2_RG; ++cg) {
           const int c = c0 + cg;
           if (c >= nch) break;
-          const int s = g % TC_NA;
-          const uint32_t a_par = ((g / TC_NA) & 1u) ^ 1u;
+          const int s = g % TC2_NA;
+          const uint32_t a_par = ((g / TC2_NA) & 1u) ^ 1u;
           const bool a_ready = tc::mbar_test(a_empty + s, a_par);
-          float kh[TC_JPT], kl[TC_JPT];
+          float kv[TC_JPT];
 #pragma unroll
           for (int q = 0; q < TC_JPT; ++q) {
             const int jo = c * TC_KCH + jq * TC_JPT + q;
@@ -402,13 +414,19 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
             mu_p = fmaf(kval, al, mu_p);
             sb_p = fmaf(cc, aa, sb_p);
             kk_p = fmaf(cc, cc, kk_p);
-            tc::split_tf32_fast(kval, kh[q], kl[q]);
+            kv[q] = kval;
           }
+          // FP16 hi / lo split of the (2^ek-scaled) cross-covariances, packed two per column
+          const uint32_t h01 = tc::pack_f16x2(kv[0], kv[1]), h23 = tc::pack_f16x2(kv[2], kv[3]);
+          float f0, f1, f2, f3;
+          tc::unpack_f16x2(h01, f0, f1);
+          tc::unpack_f16x2(h23, f2, f3);
+          const uint32_t l01 = tc::pack_f16x2(kv[0] - f0, kv[1] - f1), l23 = tc::pack_f16x2(kv[2] - f2, kv[3] - f3);
           if (!a_ready) tc::mbar_wait(a_empty + s, a_par);
           tc::fence_after_sync();
-          const uint32_t acol = lane_base + A0col + 32u * s + jq * TC_JPT;
-          tc::tmem_st4(acol, kh[0], kh[1], kh[2], kh[3]);
-          tc::tmem_st4(acol + 16, kl[0], kl[1], kl[2], kl[3]);
+          const uint32_t acol = lane_base + A0col + 16u * s + 2 * jq;
+          tc::tmem_st2(acol, h01, h23);
+          tc::tmem_st2(acol + 8, l01, l23);
           tc::tmem_st_wait();
           tc::fence_before_sync();
           __syncwarp();
@@ -419,20 +437,20 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         // [c0 - NA, c_last - NA]; one batched read (the last NA blocks are left to the epilogue)
         {
           const int c_last = (c0 + TC2_RG < nch ? c0 + TC2_RG : nch) - 1;
-          const int b0 = c0 - TC_NA;
-          if (c_last - TC_NA >= 0) {
+          const int b0 = c0 - TC2_NA;
+          if (c_last - TC2_NA >= 0) {
             float v[16];
             uint32_t ad[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               const int b = b0 + i;
-              ad[i] = dq + 16u * static_cast<uint32_t>(b >= 0 && b <= c_last - TC_NA ? b : 0);
+              ad[i] = dq + 16u * static_cast<uint32_t>(b >= 0 && b <= c_last - TC2_NA ? b : 0);
             }
             tc::tmem_ld4x4(ad[0], ad[1], ad[2], ad[3], v);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               const int b = b0 + i;
-              if (b >= 0 && b <= c_last - TC_NA)
+              if (b >= 0 && b <= c_last - TC2_NA)
                 vsq_run = fmaf(v[4 * i], v[4 * i],
                                fmaf(v[4 * i + 1], v[4 * i + 1], fmaf(v[4 * i + 2], v[4 * i + 2], fmaf(v[4 * i + 3], v[4 * i + 3], vsq_run))));
             }
@@ -440,9 +458,9 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         }
       }
       float* mp = m_part + (t % TC_TI) * 3 * TC_ROWS;
-      atomicAdd(mp + cand, mu_p);
-      atomicAdd(mp + TC_ROWS + cand, sb_p);
-      atomicAdd(mp + 2 * TC_ROWS + cand, kk_p);
+      atomicAdd(mp + cand, mu_p * T2.k_unscale);
+      atomicAdd(mp + TC_ROWS + cand, sb_p * T2.k_unscale);
+      atomicAdd(mp + 2 * TC_ROWS + cand, kk_p * (T2.k_unscale * T2.k_unscale));
       epilogue(t, vsq_run);
       named_sync(1, TC_PROD_THREADS);
       n_cur = n_next;
@@ -477,9 +495,9 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       const int s = gl % TC2_NB;
       tc::mbar_wait(b_empty + s, ((gl / TC2_NB) & 1u) ^ 1u);
       if (lane == 0) {
-        const uint32_t bytes = 2u * (Mp16 - lc * TC_KCH) * TC_KCH * 4;
+        const uint32_t bytes = 2u * (Mp16 - lc * TC_KCH) * TC_KCH * 2;
         tc::mbar_arrive_expect_tx(b_full + s, bytes);
-        tc::bulk_g2s(B0 + static_cast<size_t>(s) * b_stage_bytes, TB.chunks + TB.off[lc], bytes, b_full + s);
+        tc::bulk_g2s(B0 + static_cast<size_t>(s) * b_stage_bytes, T2.wch + T2.woff[lc], bytes, b_full + s);
       }
       ++gl;
       if (++lc == nch) lc = 0;
@@ -517,7 +535,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     __syncwarp();
     const uint32_t sbo16 = (Kp / 8) * 128;
     const uint64_t dE = tc::sdesc(sE0, 128, sbo16), dT = tc::sdesc(sT0, 128, sbo16);
-    const uint64_t dB = tc::sdesc(sB0, 128, (TC_KCH / 4) * 128);
+    const uint64_t dB = tc::sdesc(sB0, 128, (TC_KCH / 8) * 128);
     const uint32_t piece16 = ((TC2_RG * TC_KCH) * Kp * 2) >> 4;   // descriptor units (16 B)
     const uint32_t idesc_r = tc::idesc_f16(TC_ROWS, TC2_RG * TC_KCH);
     const int ksteps_r = Kp / 16;
@@ -561,28 +579,26 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         // c + NA must be issued before M(g); never beyond the next tile (tile t+2 is published
         // only after the epilogue of tile t, which needs MMAs not issued yet).
         {
-          const int cn = c + TC_NA;
+          const int cn = c + TC2_NA;
           const uint32_t target = cn < nch ? static_cast<uint32_t>(t * ng + cn / TC2_RG)
                                            : static_cast<uint32_t>((t + 1) * ng + min((cn - nch) / TC2_RG, ng - 1));
           while (x <= target && issue_R()) {
           }
         }
-        const int sa = g % TC_NA, sbb = g % TC2_NB;
-        tc::mbar_wait(a_full + sa, (g / TC_NA) & 1);
+        const int sa = g % TC2_NA, sbb = g % TC2_NB;
+        tc::mbar_wait(a_full + sa, (g / TC2_NA) & 1);
         tc::mbar_wait(b_full + sbb, (g / TC2_NB) & 1);
         tc::fence_after_sync();
         const int N = Mp16 - c * TC_KCH;
-        const uint32_t idesc = tc::idesc_tf32(TC_ROWS, N);
-        const uint32_t a_h = tmem + A0col + 32u * sa, a_l = a_h + 16;
+        const uint32_t idesc = tc::idesc_f16(TC_ROWS, N);
+        const uint32_t a_h = tmem + A0col + 16u * sa, a_l = a_h + 8;
         const uint64_t bh = dB + ((sbb * b_stage_bytes) >> 4);
-        const uint64_t bl = bh + ((N * TC_KCH * 4) >> 4);
+        const uint64_t bl = bh + ((N * TC_KCH * 2) >> 4);
         const uint32_t d = tmem + c * TC_KCH;
-#pragma unroll
-        for (int ks = 0; ks < TC_KCH / 8; ++ks) {
-          tc::mma_tf32_ts_w(d, a_h + 8 * ks, bh + 16 * ks, idesc, (c > 0 || ks > 0) ? 1u : 0u);
-          tc::mma_tf32_ts_w(d, a_h + 8 * ks, bl + 16 * ks, idesc, 1u);
-          tc::mma_tf32_ts_w(d, a_l + 8 * ks, bh + 16 * ks, idesc, 1u);
-        }
+        // 3-term FP16 split: hi.hi + hi.lo + lo.hi (one K = 16 step each)
+        tc::mma_f16_ts_w(d, a_h, bh, idesc, c > 0 ? 1u : 0u);
+        tc::mma_f16_ts_w(d, a_h, bl, idesc, 1u);
+        tc::mma_f16_ts_w(d, a_l, bh, idesc, 1u);
         tc::mma_commit_w(a_empty + sa);
         tc::mma_commit_w(b_empty + sbb);
         load_L();
