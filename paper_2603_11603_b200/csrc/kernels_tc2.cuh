@@ -28,7 +28,9 @@ namespace as {
 constexpr int TC2_RG = 4;                    // K-chunks per R2 group (N = 64)
 constexpr int TC2_RS = 2;                    // R2 group slots in TMEM
 constexpr int TC2_NA = 8;                    // A ring stages (16 TMEM columns each: FP16 hi | lo)
-constexpr int TC2_NB = 4;                    // L^-1 chunk ring stages (3 chunks prefetched: L2 latency)
+constexpr int TC2_NB = 6;                    // L^-1 chunk ring stages
+constexpr int TC2_PF = TC2_NB - 2;           // chunks prefetched ahead of the MMA (L2 latency); a refill
+                                             // waits for the MMAs two chunks back, not the previous one
 constexpr int TC2_NT = 3;                    // T group ring stages
 constexpr int TC2_KPMAX = 64;                // one-hot width the host aims for (features beyond go SIMT)
 
@@ -348,120 +350,140 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     uint32_t g = 0;                                   // global chunk counter (A ring)
     uint32_t gr = 0;                                  // global R2 group counter
     const uint32_t sOH = tc::smem_u32(oh_s);
-    for (int t = 0; n_cur > 0; ++t) {
-      const int n_next = publish(t + 1);
-      // ---- chunk loop: R2 (+ SIMT features) -> k -> A ring
-      float mu_p = 0.f, sb_p = 0.f, kk_p = 0.f, vsq_run = 0.f;
+    // Chunks [cb, ce) of tile u (cb a multiple of the R2 group size; ce == nch or a multiple of it):
+    // R2 (+ SIMT features) -> k -> A ring; partial sums accumulate into the caller's registers.
+    auto produce = [&](int u, int cb, int ce, float& mu_p, float& sb_p, float& kk_p, float& vsq_run) {
       const uint32_t dq = lane_base + TC_JPT * jq;
       unsigned long long xhp[NH > 0 ? NH / 2 : 1];
 #pragma unroll
       for (int h = 0; h < NH / 2; ++h) {
-        const float* xq = m_xh + ((t % TC_TI) * TC_ROWS + cand) * (NH > 0 ? NH : 1) + 2 * h;
+        const float* xq = m_xh + ((u % TC_TI) * TC_ROWS + cand) * (NH > 0 ? NH : 1) + 2 * h;
         xhp[h] = f2_pack(xq[0], xq[1]);
       }
-      for (int c0 = 0; c0 < nch; c0 += TC2_RG) {
-        // ---- one R2 group: the thread's 4 points of each of the 4 chunks are 16 contiguous
-        // columns (T rows are permuted on the host), read with one load
-        const int rs = gr % TC2_RS;
-        float rv[TC2_RG * TC_JPT];
-        tc::mbar_wait(r_full + rs, (gr / TC2_RS) & 1u);
-        tc::fence_after_sync();
-        tc::tmem_ld16(lane_base + R0col + 64u * rs + 16u * jq, rv);
-        tc::fence_before_sync();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(r_empty + rs);
-        ++gr;
-#pragma unroll
-        for (int cg = 0; cg < TC2_RG; ++cg) {
-          const int c = c0 + cg;
-          if (c >= nch) break;
-          const int s = g % TC2_NA;
-          const uint32_t a_par = ((g / TC2_NA) & 1u) ^ 1u;
-          const bool a_ready = tc::mbar_test(a_empty + s, a_par);
-          float kv[TC_JPT];
-#pragma unroll
-          for (int q = 0; q < TC_JPT; ++q) {
-            const int jo = c * TC_KCH + jq * TC_JPT + q;
-            float r2s = rv[cg * TC_JPT + q];
-            if (NH > 0) {
-              unsigned long long acc = 0ull;
-#pragma unroll
-              for (int h = 0; h < NH / 2; ++h) {
-                unsigned long long o2;
-                asm volatile("ld.shared.b64 %0, [%1];" : "=l"(o2) : "r"(sOH + 4u * (jo * NH + 2 * h)));
-                const unsigned long long dd = f2_sub(xhp[h], o2);
-                acc = f2_fma(dd, dd, acc);
-              }
-              const float2 a2 = f2_unpack(acc);
-              r2s += a2.x + a2.y;
-            }
-            const float r2 = fmaxf(r2s, 0.f);
-            float arg, poly, ex;
-            if (KT == 0) {
-              const float r = tc::sqrt_approx_ftz(r2);
-              arg = c_arg * r;
-              poly = fmaf(arg, fmaf(arg, 0.33333333333333333f, 1.0f), 1.0f);
-              ex = tc::ex2_approx(fmaf(r, ex_c1, ex_c0));
-            } else {
-              arg = c_arg * r2;
-              poly = 1.0f;
-              ex = tc::ex2_approx(fmaf(r2, ex_c1, ex_c0));
-            }
-            const float kval = poly * ex;
-            const float cc = fmaf(kval, arg, kval);
-            float al, aa;
-            tc::lds_f32x2(sAl + 8 * jo, al, aa);
-            mu_p = fmaf(kval, al, mu_p);
-            sb_p = fmaf(cc, aa, sb_p);
-            kk_p = fmaf(cc, cc, kk_p);
-            kv[q] = kval;
-          }
-          // FP16 hi / lo split of the (2^ek-scaled) cross-covariances, packed two per column
-          const uint32_t h01 = tc::pack_f16x2(kv[0], kv[1]), h23 = tc::pack_f16x2(kv[2], kv[3]);
-          float f0, f1, f2, f3;
-          tc::unpack_f16x2(h01, f0, f1);
-          tc::unpack_f16x2(h23, f2, f3);
-          const uint32_t l01 = tc::pack_f16x2(kv[0] - f0, kv[1] - f1), l23 = tc::pack_f16x2(kv[2] - f2, kv[3] - f3);
-          if (!a_ready) tc::mbar_wait(a_empty + s, a_par);
+        for (int c0 = cb; c0 < ce; c0 += TC2_RG) {
+          // ---- one R2 group: the thread's 4 points of each of the 4 chunks are 16 contiguous
+          // columns (T rows are permuted on the host), read with one load
+          const int rs = gr % TC2_RS;
+          float rv[TC2_RG * TC_JPT];
+          tc::mbar_wait(r_full + rs, (gr / TC2_RS) & 1u);
           tc::fence_after_sync();
-          const uint32_t acol = lane_base + A0col + 16u * s + 2 * jq;
-          tc::tmem_st2(acol, h01, h23);
-          tc::tmem_st2(acol + 8, l01, l23);
-          tc::tmem_st_wait();
+          tc::tmem_ld16(lane_base + R0col + 64u * rs + 16u * jq, rv);
           tc::fence_before_sync();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive(a_full + s);
-          ++g;
-        }
-        // ---- accumulator column blocks made final by this group's a_empty waits:
-        // [c0 - NA, c_last - NA]; one batched read (the last NA blocks are left to the epilogue)
-        {
-          const int c_last = (c0 + TC2_RG < nch ? c0 + TC2_RG : nch) - 1;
-          const int b0 = c0 - TC2_NA;
-          if (c_last - TC2_NA >= 0) {
-            float v[16];
-            uint32_t ad[4];
+          if (lane == 0) tc::mbar_arrive(r_empty + rs);
+          ++gr;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int b = b0 + i;
-              ad[i] = dq + 16u * static_cast<uint32_t>(b >= 0 && b <= c_last - TC2_NA ? b : 0);
+          for (int cg = 0; cg < TC2_RG; ++cg) {
+            const int c = c0 + cg;
+            if (c >= nch) break;
+            const int s = g % TC2_NA;
+            const uint32_t a_par = ((g / TC2_NA) & 1u) ^ 1u;
+            const bool a_ready = tc::mbar_test(a_empty + s, a_par);
+            float kv[TC_JPT];
+#pragma unroll
+            for (int q = 0; q < TC_JPT; ++q) {
+              const int jo = c * TC_KCH + jq * TC_JPT + q;
+              float r2s = rv[cg * TC_JPT + q];
+              if (NH > 0) {
+                unsigned long long acc = 0ull;
+#pragma unroll
+                for (int h = 0; h < NH / 2; ++h) {
+                  unsigned long long o2;
+                  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(o2) : "r"(sOH + 4u * (jo * NH + 2 * h)));
+                  const unsigned long long dd = f2_sub(xhp[h], o2);
+                  acc = f2_fma(dd, dd, acc);
+                }
+                const float2 a2 = f2_unpack(acc);
+                r2s += a2.x + a2.y;
+              }
+              const float r2 = fmaxf(r2s, 0.f);
+              float arg, poly, ex;
+              if (KT == 0) {
+                const float r = tc::sqrt_approx_ftz(r2);
+                arg = c_arg * r;
+                poly = fmaf(arg, fmaf(arg, 0.33333333333333333f, 1.0f), 1.0f);
+                ex = tc::ex2_approx(fmaf(r, ex_c1, ex_c0));
+              } else {
+                arg = c_arg * r2;
+                poly = 1.0f;
+                ex = tc::ex2_approx(fmaf(r2, ex_c1, ex_c0));
+              }
+              const float kval = poly * ex;
+              const float cc = fmaf(kval, arg, kval);
+              float al, aa;
+              tc::lds_f32x2(sAl + 8 * jo, al, aa);
+              mu_p = fmaf(kval, al, mu_p);
+              sb_p = fmaf(cc, aa, sb_p);
+              kk_p = fmaf(cc, cc, kk_p);
+              kv[q] = kval;
             }
-            tc::tmem_ld4x4(ad[0], ad[1], ad[2], ad[3], v);
+            // FP16 hi / lo split of the (2^ek-scaled) cross-covariances, packed two per column
+            const uint32_t h01 = tc::pack_f16x2(kv[0], kv[1]), h23 = tc::pack_f16x2(kv[2], kv[3]);
+            float f0, f1, f2, f3;
+            tc::unpack_f16x2(h01, f0, f1);
+            tc::unpack_f16x2(h23, f2, f3);
+            const uint32_t l01 = tc::pack_f16x2(kv[0] - f0, kv[1] - f1), l23 = tc::pack_f16x2(kv[2] - f2, kv[3] - f3);
+            if (!a_ready) tc::mbar_wait(a_empty + s, a_par);
+            tc::fence_after_sync();
+            const uint32_t acol = lane_base + A0col + 16u * s + 2 * jq;
+            tc::tmem_st2(acol, h01, h23);
+            tc::tmem_st2(acol + 8, l01, l23);
+            tc::tmem_st_wait();
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(a_full + s);
+            ++g;
+          }
+          // ---- accumulator column blocks made final by this group's a_empty waits:
+          // [c0 - NA, c_last - NA]; one batched read (the last NA blocks are left to the epilogue)
+          {
+            const int c_last = (c0 + TC2_RG < nch ? c0 + TC2_RG : nch) - 1;
+            const int b0 = c0 - TC2_NA;
+            if (c_last - TC2_NA >= 0) {
+              float v[16];
+              uint32_t ad[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int b = b0 + i;
-              if (b >= 0 && b <= c_last - TC2_NA)
-                vsq_run = fmaf(v[4 * i], v[4 * i],
-                               fmaf(v[4 * i + 1], v[4 * i + 1], fmaf(v[4 * i + 2], v[4 * i + 2], fmaf(v[4 * i + 3], v[4 * i + 3], vsq_run))));
+              for (int i = 0; i < 4; ++i) {
+                const int b = b0 + i;
+                ad[i] = dq + 16u * static_cast<uint32_t>(b >= 0 && b <= c_last - TC2_NA ? b : 0);
+              }
+              tc::tmem_ld4x4(ad[0], ad[1], ad[2], ad[3], v);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int b = b0 + i;
+                if (b >= 0 && b <= c_last - TC2_NA)
+                  vsq_run = fmaf(v[4 * i], v[4 * i],
+                                 fmaf(v[4 * i + 1], v[4 * i + 1], fmaf(v[4 * i + 2], v[4 * i + 2], fmaf(v[4 * i + 3], v[4 * i + 3], vsq_run))));
+              }
             }
           }
         }
-      }
-      float* mp = m_part + (t % TC_TI) * 3 * TC_ROWS;
+    };
+    auto flush_part = [&](int u, float mu_p, float sb_p, float kk_p) {
+      float* mp = m_part + (u % TC_TI) * 3 * TC_ROWS;
       atomicAdd(mp + cand, mu_p * T2.k_unscale);
       atomicAdd(mp + TC_ROWS + cand, sb_p * T2.k_unscale);
       atomicAdd(mp + 2 * TC_ROWS + cand, kk_p * (T2.k_unscale * T2.k_unscale));
-      epilogue(t, vsq_run);
+    };
+
+    // Tile loop.  Before the epilogue of tile t (which waits for all of t's MMAs) the producers
+    // already produce the first NA chunks of tile t+1 into the A ring, so the MMA drain of tile t
+    // overlaps useful work and the MMAs of t+1 start as soon as the accumulator is read out.
+    const int head = nch < TC2_NA ? nch : TC2_NA;    // multiple of the R2 group size, or all of nch
+    float mu_c = 0.f, sb_c = 0.f, kk_c = 0.f, vsq_c = 0.f;   // tile t's running sums
+    int pre = 0;                                              // chunks of tile t already produced
+    for (int t = 0; n_cur > 0; ++t) {
+      const int n_next = publish(t + 1);
+      produce(t, pre, nch, mu_c, sb_c, kk_c, vsq_c);
+      flush_part(t, mu_c, sb_c, kk_c);
+      const float vsq_t = vsq_c;
+      mu_c = sb_c = kk_c = vsq_c = 0.f;
+      pre = 0;
+      if (n_next > 0) {
+        produce(t + 1, 0, head, mu_c, sb_c, kk_c, vsq_c);
+        pre = head;
+      }
+      epilogue(t, vsq_t);
       named_sync(1, TC_PROD_THREADS);
       n_cur = n_next;
     }
@@ -565,7 +587,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     load_S(0);
     load_S(1);
     if (tile_exists(0)) {
-      for (int i = 0; i < TC2_NB - 1; ++i) load_L();
+      for (int i = 0; i < TC2_PF; ++i) load_L();
       for (int i = 0; i < TC2_NT - 1; ++i) load_T();
     }
     const uint32_t sbo = (TC_KCH / 4) * 128;
