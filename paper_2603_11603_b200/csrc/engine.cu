@@ -526,7 +526,7 @@ as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, b
 as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStream_t st) {
   const bool gp = (a.acq != AS_ACQ_SIM) && s->G.M > 0;
   int P = next_pow2_h(s->KC + SCORE_THREADS);
-  const int P_tc2 = next_pow2_h(s->KC + TC_ROWS);   // one 128-row tile is admitted at a time
+  const int P_tc2 = next_pow2_h(s->KC + 4 * TC_ROWS);   // lazy admission: room for >= 3 tiles before a prune
   const bool tc2_fits = tc2_smem_bytes(s->tb.Mp16, s->t2.Kp, s->t2.nh, P_tc2) <= static_cast<size_t>(s->smem_optin);
   const bool use_tc2 = gp && (s->path == 3 || (s->path == 0 && s->G.M >= 64 && tc2_fits && s->tc2_auto));
   const bool use_tc = !use_tc2 && gp && (s->path == 2 || (s->path == 0 && s->G.M >= 64));

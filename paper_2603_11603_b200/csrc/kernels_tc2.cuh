@@ -76,6 +76,37 @@ struct Tc2B {
   float vsq_unscale;            // 2^-2(ek + ew)
 };
 
+// Lazy top-k' admission: keys below the (possibly stale) threshold tau are appended to the
+// unsorted tail of arr; the sort-and-prune to KC entries runs only when the next tile could
+// overflow arr (P - 128 entries), and once at the end.  tau only ever tightens, so a stale tau
+// admits more keys, never fewer; rejected keys update drop exactly as in group_admit.
+__device__ __forceinline__ void tc2_prune(uint64_t* arr, TopkSmem& ts, int KC, int t, int nt, int id) {
+  const int n_tot = ts.n_list + ts.n_add;
+  if (n_tot > 0) group_bitonic(arr, next_pow2(n_tot < 2 ? 2 : n_tot), t, nt, id);
+  const int keep = n_tot < KC ? n_tot : KC;
+  if (t == 0) {
+    if (n_tot > KC && arr[KC] < ts.drop) ts.drop = arr[KC];
+    ts.n_list = keep;
+    ts.tau = (keep == KC) ? arr[KC - 1] : KEY_NONE;
+    ts.n_add = 0;
+  }
+  for (int i = keep + t; i < n_tot; i += nt) arr[i] = KEY_NONE;
+  named_sync(id, nt);
+}
+__device__ __forceinline__ void tc2_admit(uint64_t key, uint64_t* arr, TopkSmem& ts, int KC, int P, int t, int nt,
+                                          int id) {
+  if (key != KEY_NONE) {
+    if (key < ts.tau) {
+      const int pos = atomicAdd(&ts.n_add, 1);
+      arr[ts.n_list + pos] = key;
+    } else {
+      atomicMin(reinterpret_cast<unsigned long long*>(&ts.drop), static_cast<unsigned long long>(key));
+    }
+  }
+  named_sync(id, nt);
+  if (ts.n_list + ts.n_add > P - 128) tc2_prune(arr, ts, KC, t, nt, id);
+}
+
 template <int PW, int KT, int NH>
 __global__ void __launch_bounds__(PW * 32 + 32, 1)
 score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, CandList L) {
@@ -291,7 +322,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
           }
         }
       }
-      group_admit(key, arr, ts, out.KC, pt, TC_PROD_THREADS, 1);
+      tc2_admit(key, arr, ts, out.KC, out.P, pt, TC_PROD_THREADS, 1);
     };
 
     // publish tile u: meta rows, zeroed partial sums, one-hot rows E[u & 1] and the SIMT-feature
@@ -487,8 +518,9 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       named_sync(1, TC_PROD_THREADS);
       n_cur = n_next;
     }
-    // ---- CTA list
+    // ---- CTA list (final prune: sorted, at most KC entries)
     named_sync(1, TC_PROD_THREADS);
+    tc2_prune(arr, ts, out.KC, pt, TC_PROD_THREADS, 1);
     const int n = ts.n_list;
     uint64_t* dst = out.lists + static_cast<size_t>(blockIdx.x) * out.KC;
     for (int i = pt; i < n; i += TC_PROD_THREADS) dst[i] = arr[i];
