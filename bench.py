@@ -334,7 +334,35 @@ def run_ours(args):
         if os.path.exists(prof):
             with open(prof) as fh:
                 traffic = json.load(fh).get("dram_bytes_per_launch")
-        if tc_path:
+        if tc_path and one_hot:
+            # score_tc2_kernel: v = L^-1 k as a 3-term FP16 split (FP32-accurate; bf16 peak / 3) and
+            # r^2 as the one-hot FP16 contraction (bf16 peak) on the tensor pipe; k(r) on FP32 + MUFU.
+            bf16 = tf32_peak_tflops() * 2.25 / 1.1
+            f_con, f_r2 = M * (M + 1), 3 * d * M
+            f_rest = M * 10 + 4 * M
+            mufu_per_valid = 2 * M
+            t_ten = valid_per_step * (f_con / (bf16 / 3.0) + f_r2 / bf16) / 1e12
+            t_fp32 = valid_per_step * f_rest / (peak * 1e12)
+            mufu_peak = 148 * 16 * sm_max * 1e6                  # MUFU ops/s (16 / clk / SM)
+            t_mufu = valid_per_step * mufu_per_valid / mufu_peak
+            sec = score_ms * 1e-3
+            ten_peak = (f_con + f_r2) / (f_con / (bf16 / 3.0) + f_r2 / bf16)
+            ten_ach = (f_con + f_r2) * valid_per_step / sec / 1e12
+            legs = {"tensor": t_ten, "mufu": t_mufu, "fp32": t_fp32}
+            binding = max(legs, key=legs.get)
+            roof = {"bound": "tensor", "kernel": "score_tc2_kernel", "achieved": ten_ach, "peak": ten_peak,
+                    "unit": "TFLOP/s", "frac": ten_ach / ten_peak, "traffic": traffic, "kernel_ms": score_ms,
+                    "merge_ms": merge_ms, "kernel_share": score_ms / ms_per_step,
+                    "peak_source": "measured bf16 dense peak (MEASURED_PEAKS.json); L^-1 k as 3 FP16 MMAs -> /3",
+                    "flops_per_valid": {"contraction_fp32eq": f_con, "r2_onehot": f_r2, "k_eval_fp32": f_rest},
+                    "legs_ms": {k_: 1e3 * v for k_, v in legs.items()}, "binding_leg": binding,
+                    "mufu": {"ops_per_valid": mufu_per_valid, "achieved_per_s": valid_per_step * mufu_per_valid / sec,
+                             "peak_per_s": mufu_peak, "frac": valid_per_step * mufu_per_valid / sec / mufu_peak},
+                    "t_bound_ms": 1e3 * max(legs.values()),
+                    "gen": {"kernel": "gen_kernel", "ms": gen_ms, "share": gen_ms / ms_per_step,
+                            "candidates_per_s": count / (gen_ms * 1e-3) if gen_ms > 0 else None,
+                            "note": "decode + mask + simulator + list append (integer / FP64)"}}
+        elif tc_path:
             simt_ach = f_simt * valid_per_step / (score_ms * 1e-3) / 1e12
             tc_ach = f_tc * valid_per_step / (score_ms * 1e-3) / 1e12
             tc_peak = tf32_peak_tflops() / 3.0
@@ -343,17 +371,13 @@ def run_ours(args):
                 bound, ach, pk, src = "tensor", tc_ach, tc_peak, "tcgen05 TF32 = measured bf16 x 1.1/2.25, /3 for 3xTF32"
             else:
                 bound, ach, pk, src = "alu", simt_ach, peak, f"FP32 SIMT 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz"
-            roof = {"bound": bound, "kernel": "score_tc2_kernel" if one_hot else "score_tc_kernel",
+            roof = {"bound": bound, "kernel": "score_tc_kernel",
                     "achieved": ach, "peak": pk, "unit": "TFLOP/s",
                     "frac": ach / pk, "traffic": traffic, "kernel_ms": score_ms, "merge_ms": merge_ms,
                     "kernel_share": score_ms / ms_per_step, "peak_source": src,
                     "simt": {"flops_per_valid": f_simt, "achieved": simt_ach, "peak": peak, "frac": simt_ach / peak},
                     "tensor": {"flops_per_valid": f_tc, "achieved": tc_ach, "peak": tc_peak, "frac": tc_ach / tc_peak},
                     "t_bound_ms": 1e3 * max(t_simt, t_tc)}
-            if one_hot:
-                roof["gen"] = {"kernel": "gen_kernel", "ms": gen_ms, "share": gen_ms / ms_per_step,
-                               "candidates_per_s": count / (gen_ms * 1e-3) if gen_ms > 0 else None,
-                               "note": "decode + mask + simulator + list append (integer / FP64, latency-bound)"}
         else:
             roof = {"bound": "alu", "kernel": "score_kernel", "achieved": achieved, "peak": peak,
                     "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": traffic,
@@ -368,7 +392,8 @@ def run_ours(args):
                        "candidates_per_step": count, "observed_M": M, "acq": acq, "k": k,
                        "valid_per_step": valid_per_step_all, "l2": "flushed (256 MiB write) before every timed step",
                        "parallelism": f"dp{world} (candidate-range shards, one all-gather)",
-                       "arith": "decode int; simulator + resource check + acquisition FP64; GP FP32; refine FP64"},
+                       "arith": "decode int; simulator + resource check FP64; r^2 one-hot FP16 hi/lo MMA (FP32 accumulate); "
+                                "k FP32; L^-1 k 3-term FP16 MMA (FP32-accurate); screen FP32 + bound; refine FP64"},
             "valid_per_s": valid_per_step_all / (ms_per_step / 1e3),
             "roofline": roof,
             "e2e": {"value": count / (e2e_step_ms / 1e3), "unit": "candidates/s", "ms_per_step": e2e_step_ms,
