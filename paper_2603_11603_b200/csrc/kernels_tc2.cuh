@@ -166,13 +166,18 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
   uint64_t* s_empty = s_full + 2;              // [2]  count PW
 
   // ---- setup
+  // point-pair layout: [al_2p, al_2p+1, |al_2p|, |al_2p+1|] so one LDS.128 feeds packed f32x2 math
   for (int i = tid; i < Mp16; i += TC_THREADS) {
-    alpha_s[2 * i] = i < G.Mp ? __ldg(G.alpha + i) : 0.f;
-    alpha_s[2 * i + 1] = i < G.Mp ? __ldg(G.aabs + i) : 0.f;
+    alpha_s[4 * (i >> 1) + (i & 1)] = i < G.Mp ? __ldg(G.alpha + i) : 0.f;
+    alpha_s[4 * (i >> 1) + 2 + (i & 1)] = i < G.Mp ? __ldg(G.aabs + i) : 0.f;
   }
   for (int i = tid; i < out.P; i += TC_THREADS) arr[i] = KEY_NONE;
   if (tid < DMAX) eoff_s[tid] = T2.eoff[tid];
-  for (int i = tid; i < NH * Mp16; i += TC_THREADS) oh_s[i] = __ldg(T2.oh + i);
+  // SIMT features, point-pair layout: [pair][h][2 points]
+  for (int i = tid; i < NH * Mp16; i += TC_THREADS) {
+    const int j = i / (NH > 0 ? NH : 1), h = i - j * NH;
+    oh_s[(j >> 1) * 2 * NH + 2 * h + (j & 1)] = __ldg(T2.oh + i);
+  }
   for (int i = tid; i < NH * VMAX; i += TC_THREADS) xh_s[i] = __ldg(T2.xh + i);
   if (tid == 0) {
     for (int s = 0; s < TC2_NA; ++s) {
@@ -383,14 +388,18 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     const uint32_t sOH = tc::smem_u32(oh_s);
     // Chunks [cb, ce) of tile u (cb a multiple of the R2 group size; ce == nch or a multiple of it):
     // R2 (+ SIMT features) -> k -> A ring; partial sums accumulate into the caller's registers.
-    auto produce = [&](int u, int cb, int ce, float& mu_p, float& sb_p, float& kk_p, float& vsq_run) {
+    auto produce = [&](int u, int cb, int ce, unsigned long long& mu2, unsigned long long& sb2,
+                       unsigned long long& kk2, float& vsq_run) {
       const uint32_t dq = lane_base + TC_JPT * jq;
-      unsigned long long xhp[NH > 0 ? NH / 2 : 1];
+      unsigned long long xb[NH > 0 ? NH : 1];                 // (x_h, x_h): broadcast over a point pair
 #pragma unroll
-      for (int h = 0; h < NH / 2; ++h) {
-        const float* xq = m_xh + ((u % TC_TI) * TC_ROWS + cand) * (NH > 0 ? NH : 1) + 2 * h;
-        xhp[h] = f2_pack(xq[0], xq[1]);
+      for (int h = 0; h < NH; ++h) {
+        const float xv = m_xh[((u % TC_TI) * TC_ROWS + cand) * (NH > 0 ? NH : 1) + h];
+        xb[h] = f2_pack(xv, xv);
       }
+      const unsigned long long carg2 = f2_pack(c_arg, c_arg), c1_2 = f2_pack(ex_c1, ex_c1),
+                               c0_2 = f2_pack(ex_c0, ex_c0), one2 = f2_pack(1.0f, 1.0f),
+                               third2 = f2_pack(0.33333333333333333f, 0.33333333333333333f);
         for (int c0 = cb; c0 < ce; c0 += TC2_RG) {
           // ---- one R2 group: the thread's 4 points of each of the 4 chunks are 16 contiguous
           // columns (T rows are permuted on the host), read with one load
@@ -411,42 +420,47 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
             const uint32_t a_par = ((g / TC2_NA) & 1u) ^ 1u;
             const bool a_ready = tc::mbar_test(a_empty + s, a_par);
             float kv[TC_JPT];
+            // two observed points at a time in packed f32x2 (FFMA2 / FMUL2); MUFU stays scalar
 #pragma unroll
-            for (int q = 0; q < TC_JPT; ++q) {
-              const int jo = c * TC_KCH + jq * TC_JPT + q;
-              float r2s = rv[cg * TC_JPT + q];
+            for (int qp = 0; qp < TC_JPT / 2; ++qp) {
+              const int jo = c * TC_KCH + jq * TC_JPT + 2 * qp;      // even
+              unsigned long long r2p = f2_pack(rv[cg * TC_JPT + 2 * qp], rv[cg * TC_JPT + 2 * qp + 1]);
               if (NH > 0) {
-                unsigned long long acc = 0ull;
 #pragma unroll
-                for (int h = 0; h < NH / 2; ++h) {
-                  unsigned long long o2;
-                  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(o2) : "r"(sOH + 4u * (jo * NH + 2 * h)));
-                  const unsigned long long dd = f2_sub(xhp[h], o2);
-                  acc = f2_fma(dd, dd, acc);
+                for (int h = 0; h < NH; h += 2) {
+                  unsigned long long o0, o1;
+                  tc::lds_u64x2(sOH + 4u * ((jo >> 1) * 2 * NH + 2 * h), o0, o1);
+                  const unsigned long long d0 = f2_sub(xb[h], o0), d1 = f2_sub(xb[h + 1], o1);
+                  r2p = f2_fma(d0, d0, r2p);
+                  r2p = f2_fma(d1, d1, r2p);
                 }
-                const float2 a2 = f2_unpack(acc);
-                r2s += a2.x + a2.y;
               }
-              const float r2 = fmaxf(r2s, 0.f);
-              float arg, poly, ex;
+              const float2 r2 = f2_unpack(r2p);
+              const float r2a = fmaxf(r2.x, 0.f), r2b = fmaxf(r2.y, 0.f);
+              unsigned long long argp, expp, polyp;
               if (KT == 0) {
-                const float r = tc::sqrt_approx_ftz(r2);
-                arg = c_arg * r;
-                poly = fmaf(arg, fmaf(arg, 0.33333333333333333f, 1.0f), 1.0f);
-                ex = tc::ex2_approx(fmaf(r, ex_c1, ex_c0));
+                const unsigned long long rp = f2_pack(tc::sqrt_approx_ftz(r2a), tc::sqrt_approx_ftz(r2b));
+                argp = f2_mul(rp, carg2);
+                const float2 ea = f2_unpack(f2_fma(rp, c1_2, c0_2));
+                expp = f2_pack(tc::ex2_approx(ea.x), tc::ex2_approx(ea.y));
+                polyp = f2_fma(argp, f2_fma(argp, third2, one2), one2);
               } else {
-                arg = c_arg * r2;
-                poly = 1.0f;
-                ex = tc::ex2_approx(fmaf(r2, ex_c1, ex_c0));
+                const unsigned long long rp2 = f2_pack(r2a, r2b);
+                argp = f2_mul(rp2, carg2);
+                const float2 ea = f2_unpack(f2_fma(rp2, c1_2, c0_2));
+                expp = f2_pack(tc::ex2_approx(ea.x), tc::ex2_approx(ea.y));
+                polyp = one2;
               }
-              const float kval = poly * ex;
-              const float cc = fmaf(kval, arg, kval);
-              float al, aa;
-              tc::lds_f32x2(sAl + 8 * jo, al, aa);
-              mu_p = fmaf(kval, al, mu_p);
-              sb_p = fmaf(cc, aa, sb_p);
-              kk_p = fmaf(cc, cc, kk_p);
-              kv[q] = kval;
+              const unsigned long long kvalp = f2_mul(polyp, expp);
+              const unsigned long long ccp = f2_fma(kvalp, argp, kvalp);
+              unsigned long long alp, aap;
+              tc::lds_u64x2(sAl + 16u * (jo >> 1), alp, aap);
+              mu2 = f2_fma(kvalp, alp, mu2);
+              sb2 = f2_fma(ccp, aap, sb2);
+              kk2 = f2_fma(ccp, ccp, kk2);
+              const float2 kk = f2_unpack(kvalp);
+              kv[2 * qp] = kk.x;
+              kv[2 * qp + 1] = kk.y;
             }
             // FP16 hi / lo split of the (2^ek-scaled) cross-covariances, packed two per column
             const uint32_t h01 = tc::pack_f16x2(kv[0], kv[1]), h23 = tc::pack_f16x2(kv[2], kv[3]);
@@ -490,7 +504,9 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
           }
         }
     };
-    auto flush_part = [&](int u, float mu_p, float sb_p, float kk_p) {
+    auto flush_part = [&](int u, unsigned long long mu2, unsigned long long sb2, unsigned long long kk2) {
+      const float2 m_ = f2_unpack(mu2), s_ = f2_unpack(sb2), k_ = f2_unpack(kk2);
+      const float mu_p = m_.x + m_.y, sb_p = s_.x + s_.y, kk_p = k_.x + k_.y;
       float* mp = m_part + (u % TC_TI) * 3 * TC_ROWS;
       atomicAdd(mp + cand, mu_p * T2.k_unscale);
       atomicAdd(mp + TC_ROWS + cand, sb_p * T2.k_unscale);
@@ -501,14 +517,16 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     // already produce the first NA chunks of tile t+1 into the A ring, so the MMA drain of tile t
     // overlaps useful work and the MMAs of t+1 start as soon as the accumulator is read out.
     const int head = nch < TC2_NA ? nch : TC2_NA;    // multiple of the R2 group size, or all of nch
-    float mu_c = 0.f, sb_c = 0.f, kk_c = 0.f, vsq_c = 0.f;   // tile t's running sums
+    unsigned long long mu_c = 0ull, sb_c = 0ull, kk_c = 0ull;  // tile t's running sums (packed pairs)
+    float vsq_c = 0.f;
     int pre = 0;                                              // chunks of tile t already produced
     for (int t = 0; n_cur > 0; ++t) {
       const int n_next = publish(t + 1);
       produce(t, pre, nch, mu_c, sb_c, kk_c, vsq_c);
       flush_part(t, mu_c, sb_c, kk_c);
       const float vsq_t = vsq_c;
-      mu_c = sb_c = kk_c = vsq_c = 0.f;
+      mu_c = sb_c = kk_c = 0ull;
+      vsq_c = 0.f;
       pre = 0;
       if (n_next > 0) {
         produce(t + 1, 0, head, mu_c, sb_c, kk_c, vsq_c);
