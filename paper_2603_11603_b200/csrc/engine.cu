@@ -696,7 +696,7 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
   {
     // one-hot layout of the R2 contraction (kernels_tc2.cuh): column of (f, v) = eoff[f] + v.
     // The widest features move to the SIMT side (at most 4) while the one-hot width exceeds
-    // TC2_KPMAX; their count is padded to 0 / 2 / 4 with a zero feature (hf = -1).
+    // gp.onehot_max_width (default TC2_KPMAX = 64); their count is padded to 0 / 2 / 4 with a zero feature (hf = -1).
     Tc2B& t2 = s->t2;
     const int d = s->H.d;
     std::vector<bool> simt(d, false);
@@ -704,7 +704,7 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
     for (int f = 0; f < d; ++f) K += s->H.feat[f].n;
     int nh = 0;
     for (int f = 0; f < 4; ++f) t2.hf[f] = -1;
-    while (K > TC2_KPMAX && nh < 4) {
+    while (K > s->H.onehot_max && nh < 4) {
       int best = -1;
       for (int f = 0; f < d; ++f)
         if (!simt[f] && (best < 0 || s->H.feat[f].n > s->H.feat[best].n)) best = f;

@@ -605,6 +605,11 @@ Status build_space(const char* json, HostSpace& S) {
     S.sn2 = model_const(gp, "sn2", 1e-3);
     S.xi = model_const(gp, "xi", 0.0);
     S.kappa = model_const(gp, "kappa", 2.0);
+    if (const asj::Value* w = gp->get("onehot_max_width")) {
+      if (w->kind != asj::Value::Number || !(w->num >= 0) || w->num != static_cast<int>(w->num))
+        return err(E_SCHEMA, "gp.onehot_max_width must be a non-negative integer");
+      S.onehot_max = static_cast<int>(w->num);
+    }
   }
   for (double l : S.ls)
     if (!(l > 0)) return err(E_SCHEMA, "gp.lengthscale must be positive");

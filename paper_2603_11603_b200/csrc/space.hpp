@@ -74,6 +74,7 @@ struct HostSpace {
   // GP hyper-parameters
   int kernel = 0;                 // 0 matern52, 1 rbf
   double sf2 = 0.1, sn2 = 1e-3, xi = 0.0, kappa = 2.0;
+  int onehot_max = 64;            // gp.onehot_max_width: one-hot r^2 width target of the TC kernel (impl. knob)
   std::vector<double> ls;
 };
 

@@ -269,3 +269,45 @@ def test_native_library_is_the_in_tree_build():
     with open("/proc/self/maps") as fh:
         maps = fh.read()
     assert A.LIB_PATH in maps
+
+
+# One-hot tensor-core kernel variants the presets do not reach: RBF kernel (KT = 1), four SIMT-side
+# features (NH = 4, via the gp.onehot_max_width implementation knob), per-feature lengthscales.
+VARIANTS = [
+    ("C2", {"kernel": "rbf"}, 64, "range", 0, None),
+    ("C2", {"onehot_max_width": 16}, 64, "range", 0, None),
+    ("C2", {"onehot_max_width": 0, "kernel": "rbf"}, 80, "range", 0, None),
+    ("C5", {"lengthscale": [0.3 + 0.1 * (j % 7) for j in range(16)]}, 128, "range", 2_000_000, 40000),
+    ("C4", {"onehot_max_width": 40, "sf2": 0.5, "sn2": 0.01}, 96, "sample", 0, 30000),
+]
+
+
+@pytest.mark.parametrize("base,gp,M,mode,begin,count", VARIANTS)
+def test_tc2_variants(base, gp, M, mode, begin, count):
+    with open(space_path(base)) as fh:
+        doc = json.load(fh)
+    doc["gp"].update(gp)
+    from oracle import space as S
+    o = S.load_space(json.dumps(doc))
+    raws, costs = observed(o, M, 3)
+    fit = run.observed_fit(o, raws, costs)
+    n = o.n_cvi() - begin if count is None else count
+    rec = oracle_records(o, fit, mode, begin, n, 5)
+    sp = A.Space(doc, 0)
+    sp.observe(raws, costs)
+    sp.set_path("tc2")
+    batch = (mode, begin, n, 5)
+    s0, rw, nv, top0 = gpu_run(sp, batch, "lcb", kappa=0.0)
+    s1, _, _, _ = gpu_run(sp, batch, "lcb", kappa=1.0)
+    v = rec["valid"]
+    assert np.array_equal(rw, rec["raw"]) and np.array_equal(np.isfinite(s0), v)
+    mu = rec["mu"][v]
+    assert np.all(np.abs(-s0[v].astype(np.float64) - mu) <= 1e-5 * np.maximum(1.0, np.abs(mu)))
+    sig = s1[v].astype(np.float64) - s0[v].astype(np.float64)
+    assert np.all(np.abs(sig ** 2 - rec["s2"][v]) <= 1e-5 * fit.sf2 + 4e-7)
+    check_topk(top0, oracle_topk(rec, oracle_scores(o, fit, rec, "lcb", kappa=0.0), 32))
+    sc, _, _, top = gpu_run(sp, batch, "ei")
+    ref = oracle_scores(o, fit, rec, "ei")
+    ok = ei_tolerance_ok(sc[v].astype(np.float64), ref[v], rec["mu"][v], rec["s2"][v], fit.fstar, fit.sf2)
+    assert ok.all(), f"{(~ok).sum()} EI values out of tolerance"
+    check_topk(top, oracle_topk(rec, ref, 32))

@@ -141,6 +141,9 @@ def test_observe_rejects_invalid(host_spaces, oracle_spaces):
     (lambda d: d["constraints"].append({"type": "product_eq_devices", "features": ["pp"]}) or
      d["constraints"].append({"type": "divides_const", "features": ["pp"], "const": "F_work"}) or
      d["model"].update(F_work=3), "AS_ERR_SPACE_EMPTY"),
+    (lambda d: d["gp"].update(onehot_max_width=-1), "AS_ERR_SPACE_SCHEMA"),
+    (lambda d: d["gp"].update(onehot_max_width=2.5), "AS_ERR_SPACE_SCHEMA"),
+    (lambda d: d["gp"].update(kernel="cubic"), "AS_ERR_SPACE_SCHEMA"),
 ])
 def test_space_errors(mutate, status):
     doc = json.loads(space_text("P0"))
