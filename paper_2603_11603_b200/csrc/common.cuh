@@ -65,6 +65,11 @@ struct SimParams {
   // derived / serving constants (model + hardware descriptor)
   double L, h, a, kv, S, GBS, P, P_exp, E, topk, peak, mfu0, bw_intra, bw_inter, gpn, n_sm;
   double dh, ffn, P_in, P_out, mml, w_tpot, bw_hbm, G;
+  // derived per-space constants of the cost terms (set by build_space; the resource check does not
+  // use them).  Cost terms multiply by per-digit reciprocals instead of dividing (R7:
+  // only the resource check is bit-exact; the cost agrees with the oracle to rounding).
+  double inv_B, inv_GBS, inv_bw_intra, inv_bw_inter, half_inv_nsm, T_work, C_tp, C_ep, C_cp;
+  double neutral_inv[NKNOB], neutral_lg2[NKNOB];
 };
 
 // ---- exact FP64 arithmetic for the resource check (A.2): no FMA contraction, fixed order.
@@ -82,21 +87,34 @@ AS_HD double xdiv(double a, double b) { return a / b; }
 
 struct Knobs {
   double v[NKNOB];
+  double vi[NKNOB];  // 1 / value        (knobs in knob_has_inv)
+  double lg[NKNOB];  // log2(value)      (knobs in knob_has_lg2)
   uint32_t act;  // bit k: knob k bound to an active feature
 };
+AS_HD constexpr bool knob_has_inv(int i) {
+  return i == K_PP || i == K_VPP || i == K_TP || i == K_DP || i == K_CP || i == K_EP || i == K_MBS;
+}
+AS_HD constexpr bool knob_has_lg2(int i) { return i == K_MBS || i == K_BUCKET; }
 
 // Effective knob values of a decoded canonical configuration: inactive features carry their
 // default digit (G1), so the digit's value is the effective value.
-AS_HD void load_knobs(const SimParams& P, const double* val, const DV& dv, uint32_t act_bits, Knobs& k) {
+// Tables: val / inv / lg2 [feature][digit] (inv and lg2 only read for the knobs that need them).
+AS_HD void load_knobs(const SimParams& P, const double* val, const double* inv, const double* lg2, const DV& dv,
+                      uint32_t act_bits, Knobs& k) {
   k.act = 0;
 #pragma unroll
   for (int i = 0; i < NKNOB; ++i) {
     int f = P.kf[i];
     if (f >= 0) {
-      k.v[i] = val[f * VMAX + dv_get(dv, f)];
+      const int o = f * VMAX + static_cast<int>(dv_get(dv, f));
+      k.v[i] = val[o];
+      if (knob_has_inv(i)) k.vi[i] = inv[o];
+      if (knob_has_lg2(i)) k.lg[i] = lg2[o];
       if ((act_bits >> f) & 1u) k.act |= (1u << i);
     } else {
       k.v[i] = P.neutral[i];
+      if (knob_has_inv(i)) k.vi[i] = P.neutral_inv[i];
+      if (knob_has_lg2(i)) k.lg[i] = P.neutral_lg2[i];
     }
   }
 }
@@ -114,6 +132,7 @@ AS_HD void device_assignment(const SimParams& P, double world, double& eff, doub
 }
 
 AS_HD double bw_of(const SimParams& P, double span) { return span <= P.gpn ? P.bw_intra : P.bw_inter; }
+AS_HD double inv_bw_of(const SimParams& P, double span) { return span <= P.gpn ? P.inv_bw_intra : P.inv_bw_inter; }
 AS_HD double clamp(double x, double lo, double hi) { return fmin(fmax(x, lo), hi); }
 
 // Simulator: cost in objective units (s/iter, or the scalarized serving cost), resource check.
@@ -126,16 +145,15 @@ AS_HD void simulate(const SimParams& P, const Knobs& k, double& cost, bool& ok, 
     const double world = pp * tp * dp * cp;
     double eff, cap;
     device_assignment(P, world, eff, cap);
-    const double micro = P.B / (dp * mbs);
     const double r = ar ? P.r_ar : 1.0;
-    const double t_comp = P.F_work * r / (world * eff * (1.0 + 0.1 * log2(mbs)));
-    const double t_bubble = t_comp * (pp - 1.0) / micro;
-    const double ov = tp > 1.0 ? clamp((k.v[K_TPCOMM] - 12.0) / 16.0, 0.0, 0.5) : 0.0;
-    const double t_tp = P.alpha_tp * (tp - 1.0) / tp * (1.0 - ov) * ((sp && tp > 1.0) ? 0.8 : 1.0);
-    const double lb = log2(k.v[K_BUCKET]) - 2.0;
+    const double t_comp = P.F_work * r / (world * eff * (1.0 + 0.1 * k.lg[K_MBS]));
+    const double t_bubble = t_comp * (pp - 1.0) * (dp * mbs) * P.inv_B;   // / micro, micro = B/(dp mbs)
+    const double ov = tp > 1.0 ? clamp((k.v[K_TPCOMM] - 12.0) * 0.0625, 0.0, 0.5) : 0.0;
+    const double t_tp = P.alpha_tp * (1.0 - k.vi[K_TP]) * (1.0 - ov) * ((sp && tp > 1.0) ? 0.8 : 1.0);
+    const double lb = k.lg[K_BUCKET] - 2.0;
     const double bp = dp > 1.0 ? 1.0 + 0.1 * lb * lb : 0.0;
-    const double t_dp = P.alpha_dp * (dp - 1.0) / dp * bp;
-    const double t_ep = P.alpha_tp * 0.5 * (ep - 1.0) / ep;
+    const double t_dp = P.alpha_dp * (1.0 - k.vi[K_DP]) * bp;
+    const double t_ep = P.alpha_tp * 0.5 * (1.0 - k.vi[K_EP]);
     cost = t_comp + t_bubble + t_tp + t_dp + t_ep;
     // S:496 in the normative order (R7): (P_mem/(pp*tp)) + (((A_mem*mbs)*f)/cp)
     const double m1 = xdiv(P.P_mem, xmul(pp, tp));
@@ -152,33 +170,28 @@ AS_HD void simulate(const SimParams& P, const Knobs& k, double& cost, bool& ok, 
     const double arc = k.v[K_AR];
     const bool full = arc == 2.0, sel = arc == 1.0, sp = k.v[K_SP] == 1.0;
     const double world = pp * tp * dp * cp;
-    const double m = P.GBS / (dp * mbs);
     const double L_st = xdiv(P.L, xmul(pp, vpp));
     const bool arl_active = (k.act >> K_ARL) & 1u;
     const double f_rc = full ? (arl_active ? fmin(1.0, xdiv(k.v[K_ARL], L_st)) : 1.0) : 0.0;
     const double r = 1.0 + 0.33 * f_rc + (sel ? 0.03 : 0.0);
-    const double P_act = P.P - P.P_exp + P.P_exp * P.topk / P.E;
-    const double T_work = P.GBS * P.S * (6.0 * P_act + 12.0 * P.L * P.h * P.S) / (P.peak * P.mfu0);
     const bool tpc_active = (k.act >> K_TPCOMM) & 1u;
-    const double steal = tpc_active ? 0.5 * k.v[K_TPCOMM] / P.n_sm : 0.0;
-    const double t_comp = T_work * r * (1.0 + steal) / (world * (1.0 + 0.1 * log2(mbs)));
-    const double t_bubble = t_comp * (pp - 1.0) / (m * vpp);
-    const double ov = (tp > 1.0 && tpc_active) ? clamp((k.v[K_TPCOMM] - 12.0) / 16.0, 0.0, 0.5) : 0.0;
-    const double t_tp = tp > 1.0 ? 16.0 * P.L * P.GBS * P.S * P.h / (pp * dp * cp * bw_of(P, tp)) *
-                                       (tp - 1.0) / tp * (1.0 - ov) * (sp ? 0.8 : 1.0)
+    const double steal = tpc_active ? k.v[K_TPCOMM] * P.half_inv_nsm : 0.0;
+    const double ipdc = k.vi[K_PP] * k.vi[K_DP] * k.vi[K_CP];         // 1 / (pp dp cp)
+    const double t_comp = P.T_work * r * (1.0 + steal) * (ipdc * k.vi[K_TP]) / (1.0 + 0.1 * k.lg[K_MBS]);
+    const double t_bubble = t_comp * (pp - 1.0) * (dp * mbs * P.inv_GBS) * k.vi[K_VPP];   // / (m vpp)
+    const double ov = (tp > 1.0 && tpc_active) ? clamp((k.v[K_TPCOMM] - 12.0) * 0.0625, 0.0, 0.5) : 0.0;
+    const double t_tp = tp > 1.0 ? P.C_tp * ipdc * inv_bw_of(P, tp) * (1.0 - k.vi[K_TP]) * (1.0 - ov) * (sp ? 0.8 : 1.0)
                                  : 0.0;
     const double P_loc = xdiv(xadd(P.P - P.P_exp, xdiv(P.P_exp, ep)), xmul(pp, tp));
-    const double lb = log2(k.v[K_BUCKET]) - 2.0;
+    const double lb = k.lg[K_BUCKET] - 2.0;
     const bool ovg = k.v[K_OVG] == 1.0, ovp = k.v[K_OVP] == 1.0;
-    const double t_dp = dp > 1.0 ? 4.0 * P_loc / bw_of(P, tp * cp * dp) * (dp - 1.0) / dp *
+    const double t_dp = dp > 1.0 ? 4.0 * P_loc * inv_bw_of(P, tp * cp * dp) * (1.0 - k.vi[K_DP]) *
                                        (1.0 + 0.1 * lb * lb) * (ovg ? 0.5 : 1.0) * (ovp ? 0.75 : 1.0)
                                  : 0.0;
-    const double t_ep = ep > 1.0 ? 8.0 * P.topk * P.L * P.GBS * P.S * P.h /
-                                       (pp * dp * cp * (sp ? tp : 1.0) * bw_of(P, tp * cp * ep)) *
-                                       (ep - 1.0) / ep * (k.v[K_DISP] == 1.0 ? 1.5 : 1.0)
+    const double t_ep = ep > 1.0 ? P.C_ep * ipdc * (sp ? k.vi[K_TP] : 1.0) * inv_bw_of(P, tp * cp * ep) *
+                                       (1.0 - k.vi[K_EP]) * (k.v[K_DISP] == 1.0 ? 1.5 : 1.0)
                                  : 0.0;
-    const double t_cp = cp > 1.0 ? 0.5 * 12.0 * P.L * P.GBS * P.S * P.kv * (P.h / P.a) /
-                                       (pp * dp * bw_of(P, tp * cp)) * (cp - 1.0) / cp
+    const double t_cp = cp > 1.0 ? P.C_cp * k.vi[K_PP] * k.vi[K_DP] * inv_bw_of(P, tp * cp) * (1.0 - k.vi[K_CP])
                                  : 0.0;
     cost = t_comp + t_bubble + t_tp + t_dp + t_ep + t_cp;
     // memory, normative FP64 order (R7)

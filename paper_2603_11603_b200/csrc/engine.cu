@@ -755,15 +755,24 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
       D.comp_width[j] = j < D.n_comp ? H.comp_width[j] : 0;
     }
     D.sim = H.sim;
-    std::vector<uint2> oc(H.s_off.size());
-    for (size_t i = 0; i < oc.size(); ++i) oc[i] = make_uint2(H.s_off[i], H.s_cnt[i]);
+    // (offset, count, magic, shifts): t / count as (hi + ((t - hi) >> sh1)) >> sh2 with
+    // hi = umulhi(magic, t) (Granlund-Montgomery round-up method; exact for every 32-bit t)
+    std::vector<uint4> oc(H.s_off.size());
+    for (size_t i = 0; i < oc.size(); ++i) {
+      const uint32_t c = H.s_cnt[i] > 0 ? H.s_cnt[i] : 1;
+      int l = 0;
+      while ((1ull << l) < c) ++l;
+      const uint32_t magic = static_cast<uint32_t>((((1ull << 32) * ((1ull << l) - c)) / c) + 1);
+      const uint32_t sh1 = l > 0 ? 1u : 0u, sh2 = l > 0 ? static_cast<uint32_t>(l - 1) : 0u;
+      oc[i] = make_uint4(H.s_off[i], H.s_cnt[i], magic, sh1 | (sh2 << 8));
+    }
     as_status r;
     uint64_t *p_prefix, *p_sraw;
     uint32_t* p_sact;
     DV* p_sdv;
-    uint2* p_oc;
+    uint4* p_oc;
     Tuple* p_tu;
-    double *p_val, *p_xt64;
+    double *p_val, *p_inv, *p_lg2, *p_xt64;
     float* p_xt32;
     if ((r = upload(&p_prefix, H.prefix, s->owned)) != AS_OK) return cleanup(r);
     if ((r = upload(&p_sraw, H.s_raw, s->owned)) != AS_OK) return cleanup(r);
@@ -772,6 +781,8 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
     if ((r = upload(&p_oc, oc, s->owned)) != AS_OK) return cleanup(r);
     if ((r = upload(&p_tu, H.tuples, s->owned)) != AS_OK) return cleanup(r);
     if ((r = upload(&p_val, H.val, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = upload(&p_inv, H.inv, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = upload(&p_lg2, H.lg2, s->owned)) != AS_OK) return cleanup(r);
     if ((r = upload(&p_xt64, H.xt64, s->owned)) != AS_OK) return cleanup(r);
     if ((r = upload(&p_xt32, H.xt32, s->owned)) != AS_OK) return cleanup(r);
     D.prefix = p_prefix;
@@ -781,6 +792,8 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
     D.s_oc = p_oc;
     D.tuples = p_tu;
     D.val = p_val;
+    D.inv = p_inv;
+    D.lg2 = p_lg2;
     D.xt64 = p_xt64;
     D.xt32 = p_xt32;
     // GP buffers at capacity

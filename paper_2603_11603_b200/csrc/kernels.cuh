@@ -26,9 +26,11 @@ struct DevSpace {
   const uint64_t* s_raw;   // [n_struct]
   const uint32_t* s_act;   // [n_struct]
   const DV* s_dv;          // [n_struct]
-  const uint2* s_oc;       // [n_struct*n_comp] (offset, count)
+  const uint4* s_oc;       // [n_struct*n_comp] (offset, count, magic, sh1 | sh2 << 8): t / count by multiply
   const Tuple* tuples;
   const double* val;       // [d*VMAX]
+  const double* inv;       // [d*VMAX] 1/val   (simulator cost terms)
+  const double* lg2;       // [d*VMAX] log2(val)
   const float* xt32;       // [d*VMAX]
   const double* xt64;      // [d*VMAX]
   uint64_t stride[DMAX];
@@ -96,8 +98,9 @@ __device__ __forceinline__ void decode_dev(const DevSpace& S, uint64_t p, DV& dv
   act = __ldg(S.s_act + lo);
   raw = __ldg(S.s_raw + lo);
   for (int c = S.n_comp - 1; c >= 0; --c) {
-    const uint2 oc = __ldg(S.s_oc + static_cast<size_t>(lo) * S.n_comp + c);
-    const uint32_t q = t / oc.y;
+    const uint4 oc = __ldg(S.s_oc + static_cast<size_t>(lo) * S.n_comp + c);
+    const uint32_t hi = __umulhi(oc.z, t);
+    const uint32_t q = (hi + ((t - hi) >> (oc.w & 0xFFu))) >> (oc.w >> 8);
     const uint32_t r = t - q * oc.y;
     t = q;
     const Tuple* tu = S.tuples + oc.x + r;
@@ -135,8 +138,9 @@ __device__ __forceinline__ void decode_dev_ci(const DevSpace& S, const uint64_t*
   act = __ldg(S.s_act + lo);
   raw = __ldg(S.s_raw + lo);
   for (int c = S.n_comp - 1; c >= 0; --c) {
-    const uint2 oc = __ldg(S.s_oc + static_cast<size_t>(lo) * S.n_comp + c);
-    const uint32_t q = t / oc.y;
+    const uint4 oc = __ldg(S.s_oc + static_cast<size_t>(lo) * S.n_comp + c);
+    const uint32_t hi = __umulhi(oc.z, t);
+    const uint32_t q = (hi + ((t - hi) >> (oc.w & 0xFFu))) >> (oc.w >> 8);
     const uint32_t r = t - q * oc.y;
     t = q;
     const Tuple* tu = S.tuples + oc.x + r;
@@ -215,17 +219,7 @@ __device__ __forceinline__ float r2_packed(const unsigned long long* xp, const f
 
 __device__ __forceinline__ void sim_dev(const DevSpace& S, const DV& dv, uint32_t act, double& cost, bool& ok) {
   Knobs k;
-  k.act = 0;
-#pragma unroll
-  for (int i = 0; i < NKNOB; ++i) {
-    const int f = S.sim.kf[i];
-    if (f >= 0) {
-      k.v[i] = __ldg(S.val + f * VMAX + dv_get(dv, f));
-      if ((act >> f) & 1u) k.act |= (1u << i);
-    } else {
-      k.v[i] = S.sim.neutral[i];
-    }
-  }
+  load_knobs(S.sim, S.val, S.inv, S.lg2, dv, act, k);
   double mem;
   simulate(S.sim, k, cost, ok, mem);
 }
@@ -783,7 +777,7 @@ __global__ void mask_kernel(DevSpace S, uint64_t raw_begin, uint64_t count, uint
           uint64_t contrib = 0;
           for (int q = S.comp_first[c]; q < S.comp_first[c] + S.comp_width[c]; ++q)
             contrib += ((raw / S.stride[q]) % static_cast<uint64_t>(S.nval[q])) * S.stride[q];
-          const uint2 oc = S.s_oc[static_cast<size_t>(lo) * S.n_comp + c];
+          const uint4 oc = S.s_oc[static_cast<size_t>(lo) * S.n_comp + c];
           int a = 0, b = static_cast<int>(oc.y);  // tuples sorted by raw contribution
           while (b - a > 1) {
             const int mid = (a + b) >> 1;

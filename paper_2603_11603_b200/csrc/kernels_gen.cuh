@@ -27,7 +27,7 @@ struct CandList {
   unsigned long long* count;    // number of records
 };
 
-__global__ void __launch_bounds__(GEN_THREADS)
+__global__ void __launch_bounds__(GEN_THREADS, 3)
 gen_kernel(DevSpace S, BatchArgs A, uint64_t j0, uint64_t nj, CandList L, int ci_n, unsigned long long* valid_total) {
   extern __shared__ __align__(16) uint64_t gen_cidx[];
   __shared__ unsigned long long blk_valid;

@@ -567,6 +567,13 @@ Status build_space(const char* json, HostSpace& S) {
       S.val[j * VMAX + v] = x;
     }
   }
+  S.inv.assign(S.val.size(), 0.0);
+  S.lg2.assign(S.val.size(), 0.0);
+  for (size_t i = 0; i < S.val.size(); ++i) {
+    const double x = S.val[i];
+    S.inv[i] = x != 0.0 ? 1.0 / x : 0.0;
+    S.lg2[i] = x > 0.0 ? std::log2(x) : 0.0;
+  }
   P.n_cls = static_cast<int>(cls.size());
   for (int i = 0; i < P.n_cls; ++i) {
     P.cls_count[i] = cls[i].count;
@@ -585,6 +592,22 @@ Status build_space(const char* json, HostSpace& S) {
   P.bw_inter = hc("bw_inter", 25e9); P.gpn = hc("gpus_per_node", 8); P.n_sm = hc("n_sm", 108);
   P.bw_hbm = hc("bw_hbm", 2.039e12);
   P.G = S.G;
+  P.inv_B = 1.0 / P.B;
+  P.inv_GBS = 1.0 / P.GBS;
+  P.inv_bw_intra = 1.0 / P.bw_intra;
+  P.inv_bw_inter = 1.0 / P.bw_inter;
+  P.half_inv_nsm = 0.5 / P.n_sm;
+  {
+    const double P_act = P.P - P.P_exp + P.P_exp * P.topk / P.E;
+    P.T_work = P.GBS * P.S * (6.0 * P_act + 12.0 * P.L * P.h * P.S) / (P.peak * P.mfu0);
+  }
+  P.C_tp = 16.0 * P.L * P.GBS * P.S * P.h;
+  P.C_ep = 8.0 * P.topk * P.L * P.GBS * P.S * P.h;
+  P.C_cp = 0.5 * 12.0 * P.L * P.GBS * P.S * P.kv * (P.h / P.a);
+  for (int k = 0; k < NKNOB; ++k) {
+    P.neutral_inv[k] = P.neutral[k] != 0.0 ? 1.0 / P.neutral[k] : 0.0;
+    P.neutral_lg2[k] = P.neutral[k] > 0.0 ? std::log2(P.neutral[k]) : 0.0;
+  }
 
   // ---------------------------------------------------------------- GP hyper-parameters + features
   const asj::Value* gp = doc.get("gp");
@@ -665,7 +688,7 @@ bool raw_decode(const HostSpace& S, uint64_t raw, int* dig, DV& dv, uint32_t& ac
 
 void simulate_host(const HostSpace& S, const DV& dv, uint32_t act, double& cost, bool& ok, double& mem) {
   Knobs k;
-  load_knobs(S.sim, S.val.data(), dv, act, k);
+  load_knobs(S.sim, S.val.data(), S.inv.data(), S.lg2.data(), dv, act, k);
   simulate(S.sim, k, cost, ok, mem);
 }
 

@@ -68,6 +68,7 @@ struct HostSpace {
   uint64_t tail_span = 1;         // stride of the last prefix feature (raw size of one structure's tail)
   // value tables (VMAX per feature)
   std::vector<double> val;        // simulator values
+  std::vector<double> inv, lg2;   // 1/value, log2(value) (cost terms; 0 where value == 0)
   std::vector<double> xt64;       // GP features x~ = phi / l
   std::vector<float> xt32;
   SimParams sim{};
