@@ -55,6 +55,10 @@ enum Knob {
 struct SimParams {
   int mode;                  // 0 spec, 1 derived (A.3), 2 serve (A.4)
   int kf[NKNOB];             // feature index bound to each knob, -1 if the preset lacks it
+  // digit extraction of a bound knob without per-call index arithmetic: digit vector word kw,
+  // bit shift ks, table offset ko = kf * VMAX, activity bit kbit = 1 << kf
+  int kw[NKNOB], ks[NKNOB], ko[NKNOB];
+  uint32_t kbit[NKNOB];
   double neutral[NKNOB];     // value of an absent knob (A.3 "Knobs absent from a preset")
   int n_cls;                 // device classes, sorted by relative throughput (fastest first)
   int cls_count[MAX_CLS];
@@ -104,13 +108,14 @@ AS_HD void load_knobs(const SimParams& P, const double* val, const double* inv, 
   k.act = 0;
 #pragma unroll
   for (int i = 0; i < NKNOB; ++i) {
-    int f = P.kf[i];
-    if (f >= 0) {
-      const int o = f * VMAX + static_cast<int>(dv_get(dv, f));
+    if (P.kf[i] >= 0) {
+      const int kw = P.kw[i];
+      const uint64_t w = kw == 0 ? dv.w[0] : (kw == 1 ? dv.w[1] : dv.w[2]);
+      const int o = P.ko[i] + static_cast<int>((w >> P.ks[i]) & 0xFFu);
       k.v[i] = val[o];
       if (knob_has_inv(i)) k.vi[i] = inv[o];
       if (knob_has_lg2(i)) k.lg[i] = lg2[o];
-      if ((act_bits >> f) & 1u) k.act |= (1u << i);
+      if (act_bits & P.kbit[i]) k.act |= (1u << i);
     } else {
       k.v[i] = P.neutral[i];
       if (knob_has_inv(i)) k.vi[i] = P.neutral_inv[i];

@@ -480,9 +480,14 @@ as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, b
     r = ensure_cand_list(s, static_cast<size_t>(std::min<uint64_t>(count, GEN_SLICE)));
     if (r != AS_OK) return r;
   }
-  const int ci_n = std::min(s->H.n_struct, GEN_CI_MAX);
+  // whole prefix table + bucket index in SMEM when they fit, else a coarse index of GEN_CI_MAX entries
+  const bool by_bucket = s->H.n_struct + 1 <= GEN_CI_MAX;
+  const int ci_n = by_bucket ? -1 : std::min(s->H.n_struct, GEN_CI_MAX);
+  const size_t gen_smem = by_bucket ? (static_cast<size_t>(s->H.n_struct) + 1) * 8 + (s->D.n_bucket + 1) * 4
+                                    : static_cast<size_t>(ci_n) * 8;
+  CUDA_TRY(cudaFuncSetAttribute(gen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gen_smem)));
   int occ = 1;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gen_kernel, GEN_THREADS, ci_n * 8));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gen_kernel, GEN_THREADS, gen_smem));
   const int grid_gen = s->n_sm * std::max(occ, 1);
   auto k2 = tc2_kernel_for(s->G.kernel, s->t2.nh);
   CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -497,7 +502,7 @@ as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, b
     if (nj > 0) {
       CUDA_TRY(cudaMemsetAsync(s->list.count, 0, sizeof(unsigned long long), st));
       if (ev) CUDA_TRY(cudaEventRecord(s->sev[s->sev_used], st));
-      gen_kernel<<<grid_gen, GEN_THREADS, ci_n * 8, st>>>(s->D, A, j0, nj, s->list, ci_n,
+      gen_kernel<<<grid_gen, GEN_THREADS, gen_smem, st>>>(s->D, A, j0, nj, s->list, ci_n,
                                                            reinterpret_cast<unsigned long long*>(s->d_valid));
       CUDA_TRY(cudaGetLastError());
       ++s->n_launches;
@@ -775,6 +780,25 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
     double *p_val, *p_inv, *p_lg2, *p_xt64;
     float* p_xt32;
     if ((r = upload(&p_prefix, H.prefix, s->owned)) != AS_OK) return cleanup(r);
+    {
+      // bucket index: bucket[b] = structure holding position b << bshift (positions beyond n_cvi
+      // map to the last structure); at most 4096 buckets
+      int bshift = 0;
+      while (((H.n_cvi + (1ull << bshift) - 1) >> bshift) > 4096) ++bshift;
+      const int nb = static_cast<int>((H.n_cvi + (1ull << bshift) - 1) >> bshift);
+      std::vector<uint32_t> bk(static_cast<size_t>(nb) + 1);
+      int st = 0;
+      for (int b = 0; b <= nb; ++b) {
+        const uint64_t pos = std::min<uint64_t>(static_cast<uint64_t>(b) << bshift, H.n_cvi - 1);
+        while (st + 1 < H.n_struct && H.prefix[st + 1] <= pos) ++st;
+        bk[b] = static_cast<uint32_t>(st);
+      }
+      uint32_t* p_bk;
+      if ((r = upload(&p_bk, bk, s->owned)) != AS_OK) return cleanup(r);
+      D.bucket = p_bk;
+      D.n_bucket = nb;
+      D.bshift = bshift;
+    }
     if ((r = upload(&p_sraw, H.s_raw, s->owned)) != AS_OK) return cleanup(r);
     if ((r = upload(&p_sact, H.s_act, s->owned)) != AS_OK) return cleanup(r);
     if ((r = upload(&p_sdv, H.s_dv, s->owned)) != AS_OK) return cleanup(r);

@@ -23,6 +23,8 @@ struct DevSpace {
   int d, n_prefix, n_comp, n_struct;
   uint64_t n_cvi, n_raw, tail_span;
   const uint64_t* prefix;  // [n_struct+1]
+  const uint32_t* bucket;  // [n_bucket+1]: structure of position b << bshift (SMEM-resident decode, gen kernel)
+  int n_bucket, bshift;
   const uint64_t* s_raw;   // [n_struct]
   const uint32_t* s_act;   // [n_struct]
   const DV* s_dv;          // [n_struct]
@@ -112,25 +114,9 @@ __device__ __forceinline__ void decode_dev(const DevSpace& S, uint64_t p, DV& dv
   }
 }
 
-// Decode with a coarse SMEM index of the structure prefix array: cidx[k] = prefix[k * n_struct / ci_n]
-// (k < ci_n) brackets the structure before a short binary search in global memory; with
-// ci_n == n_struct the whole search runs in shared memory.
-constexpr int CI = 256;
-__device__ __forceinline__ void decode_dev_ci(const DevSpace& S, const uint64_t* cidx, int ci_n, uint64_t p, DV& dv,
-                                              uint32_t& act, uint64_t& raw) {
-  int a = 0, b = ci_n;                       // largest k with cidx[k] <= p
-  while (b - a > 1) {
-    const int mid = (a + b) >> 1;
-    if (cidx[mid] <= p) a = mid; else b = mid;
-  }
-  int lo = static_cast<int>((static_cast<long long>(a) * S.n_struct) / ci_n);
-  int hi = (b >= ci_n) ? S.n_struct : static_cast<int>((static_cast<long long>(b) * S.n_struct) / ci_n);
-  if (hi <= lo) hi = lo + 1;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (__ldg(S.prefix + mid) <= p) lo = mid; else hi = mid;
-  }
-  uint32_t t = static_cast<uint32_t>(p - __ldg(S.prefix + lo));
+// Tail of the CVI decode: structure record, then one mixed-radix digit (multiply-shift division)
+// and one tuple per gating group, OR-ed into the digit vector.
+__device__ __forceinline__ void decode_tail(const DevSpace& S, int lo, uint32_t t, DV& dv, uint32_t& act, uint64_t& raw) {
   const DV* sd = S.s_dv + lo;
   dv.w[0] = __ldg(&sd->w[0]);
   dv.w[1] = __ldg(&sd->w[1]);
@@ -150,6 +136,40 @@ __device__ __forceinline__ void decode_dev_ci(const DevSpace& S, const uint64_t*
     act |= __ldg(&tu->act);
     raw += __ldg(&tu->raw);
   }
+}
+
+// Decode with a coarse SMEM index of the structure prefix array: cidx[k] = prefix[k * n_struct / ci_n]
+// (k < ci_n) brackets the structure before a short binary search in global memory; with
+// ci_n == n_struct the whole search runs in shared memory.
+constexpr int CI = 256;
+__device__ __forceinline__ void decode_dev_ci(const DevSpace& S, const uint64_t* cidx, int ci_n, uint64_t p, DV& dv,
+                                              uint32_t& act, uint64_t& raw) {
+  int a = 0, b = ci_n;                       // largest k with cidx[k] <= p
+  while (b - a > 1) {
+    const int mid = (a + b) >> 1;
+    if (cidx[mid] <= p) a = mid; else b = mid;
+  }
+  int lo = static_cast<int>((static_cast<long long>(a) * S.n_struct) / ci_n);
+  int hi = (b >= ci_n) ? S.n_struct : static_cast<int>((static_cast<long long>(b) * S.n_struct) / ci_n);
+  if (hi <= lo) hi = lo + 1;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(S.prefix + mid) <= p) lo = mid; else hi = mid;
+  }
+  decode_tail(S, lo, static_cast<uint32_t>(p - __ldg(S.prefix + lo)), dv, act, raw);
+}
+// Structure lookup from SMEM copies of the whole prefix table and of the bucket index: the
+// position's bucket brackets its structure, then a short binary search (typically 0-2 probes).
+__device__ __forceinline__ void decode_dev_bucket(const DevSpace& S, const uint64_t* pre, const uint32_t* bkt,
+                                                  uint64_t p, DV& dv, uint32_t& act, uint64_t& raw) {
+  const int b = static_cast<int>(p >> S.bshift);
+  int lo = static_cast<int>(bkt[b]), hi = static_cast<int>(bkt[b + 1]) + 1;
+  if (hi > S.n_struct) hi = S.n_struct;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (pre[mid] <= p) lo = mid; else hi = mid;
+  }
+  decode_tail(S, lo, static_cast<uint32_t>(p - pre[lo]), dv, act, raw);
 }
 __device__ __forceinline__ void decode_dev_idx(const DevSpace& S, const uint64_t* cidx, uint64_t p, DV& dv,
                                                uint32_t& act, uint64_t& raw) {

@@ -32,8 +32,17 @@ gen_kernel(DevSpace S, BatchArgs A, uint64_t j0, uint64_t nj, CandList L, int ci
   extern __shared__ __align__(16) uint64_t gen_cidx[];
   __shared__ unsigned long long blk_valid;
   const int tid = threadIdx.x, lane = tid & 31;
+  // ci_n < 0: SMEM copies of the whole prefix table (n_struct + 1) and the bucket index (decode by
+  // bucket); else a coarse index of ci_n entries
+  const bool by_bucket = ci_n < 0;
+  uint32_t* gen_bkt = reinterpret_cast<uint32_t*>(gen_cidx + (S.n_struct + 1));
   if (tid == 0) blk_valid = 0;
-  load_cidx_n(S, gen_cidx, ci_n, tid, GEN_THREADS);
+  if (by_bucket) {
+    for (int i = tid; i <= S.n_struct; i += GEN_THREADS) gen_cidx[i] = __ldg(S.prefix + i);
+    for (int i = tid; i <= S.n_bucket; i += GEN_THREADS) gen_bkt[i] = __ldg(S.bucket + i);
+  } else {
+    load_cidx_n(S, gen_cidx, ci_n, tid, GEN_THREADS);
+  }
   __syncthreads();
   unsigned long long my_valid = 0;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * GEN_THREADS;
@@ -48,7 +57,8 @@ gen_kernel(DevSpace S, BatchArgs A, uint64_t j0, uint64_t nj, CandList L, int ci
     const uint64_t j = j0 + jj;
     if (in) {
       pcvi = (A.mode == 0) ? A.begin + j : feistel_pi(A.fk, A.begin + j);
-      decode_dev_ci(S, gen_cidx, ci_n, pcvi, dv, act, raw);
+      if (by_bucket) decode_dev_bucket(S, gen_cidx, gen_bkt, pcvi, dv, act, raw);
+      else decode_dev_ci(S, gen_cidx, ci_n, pcvi, dv, act, raw);
       sim_dev(S, dv, act, cost, ok);
       if (A.d_raw) A.d_raw[j] = raw;
       if (!ok && A.d_scores) A.d_scores[j] = -INFINITY;

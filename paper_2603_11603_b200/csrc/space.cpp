@@ -545,6 +545,11 @@ Status build_space(const char* json, HostSpace& S) {
     else if (k == K_MBT) nm = "mbt";
     else if (k == K_U) nm = "u";
     if (nm) P.kf[k] = feature_index(S, nm);
+    const int f = P.kf[k] >= 0 ? P.kf[k] : 0;
+    P.kw[k] = f >> 3;
+    P.ks[k] = (f & 7) * 8;
+    P.ko[k] = f * VMAX;
+    P.kbit[k] = P.kf[k] >= 0 ? (1u << f) : 0u;
   }
   S.val.assign(static_cast<size_t>(S.d) * VMAX, 0.0);
   for (int j = 0; j < S.d; ++j) {
