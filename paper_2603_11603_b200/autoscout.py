@@ -18,7 +18,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libautoscout.so")
+LIB_PATH = os.environ.get("AUTOSCOUT_LIB") or os.path.join(HERE, "libautoscout.so")   # env: dev A/B builds only
 
 AS_MODE_RANGE, AS_MODE_SAMPLE = 0, 1
 AS_ACQ_EI, AS_ACQ_LCB, AS_ACQ_SIM = 0, 1, 2

@@ -507,7 +507,7 @@ as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, b
       CUDA_TRY(cudaGetLastError());
       ++s->n_launches;
       if (ev) CUDA_TRY(cudaEventRecord(s->sev[s->sev_used + 1], st));
-      k2<<<grid, TC_WARPS * 32 + 32, smem, st>>>(s->D, s->G, A, out, tb, s->t2, s->list);
+      k2<<<grid, TC_WARPS * 32 + 64, smem, st>>>(s->D, s->G, A, out, tb, s->t2, s->list);
       CUDA_TRY(cudaGetLastError());
       ++s->n_launches;
       if (ev) {

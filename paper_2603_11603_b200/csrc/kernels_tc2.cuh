@@ -16,8 +16,9 @@
 //   warps 0-15  producers: phase 0 (decode + mask + simulator -> queue), publish tile t+1 (meta +
 //               E rows) BEFORE the chunk loop of tile t, so the R2 MMAs of t+1 overlap tile t;
 //               chunk loop: R2 chunk from TMEM -> k -> TF32 hi/lo -> A ring (TMEM); epilogue.
-//   warp 16     MMA issuer + loader (warp-converged, one elected lane issues): R2 chunks RR ahead
-//               of the L^-1 chunks in one instruction stream; bulk copies of the L^-1 and T chunks.
+//   warp 16     MMA issuer (warp-converged, one elected lane issues): R2 groups ahead of the
+//               L^-1 chunks in one instruction stream.
+//   warp 17     loader: bulk copies of the L^-1 chunks, T groups and staged list records.
 // TMEM: D [Mp16] | A ring [4 x 32] | R2 ring [2 groups x 64]  (Mp16 <= 256 -> <= 512 columns).
 #pragma once
 #include "kernels_gen.cuh"
@@ -108,11 +109,11 @@ __device__ __forceinline__ void tc2_admit(uint64_t key, uint64_t* arr, TopkSmem&
 }
 
 template <int PW, int KT, int NH>
-__global__ void __launch_bounds__(PW * 32 + 32, 1)
+__global__ void __launch_bounds__(PW * 32 + 64, 1)
 score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, CandList L) {
   constexpr int TC_PROD_WARPS = PW;
   constexpr int TC_PROD_THREADS = PW * 32;
-  constexpr int TC_THREADS = TC_PROD_THREADS + 32;
+  constexpr int TC_THREADS = TC_PROD_THREADS + 64;   // + MMA warp + loader warp
   constexpr int TC_JQ = TC_PROD_THREADS / TC_ROWS;   // producer threads per candidate
   constexpr int TC_JPT = TC_KCH / TC_JQ;             // observed points per thread per chunk
   static_assert(TC_JQ == 4 && TC_JPT == 4, "R2 group columns are laid out for 16 producer warps");
@@ -546,13 +547,13 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       out.counts[blockIdx.x] = n;
       out.drop[blockIdx.x] = ts.drop;
     }
-  } else {
-    // =========================================================== MMA issuer + loader
+  } else if (warp == TC_PROD_WARPS) {
+    // =========================================================== MMA issuer
     // The whole warp runs this loop in lock-step (warp-uniform state); one elected lane issues the
-    // MMAs / commits (elect.sync inside the asm) and lane 0 the bulk copies.
-    uint32_t g = 0, gl = 0;          // L^-1 chunks consumed / loaded
-    uint32_t x = 0, xl = 0;          // R2 chunks issued / T chunks loaded
-    int lc = 0, xc = 0;              // chunk index of the next L^-1 / T load
+    // MMAs / commits (elect.sync inside the asm).  All bulk copies are the loader warp's, so this
+    // warp never waits on a ring refill.
+    uint32_t g = 0;                  // L^-1 chunks consumed
+    uint32_t x = 0;                  // R2 groups issued
     int ru = 0, rgi = 0;             // tile / group index of the next R2 group
     int known = 0, end_tile = 0x7fffffff;
     auto tile_exists = [&](int u) -> bool {
@@ -562,47 +563,6 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         ++known;
       }
       return u < end_tile;
-    };
-    auto load_L = [&]() {
-      const int s = gl % TC2_NB;
-      tc::mbar_wait(b_empty + s, ((gl / TC2_NB) & 1u) ^ 1u);
-      if (lane == 0) {
-        const uint32_t bytes = 2u * (Mp16 - lc * TC_KCH) * TC_KCH * 2;
-        tc::mbar_arrive_expect_tx(b_full + s, bytes);
-        tc::bulk_g2s(B0 + static_cast<size_t>(s) * b_stage_bytes, T2.wch + T2.woff[lc], bytes, b_full + s);
-      }
-      ++gl;
-      if (++lc == nch) lc = 0;
-    };
-    // stage the list records of this CTA's tile u (rounded up to 16 B; the list is padded)
-    auto load_S = [&](int u) {
-      if (u >= my_tiles) return;
-      tc::mbar_wait(s_empty + (u & 1), ((u >> 1) & 1u) ^ 1u);
-      if (lane == 0) {
-        const uint64_t r0 = (blockIdx.x + static_cast<uint64_t>(u) * gridDim.x) * TC_ROWS;
-        const uint32_t n = static_cast<uint32_t>(n_list - r0 < TC_ROWS ? n_list - r0 : TC_ROWS);
-        const uint32_t b4 = (n * 4 + 15) & ~15u, b8 = (n * 8 + 15) & ~15u;   // bulk sizes: multiples of 16 B
-        unsigned char* sg = stg + (u & 1) * TC2_STG_BYTES;
-        tc::mbar_arrive_expect_tx(s_full + (u & 1), 2 * b4 + 4 * b8);
-        tc::bulk_g2s(sg + TC2_STG_CVI, L.cvi + r0, b4, s_full + (u & 1));
-        tc::bulk_g2s(sg + TC2_STG_J, L.j + r0, b4, s_full + (u & 1));
-        tc::bulk_g2s(sg + TC2_STG_M0, L.m0 + r0, b8, s_full + (u & 1));
-        tc::bulk_g2s(sg + TC2_STG_DV0, L.dv0 + r0, b8, s_full + (u & 1));
-        tc::bulk_g2s(sg + TC2_STG_DV1, L.dv1 + r0, b8, s_full + (u & 1));
-        tc::bulk_g2s(sg + TC2_STG_DV2, L.dv2 + r0, b8, s_full + (u & 1));
-      }
-      __syncwarp();
-    };
-    auto load_T = [&]() {
-      const int s = xl % TC2_NT;
-      tc::mbar_wait(x_empty + s, ((xl / TC2_NT) & 1u) ^ 1u);
-      if (lane == 0) {
-        tc::mbar_arrive_expect_tx(x_full + s, t_stage_bytes);
-        tc::bulk_g2s(T0 + static_cast<size_t>(s) * t_stage_bytes,
-                     T2.tch + static_cast<size_t>(xc) * (t_stage_bytes / 2), t_stage_bytes, x_full + s);
-      }
-      ++xl;
-      if (++xc == ng) xc = 0;
     };
     __syncwarp();
     const uint32_t sbo16 = (Kp / 8) * 128;
@@ -631,19 +591,9 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         rgi = 0;
         ++ru;
       }
-      load_T();                                        // refill the slot of group x-2, NT-1 ahead
       return true;
     };
-    load_S(0);
-    load_S(1);
-    if (tile_exists(0)) {
-      for (int i = 0; i < TC2_PF; ++i) load_L();
-      for (int i = 0; i < TC2_NT - 1; ++i) load_T();
-    }
-    const uint32_t sbo = (TC_KCH / 4) * 128;
-    (void)sbo;
     for (int t = 0; tile_exists(t); ++t) {
-      load_S(t + 2);                                   // slot t % 2 was consumed by publish(t)
       tc::mbar_wait(d_empty, (t & 1) ^ 1);
       tc::fence_after_sync();
       for (int c = 0; c < nch; ++c, ++g) {
@@ -673,18 +623,57 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         tc::mma_f16_ts_w(d, a_l, bh, idesc, 1u);
         tc::mma_commit_w(a_empty + sa);
         tc::mma_commit_w(b_empty + sbb);
-        load_L();
       }
       tc::mma_commit_w(d_full);
     }
-    // drain bulk copies still in flight before the CTA exits
-    while (g < gl) {
-      tc::mbar_wait(b_full + (g % TC2_NB), (g / TC2_NB) & 1);
-      ++g;
-    }
-    while (x < xl) {
-      tc::mbar_wait(x_full + (x % TC2_NT), (x / TC2_NT) & 1);
-      ++x;
+    __syncwarp();
+  } else {
+    // =========================================================== loader (lane 0)
+    // Keeps the three bulk-copy rings full with non-blocking tests: L^-1 chunks (refill of a slot
+    // once its MMAs completed), T groups (once their R2 MMAs completed), staged list records (once
+    // published).  Exactly the CTA's totals are loaded, so nothing is left in flight at exit.
+    if (lane == 0) {
+      const uint32_t tot_L = static_cast<uint32_t>(my_tiles) * nch, tot_T = static_cast<uint32_t>(my_tiles) * ng;
+      uint32_t gl = 0, xl = 0;
+      int lc = 0, xc = 0, sl = 0;
+      while (gl < tot_L || xl < tot_T || sl < my_tiles) {
+        bool prog = false;
+        if (sl < my_tiles && tc::mbar_test(s_empty + (sl & 1), ((sl >> 1) & 1u) ^ 1u)) {
+          const uint64_t r0 = (blockIdx.x + static_cast<uint64_t>(sl) * gridDim.x) * TC_ROWS;
+          const uint32_t n = static_cast<uint32_t>(n_list - r0 < TC_ROWS ? n_list - r0 : TC_ROWS);
+          const uint32_t b4 = (n * 4 + 15) & ~15u, b8 = (n * 8 + 15) & ~15u;   // bulk sizes: multiples of 16 B
+          unsigned char* sg = stg + (sl & 1) * TC2_STG_BYTES;
+          uint64_t* bar = s_full + (sl & 1);
+          tc::mbar_arrive_expect_tx(bar, 2 * b4 + 4 * b8);
+          tc::bulk_g2s(sg + TC2_STG_CVI, L.cvi + r0, b4, bar);
+          tc::bulk_g2s(sg + TC2_STG_J, L.j + r0, b4, bar);
+          tc::bulk_g2s(sg + TC2_STG_M0, L.m0 + r0, b8, bar);
+          tc::bulk_g2s(sg + TC2_STG_DV0, L.dv0 + r0, b8, bar);
+          tc::bulk_g2s(sg + TC2_STG_DV1, L.dv1 + r0, b8, bar);
+          tc::bulk_g2s(sg + TC2_STG_DV2, L.dv2 + r0, b8, bar);
+          ++sl;
+          prog = true;
+        }
+        if (gl < tot_L && tc::mbar_test(b_empty + (gl % TC2_NB), ((gl / TC2_NB) & 1u) ^ 1u)) {
+          const int s_ = gl % TC2_NB;
+          const uint32_t bytes = 2u * (Mp16 - lc * TC_KCH) * TC_KCH * 2;
+          tc::mbar_arrive_expect_tx(b_full + s_, bytes);
+          tc::bulk_g2s(B0 + static_cast<size_t>(s_) * b_stage_bytes, T2.wch + T2.woff[lc], bytes, b_full + s_);
+          ++gl;
+          if (++lc == nch) lc = 0;
+          prog = true;
+        }
+        if (xl < tot_T && tc::mbar_test(x_empty + (xl % TC2_NT), ((xl / TC2_NT) & 1u) ^ 1u)) {
+          const int s_ = xl % TC2_NT;
+          tc::mbar_arrive_expect_tx(x_full + s_, t_stage_bytes);
+          tc::bulk_g2s(T0 + static_cast<size_t>(s_) * t_stage_bytes,
+                       T2.tch + static_cast<size_t>(xc) * (t_stage_bytes / 2), t_stage_bytes, x_full + s_);
+          ++xl;
+          if (++xc == ng) xc = 0;
+          prog = true;
+        }
+        if (!prog) __nanosleep(100);
+      }
     }
     __syncwarp();
   }
