@@ -32,7 +32,7 @@ constexpr int TC2_NA = 8;                    // A ring stages (16 TMEM columns e
 constexpr int TC2_NB = 6;                    // L^-1 chunk ring stages
 constexpr int TC2_PF = TC2_NB - 2;           // chunks prefetched ahead of the MMA (L2 latency); a refill
                                              // waits for the MMAs two chunks back, not the previous one
-constexpr int TC2_NT = 3;                    // T group ring stages
+constexpr int TC2_NT = 2;                    // T group ring stages (refilled early by the loader warp)
 constexpr int TC2_KPMAX = 64;                // one-hot width the host aims for (features beyond go SIMT)
 
 // Shared-memory carve-out: the fixed-size arrays first (compile-time offsets, so the hot loop
