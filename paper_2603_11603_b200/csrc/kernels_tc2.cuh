@@ -413,18 +413,17 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(r_empty + rs);
           ++gr;
+          // per chunk: k of the thread's 4 points (two packed pairs) -> FP16 hi/lo -> A stage; one
+          // st-wait and the a_full arrivals once per group
 #pragma unroll
           for (int cg = 0; cg < TC2_RG; ++cg) {
             const int c = c0 + cg;
             if (c >= nch) break;
-            const int s = g % TC2_NA;
-            const uint32_t a_par = ((g / TC2_NA) & 1u) ^ 1u;
-            const bool a_ready = tc::mbar_test(a_empty + s, a_par);
-            float kv[TC_JPT];
-            // two observed points at a time in packed f32x2 (FFMA2 / FMUL2); MUFU stays scalar
+            uint32_t hw[2], lw[2];
 #pragma unroll
             for (int qp = 0; qp < TC_JPT / 2; ++qp) {
               const int jo = c * TC_KCH + jq * TC_JPT + 2 * qp;      // even
+              // R2 >= 0 by construction (non-negative products, FP32 accumulation; squares)
               unsigned long long r2p = f2_pack(rv[cg * TC_JPT + 2 * qp], rv[cg * TC_JPT + 2 * qp + 1]);
               if (NH > 0) {
 #pragma unroll
@@ -436,19 +435,17 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
                   r2p = f2_fma(d1, d1, r2p);
                 }
               }
-              const float2 r2 = f2_unpack(r2p);
-              const float r2a = fmaxf(r2.x, 0.f), r2b = fmaxf(r2.y, 0.f);
               unsigned long long argp, expp, polyp;
               if (KT == 0) {
-                const unsigned long long rp = f2_pack(tc::sqrt_approx_ftz(r2a), tc::sqrt_approx_ftz(r2b));
+                const float2 r2 = f2_unpack(r2p);
+                const unsigned long long rp = f2_pack(tc::sqrt_approx_ftz(r2.x), tc::sqrt_approx_ftz(r2.y));
                 argp = f2_mul(rp, carg2);
                 const float2 ea = f2_unpack(f2_fma(rp, c1_2, c0_2));
                 expp = f2_pack(tc::ex2_approx(ea.x), tc::ex2_approx(ea.y));
                 polyp = f2_fma(argp, f2_fma(argp, third2, one2), one2);
               } else {
-                const unsigned long long rp2 = f2_pack(r2a, r2b);
-                argp = f2_mul(rp2, carg2);
-                const float2 ea = f2_unpack(f2_fma(rp2, c1_2, c0_2));
+                argp = f2_mul(r2p, carg2);
+                const float2 ea = f2_unpack(f2_fma(r2p, c1_2, c0_2));
                 expp = f2_pack(tc::ex2_approx(ea.x), tc::ex2_approx(ea.y));
                 polyp = one2;
               }
@@ -459,30 +456,44 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
               mu2 = f2_fma(kvalp, alp, mu2);
               sb2 = f2_fma(ccp, aap, sb2);
               kk2 = f2_fma(ccp, ccp, kk2);
+              // FP16 hi / lo split of the (2^ek-scaled) cross-covariances, packed two per column
               const float2 kk = f2_unpack(kvalp);
-              kv[2 * qp] = kk.x;
-              kv[2 * qp + 1] = kk.y;
+              const uint32_t hp = tc::pack_f16x2(kk.x, kk.y);
+              float f0, f1;
+              tc::unpack_f16x2(hp, f0, f1);
+              const float2 lo = f2_unpack(f2_sub(kvalp, f2_pack(f0, f1)));
+              hw[qp] = hp;
+              lw[qp] = tc::pack_f16x2(lo.x, lo.y);
             }
-            // FP16 hi / lo split of the (2^ek-scaled) cross-covariances, packed two per column
-            const uint32_t h01 = tc::pack_f16x2(kv[0], kv[1]), h23 = tc::pack_f16x2(kv[2], kv[3]);
-            float f0, f1, f2, f3;
-            tc::unpack_f16x2(h01, f0, f1);
-            tc::unpack_f16x2(h23, f2, f3);
-            const uint32_t l01 = tc::pack_f16x2(kv[0] - f0, kv[1] - f1), l23 = tc::pack_f16x2(kv[2] - f2, kv[3] - f3);
-            if (!a_ready) tc::mbar_wait(a_empty + s, a_par);
+            const int s = (g + cg) % TC2_NA;
+            tc::mbar_wait(a_empty + s, (((g + cg) / TC2_NA) & 1u) ^ 1u);
             tc::fence_after_sync();
             const uint32_t acol = lane_base + A0col + 16u * s + 2 * jq;
-            tc::tmem_st2(acol, h01, h23);
-            tc::tmem_st2(acol + 8, l01, l23);
-            tc::tmem_st_wait();
-            tc::fence_before_sync();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(a_full + s);
+            tc::tmem_st2(acol, hw[0], hw[1]);
+            tc::tmem_st2(acol + 8, lw[0], lw[1]);
+          }
+          tc::tmem_st_wait();
+          tc::fence_before_sync();
+          __syncwarp();
+#pragma unroll
+          for (int cg = 0; cg < TC2_RG; ++cg) {
+            if (c0 + cg >= nch) break;
+            if (lane == 0) tc::mbar_arrive(a_full + (g % TC2_NA));
             ++g;
           }
           // ---- accumulator column blocks made final by this group's a_empty waits:
           // [c0 - NA, c_last - NA]; one batched read (the last NA blocks are left to the epilogue)
-          {
+          if (c0 >= TC2_NA && c0 + TC2_RG <= nch) {
+            // steady state: blocks c0 - NA .. c0 - NA + 3, all final
+            float v[16];
+            const uint32_t a0 = dq + 16u * static_cast<uint32_t>(c0 - TC2_NA);
+            tc::tmem_ld4x4(a0, a0 + 16u, a0 + 32u, a0 + 48u, v);
+            unsigned long long acc = f2_mul(f2_pack(v[0], v[1]), f2_pack(v[0], v[1]));
+#pragma unroll
+            for (int i = 2; i < 16; i += 2) acc = f2_fma(f2_pack(v[i], v[i + 1]), f2_pack(v[i], v[i + 1]), acc);
+            const float2 a = f2_unpack(acc);
+            vsq_run += a.x + a.y;
+          } else {
             const int c_last = (c0 + TC2_RG < nch ? c0 + TC2_RG : nch) - 1;
             const int b0 = c0 - TC2_NA;
             if (c_last - TC2_NA >= 0) {

@@ -80,6 +80,10 @@ __device__ __forceinline__ float lds_f32(uint32_t a) {
 __device__ __forceinline__ void lds_u64x2(uint32_t a, unsigned long long& x, unsigned long long& y) {
   asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(a));
 }
+// non-volatile: for shared data that is read-only after setup (lets the scheduler hoist / interleave)
+__device__ __forceinline__ void lds_u64x2_nv(uint32_t a, unsigned long long& x, unsigned long long& y) {
+  asm("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(a));
+}
 __device__ __forceinline__ void sts_f32x4(uint32_t a, float x, float y, float z, float w) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
 }
