@@ -57,7 +57,7 @@ typedef enum {
   AS_ERR_OOM = 14            /* device allocation failed */
 } as_status;
 
-typedef enum { AS_MODE_RANGE = 0, AS_MODE_SAMPLE = 1 } as_mode;
+typedef enum { AS_MODE_RANGE = 0, AS_MODE_SAMPLE = 1, AS_MODE_LIST = 2 } as_mode;
 typedef enum { AS_ACQ_EI = 0, AS_ACQ_LCB = 1, AS_ACQ_SIM = 2 } as_acq;
 
 typedef struct {
@@ -75,10 +75,12 @@ typedef struct {
 
 typedef struct {
   int32_t mode;          /* as_mode.  RANGE: candidate j is CVI position begin+j.
-                            SAMPLE: candidate j is pi_seed(begin+j), a Feistel permutation of [0,n_cvi) */
+                            SAMPLE: candidate j is pi_seed(begin+j), a Feistel permutation of [0,n_cvi).
+                            LIST: candidate j is CVI position d_positions[begin+j] (an optimizer-
+                            driven batch, e.g. autoscout_neighbors) */
   int32_t acq;           /* as_acq */
-  uint64_t begin;        /* first position (RANGE) or first sample ordinal (SAMPLE) */
-  uint64_t count;        /* number of candidates; begin+count <= n_cvi */
+  uint64_t begin;        /* first position (RANGE), first sample ordinal (SAMPLE), first list entry (LIST) */
+  uint64_t count;        /* number of candidates; RANGE/SAMPLE: begin+count <= n_cvi */
   uint64_t seed;         /* SAMPLE permutation seed */
   double kappa;          /* LCB exploration weight (default 2) */
   double xi;             /* EI margin (default 0) */
@@ -87,6 +89,10 @@ typedef struct {
   float* d_scores;       /* device, nullable, [count] in batch order: FP32 score, -INF if masked */
   uint64_t* d_raw;       /* device, nullable, [count] raw index of each candidate */
   uint64_t* d_valid_count; /* device, nullable: atomically incremented by #valid candidates */
+  const uint64_t* d_positions; /* LIST only (else ignored): device array of CVI positions, caller-owned;
+                            it must stay valid until the autoscout_topk / autoscout_topk_pool call
+                            of this pool returns (certification may re-score recorded batches).
+                            An entry >= n_cvi is scored as masked (-INF, raw UINT64_MAX). */
 } as_score_args;
 
 /* Parse and validate a space JSON document (schema: DESIGN.md §2), build the
@@ -138,6 +144,30 @@ as_status autoscout_topk_merge(const as_space* s, const void* pools, const int32
 as_status autoscout_decode(const as_space* s, uint64_t raw, int32_t* digits_out, int32_t* valid_out);
 as_status autoscout_cvi_to_raw(const as_space* s, uint64_t cvi, uint64_t* raw_out);
 as_status autoscout_sample_to_cvi(const as_space* s, uint64_t seed, uint64_t ordinal, uint64_t* cvi_out);
+/* Exact CVI position of a raw index (host).  member_out = 1 iff raw is in the compact valid index
+ * (G1 canonical + every non-resource constraint, R4), and then cvi_out is its position;
+ * otherwise cvi_out = number of members with a smaller raw index.  AS_ERR_INDEX_RANGE if
+ * raw >= n_raw.  Inverse of autoscout_cvi_to_raw on members. */
+as_status autoscout_raw_to_cvi(const as_space* s, uint64_t raw, uint64_t* cvi_out, int32_t* member_out);
+/* MCTS subtree as a batch ("each node corresponds to a
+ * partial configuration ... each edge represents a valid refinement"): the configurations whose
+ * first n_assigned features (declaration order) carry digits[0..n_assigned) form one contiguous
+ * CVI range [begin, begin+count) -- the structural digits are the most significant (R2, R4) --
+ * so AS_MODE_RANGE over it scores every completion of the partial assignment in one launch.
+ * n_assigned = 0: the whole CVI.  count = 0 if no member has that prefix.  AS_ERR_INVALID_ARG
+ * for n_assigned outside [0, d] or a digit outside its domain. */
+as_status autoscout_subtree_range(const as_space* s, const int32_t* digits, int32_t n_assigned,
+                                  uint64_t* begin_out, uint64_t* count_out);
+/* Coordinate-neighbour batch of a configuration (PAPER.md:173
+ * "perturbs the active parameter along its current search direction", SPEC.md:230-247 propose /
+ * update with step doubling): for every ACTIVE feature of kind "dense" of `raw` in declaration
+ * order, every step 2^e (e = 0, 1, ... while 2^e < n_f) and direction +1 then -1, the
+ * configuration with that digit moved by the step, if it stays in the domain and is a CVI member
+ * (moving a gate can make the neighbour non-canonical: it is then skipped).  Writes the CVI
+ * positions in that order to cvi_out (host, cap entries); n_out = the number of neighbours.
+ * AS_ERR_CAPACITY (n_out still set) if n_out > cap; AS_ERR_INDEX_RANGE if raw >= n_raw.
+ * The base configuration itself need not be valid.  Score the result with AS_MODE_LIST. */
+as_status autoscout_neighbors(const as_space* s, uint64_t raw, uint64_t* cvi_out, int32_t cap, int32_t* n_out);
 /* FP64 simulator + resource check of one configuration (host).  ok_out = G4 passes. */
 as_status autoscout_simulate(const as_space* s, uint64_t raw, double* cost_out, double* mem_out,
                              int32_t* ok_out);

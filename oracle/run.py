@@ -20,8 +20,12 @@ from . import sim as _sim
 from .feistel import Feistel
 
 
-def positions(space, mode, begin, count, seed=0):
+def positions(space, mode, begin, count, seed=0, plist=None):
     n = space.n_cvi()
+    if mode == "list":
+        # LIST (NEXT-2 batches): candidate j is plist[begin + j]; entries outside [0, n) stay as
+        # given and are scored as masked by score_batch
+        return [int(x) for x in plist[begin:begin + count]]
     if begin < 0 or count < 0 or begin + count > n:
         raise IndexError("batch exceeds the CVI range")
     if mode == "range":
@@ -75,10 +79,17 @@ def evaluate(space, digits_list, fit, acq="ei", kappa=2.0, xi=0.0):
     return rec
 
 
-def score_batch(space, fit, mode, begin, count, seed=0, acq="ei", kappa=2.0, xi=0.0):
-    pos = positions(space, mode, begin, count, seed)
-    digits = [space.cvi_unrank(p) for p in pos]
+def score_batch(space, fit, mode, begin, count, seed=0, acq="ei", kappa=2.0, xi=0.0, plist=None):
+    pos = positions(space, mode, begin, count, seed, plist)
+    n = space.n_cvi()
+    inside = [0 <= p < n for p in pos]
+    digits = [space.cvi_unrank(p) if ok else space.cvi_unrank(0) for p, ok in zip(pos, inside)]
     rec = evaluate(space, digits, fit, acq, kappa, xi)
+    if not all(inside):
+        out = ~np.array(inside, dtype=bool)
+        rec["valid"] = rec["valid"] & ~out
+        rec["score"] = np.where(out, -np.inf, rec["score"])
+        rec["raw"] = np.where(out, np.uint64(np.iinfo(np.uint64).max), rec["raw"]).astype(np.uint64)
     rec["cvi"] = np.array(pos, dtype=np.int64)
     rec["digits"] = digits
     return rec

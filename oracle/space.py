@@ -376,6 +376,54 @@ class Space:
                 raise ValueError("configuration is not structurally valid")
         return p
 
+    # ---- optimizer-driven batches
+    def subtree_range(self, prefix):
+        """MCTS subtree as a CVI range ("each node corresponds to a partial
+        configuration ... each edge represents a valid refinement"): the members whose first
+        len(prefix) digits equal `prefix` are the positions [begin, begin + count) -- contiguous
+        because the CVI is ascending raw order with the first-declared feature most significant
+        (R2, R4).  begin = members below the prefix, counted by the same prefix walk
+        as cvi_rank; count = completions of the prefix (0 if the prefix itself is invalid)."""
+        n = len(prefix)
+        d = len(self.features)
+        dg = [0] * d
+        act = [False] * d
+        p = 0
+        for j in range(n):
+            for v in range(prefix[j]):
+                dg[j] = v
+                act[j] = self._act_of(j, dg, act)
+                if self._extend_ok(j, dg, act):
+                    p += self._count_key(j + 1, self._key(j + 1, dg, act))
+            dg[j] = prefix[j]
+            act[j] = self._act_of(j, dg, act)
+            if not self._extend_ok(j, dg, act):
+                return p, 0
+        return p, self._count_key(n, self._key(n, dg, act))
+
+    def coordinate_neighbors(self, digits):
+        """Coordinate-search candidates of a configuration ("perturbs the active parameter
+        along its current search direction"; S:230-247 propose/update with step doubling), all
+        at once (reading R19): for every ACTIVE dense feature in declaration order, every step
+        2^e < n_f, direction +1 then -1, the configuration with that digit moved, if inside the
+        domain and structurally valid (G1-G3)."""
+        act = self.activity(digits)
+        out = []
+        for f, feat in enumerate(self.features):
+            if feat.kind != "dense" or not act[f]:
+                continue
+            step = 1
+            while step < feat.n:
+                for sgn in (1, -1):
+                    nd = digits[f] + sgn * step
+                    if 0 <= nd < feat.n:
+                        y = list(digits)
+                        y[f] = nd
+                        if self.structurally_valid(y):
+                            out.append(y)
+                step *= 2
+        return out
+
     def enumerate_cvi(self):
         """Every structurally valid configuration exactly once, ascending raw."""
         d = len(self.features)

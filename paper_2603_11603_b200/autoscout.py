@@ -23,7 +23,8 @@ LIB_PATH = os.environ.get("AUTOSCOUT_LIB") or os.path.join(HERE, "libautoscout.s
 AS_MODE_RANGE, AS_MODE_SAMPLE = 0, 1
 AS_ACQ_EI, AS_ACQ_LCB, AS_ACQ_SIM = 0, 1, 2
 ACQ = {"ei": AS_ACQ_EI, "lcb": AS_ACQ_LCB, "sim": AS_ACQ_SIM}
-MODE = {"range": AS_MODE_RANGE, "sample": AS_MODE_SAMPLE}
+AS_MODE_LIST = 2
+MODE = {"range": AS_MODE_RANGE, "sample": AS_MODE_SAMPLE, "list": AS_MODE_LIST}
 STATUS = {0: "AS_OK", 1: "AS_ERR_INVALID_ARG", 2: "AS_ERR_SPACE_SCHEMA", 3: "AS_ERR_SPACE_CYCLE",
           4: "AS_ERR_SPACE_ORDER", 5: "AS_ERR_SPACE_EMPTY", 6: "AS_ERR_INDEX_RANGE", 7: "AS_ERR_INVALID_CONFIG",
           8: "AS_ERR_NO_OBSERVATIONS", 9: "AS_ERR_NUMERIC", 10: "AS_ERR_CAPACITY", 11: "AS_ERR_STATE",
@@ -34,7 +35,7 @@ EXPORTS = ["autoscout_space_create", "autoscout_space_destroy", "autoscout_space
            "autoscout_observe_clear", "autoscout_observe_info", "autoscout_score_batch", "autoscout_topk",
            "autoscout_topk_pool", "autoscout_topk_merge", "autoscout_decode", "autoscout_cvi_to_raw",
            "autoscout_sample_to_cvi", "autoscout_simulate", "autoscout_mask_range", "autoscout_set_path",
-           "autoscout_set_timing",
+           "autoscout_set_timing", "autoscout_raw_to_cvi", "autoscout_subtree_range", "autoscout_neighbors",
            "autoscout_last_kernel_ms", "autoscout_last_phase_ms", "autoscout_last_error"]
 
 
@@ -49,7 +50,8 @@ class ScoreArgs(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int32), ("acq", ctypes.c_int32), ("begin", ctypes.c_uint64),
                 ("count", ctypes.c_uint64), ("seed", ctypes.c_uint64), ("kappa", ctypes.c_double),
                 ("xi", ctypes.c_double), ("k", ctypes.c_int32), ("accumulate", ctypes.c_int32),
-                ("d_scores", ctypes.c_void_p), ("d_raw", ctypes.c_void_p), ("d_valid_count", ctypes.c_void_p)]
+                ("d_scores", ctypes.c_void_p), ("d_raw", ctypes.c_void_p), ("d_valid_count", ctypes.c_void_p),
+                ("d_positions", ctypes.c_void_p)]
 
 
 class AutoscoutError(RuntimeError):
@@ -80,6 +82,9 @@ def _load():
         "autoscout_decode": ([P, U64, pI32, pI32], I32),
         "autoscout_cvi_to_raw": ([P, U64, pU64], I32),
         "autoscout_sample_to_cvi": ([P, U64, U64, pU64], I32),
+        "autoscout_raw_to_cvi": ([P, U64, pU64, pI32], I32),
+        "autoscout_subtree_range": ([P, pI32, I32, pU64, pU64], I32),
+        "autoscout_neighbors": ([P, U64, pU64, I32, pI32], I32),
         "autoscout_simulate": ([P, U64, pD, pD, pI32], I32),
         "autoscout_mask_range": ([P, U64, U64, P, P, P], I32),
         "autoscout_set_path": ([P, I32], I32),
@@ -180,6 +185,28 @@ class Space:
         _check(_LIB.autoscout_cvi_to_raw(self.h, int(cvi), ctypes.byref(r)))
         return r.value
 
+    def raw_to_cvi(self, raw):
+        """-> (position, member): position of raw in the CVI if member, else #members below it."""
+        r, m = ctypes.c_uint64(), ctypes.c_int32()
+        _check(_LIB.autoscout_raw_to_cvi(self.h, int(raw), ctypes.byref(r), ctypes.byref(m)))
+        return r.value, bool(m.value)
+
+    def subtree_range(self, digits):
+        """CVI range (begin, count) of the completions of a partial assignment of the first
+        len(digits) features (MCTS subtree, NEXT-2(i))."""
+        d = (ctypes.c_int32 * max(len(digits), 1))(*[int(x) for x in digits])
+        b, c = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(_LIB.autoscout_subtree_range(self.h, d, len(digits), ctypes.byref(b), ctypes.byref(c)))
+        return b.value, c.value
+
+    def neighbors(self, raw, cap=4096):
+        """CVI positions of the coordinate neighbours of raw (NEXT-2(ii)), as a uint64 numpy array."""
+        out = np.zeros(max(cap, 1), dtype=np.uint64)
+        n = ctypes.c_int32()
+        _check(_LIB.autoscout_neighbors(self.h, int(raw), out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                        int(cap), ctypes.byref(n)))
+        return out[:n.value].copy()
+
     def sample_to_cvi(self, seed, ordinal):
         r = ctypes.c_uint64()
         _check(_LIB.autoscout_sample_to_cvi(self.h, int(seed), int(ordinal), ctypes.byref(r)))
@@ -211,14 +238,18 @@ class Space:
 
     # --------------------------------------------------------------- scoring
     def score_batch(self, mode="range", begin=0, count=None, seed=0, acq="ei", k=32, kappa=None, xi=None,
-                    accumulate=False, d_scores=None, d_raw=None, d_valid_count=None, stream=None):
+                    accumulate=False, d_scores=None, d_raw=None, d_valid_count=None, d_positions=None,
+                    stream=None):
+        """mode "list": candidate j is CVI position d_positions[begin + j] (device uint64 tensor the
+        caller keeps alive until topk); count defaults to len(d_positions) - begin."""
         gp = self.doc.get("gp", {})
         a = ScoreArgs(MODE[mode] if isinstance(mode, str) else int(mode),
                       ACQ[acq] if isinstance(acq, str) else int(acq), int(begin),
-                      int(self.n_cvi - begin if count is None else count), int(seed),
+                      int((self.n_cvi if d_positions is None else d_positions.numel()) - begin
+                          if count is None else count), int(seed),
                       float(gp.get("kappa", 2.0) if kappa is None else kappa),
                       float(gp.get("xi", 0.0) if xi is None else xi), int(k), 1 if accumulate else 0,
-                      _ptr(d_scores), _ptr(d_raw), _ptr(d_valid_count))
+                      _ptr(d_scores), _ptr(d_raw), _ptr(d_valid_count), _ptr(d_positions))
         _check(_LIB.autoscout_score_batch(self.h, ctypes.byref(a), _stream_ptr(stream)))
 
     def topk(self, k, stream=None, allow_uncertified=False):
@@ -309,3 +340,15 @@ def autoscout_topk(space, k, stream=None):
 
 
 autoscout_topk_merge = topk_merge
+
+
+def autoscout_raw_to_cvi(space, raw):
+    return space.raw_to_cvi(raw)
+
+
+def autoscout_subtree_range(space, digits):
+    return space.subtree_range(digits)
+
+
+def autoscout_neighbors(space, raw, cap=4096):
+    return space.neighbors(raw, cap)

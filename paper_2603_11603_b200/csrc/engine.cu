@@ -586,6 +586,8 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
   A.begin = a.begin;
   A.count = a.count;
   A.fk = feistel_make(s->H.n_cvi, a.seed);
+  A.list = a.mode == AS_MODE_LIST ? a.d_positions : nullptr;
+  A.n_cvi = s->H.n_cvi;
   A.kappa = a.kappa;
   A.xi = a.xi;
   A.d_scores = a.d_scores;
@@ -961,10 +963,15 @@ as_status autoscout_observe_info(const as_space* s, int32_t* m_out, double* b_ou
 as_status autoscout_score_batch(as_space* s, const as_score_args* a, void* cuda_stream) {
   if (!s || !a) return fail(AS_ERR_INVALID_ARG, "null argument");
   if (s->device < 0) return fail(AS_ERR_STATE, "host-only handle cannot score (no CUDA device)");
-  if (a->mode != AS_MODE_RANGE && a->mode != AS_MODE_SAMPLE) return fail(AS_ERR_INVALID_ARG, "bad mode");
+  if (a->mode != AS_MODE_RANGE && a->mode != AS_MODE_SAMPLE && a->mode != AS_MODE_LIST)
+    return fail(AS_ERR_INVALID_ARG, "bad mode");
+  if (a->mode == AS_MODE_LIST && a->count > 0 && !a->d_positions)
+    return fail(AS_ERR_INVALID_ARG, "LIST mode needs d_positions");
+  if (a->mode == AS_MODE_LIST && a->count > 0 && s->H.n_cvi == 0)
+    return fail(AS_ERR_INDEX_RANGE, "LIST mode on a space without valid configurations");
   if (a->acq < AS_ACQ_EI || a->acq > AS_ACQ_SIM) return fail(AS_ERR_INVALID_ARG, "bad acquisition");
   if (a->k < 1 || a->k > 1024) return fail(AS_ERR_INVALID_ARG, "k must be in [1, 1024]");
-  if (a->begin > s->H.n_cvi || a->count > s->H.n_cvi - a->begin)
+  if (a->mode != AS_MODE_LIST && (a->begin > s->H.n_cvi || a->count > s->H.n_cvi - a->begin))
     return fail(AS_ERR_INDEX_RANGE, "batch exceeds [0, n_cvi)");
   if (a->acq == AS_ACQ_EI && s->G.M == 0) return fail(AS_ERR_NO_OBSERVATIONS, "EI needs at least one observation");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
@@ -1084,6 +1091,60 @@ as_status autoscout_cvi_to_raw(const as_space* s, uint64_t cvi, uint64_t* raw_ou
   DV dv;
   uint32_t act;
   if (!cvi_decode(s->H, cvi, dv, act, *raw_out)) return fail(AS_ERR_INDEX_RANGE, "cvi >= n_cvi");
+  return AS_OK;
+}
+
+as_status autoscout_raw_to_cvi(const as_space* s, uint64_t raw, uint64_t* cvi_out, int32_t* member_out) {
+  if (!s || !cvi_out) return fail(AS_ERR_INVALID_ARG, "null argument");
+  if (raw >= s->H.n_raw) return fail(AS_ERR_INDEX_RANGE, "raw >= n_raw");
+  bool m = false;
+  *cvi_out = cvi_rank(s->H, raw, &m);
+  if (member_out) *member_out = m ? 1 : 0;
+  return AS_OK;
+}
+
+as_status autoscout_subtree_range(const as_space* s, const int32_t* digits, int32_t n_assigned,
+                                  uint64_t* begin_out, uint64_t* count_out) {
+  if (!s || !begin_out || !count_out || (n_assigned > 0 && !digits)) return fail(AS_ERR_INVALID_ARG, "null argument");
+  const HostSpace& H = s->H;
+  if (n_assigned < 0 || n_assigned > H.d) return fail(AS_ERR_INVALID_ARG, "n_assigned outside [0, d]");
+  uint64_t lo = 0;
+  for (int f = 0; f < n_assigned; ++f) {
+    if (digits[f] < 0 || digits[f] >= H.feat[f].n) return fail(AS_ERR_INVALID_ARG, "digit outside its domain");
+    lo += static_cast<uint64_t>(digits[f]) * H.stride[f];
+  }
+  const uint64_t hi = lo + (n_assigned > 0 ? H.stride[n_assigned - 1] : H.n_raw);
+  const uint64_t b = cvi_rank(H, lo, nullptr), e = cvi_rank(H, hi, nullptr);
+  *begin_out = b;
+  *count_out = e - b;
+  return AS_OK;
+}
+
+as_status autoscout_neighbors(const as_space* s, uint64_t raw, uint64_t* cvi_out, int32_t cap, int32_t* n_out) {
+  if (!s || !n_out || (cap > 0 && !cvi_out) || cap < 0) return fail(AS_ERR_INVALID_ARG, "bad arguments");
+  const HostSpace& H = s->H;
+  if (raw >= H.n_raw) return fail(AS_ERR_INDEX_RANGE, "raw >= n_raw");
+  int dig[DMAX];
+  bool act[DMAX];
+  for (int f = 0; f < H.d; ++f) dig[f] = static_cast<int>((raw / H.stride[f]) % H.feat[f].n);
+  activity(H, dig, act);
+  int n = 0;
+  for (int f = 0; f < H.d; ++f) {
+    if (!H.feat[f].dense || !act[f]) continue;
+    for (int step = 1; step < H.feat[f].n; step *= 2)
+      for (int dir = 1; dir >= -1; dir -= 2) {
+        const int nd = dig[f] + dir * step;
+        if (nd < 0 || nd >= H.feat[f].n) continue;
+        const uint64_t r2 = raw - static_cast<uint64_t>(dig[f]) * H.stride[f] + static_cast<uint64_t>(nd) * H.stride[f];
+        bool m = false;
+        const uint64_t pos = cvi_rank(H, r2, &m);
+        if (!m) continue;
+        if (n < cap) cvi_out[n] = pos;
+        ++n;
+      }
+  }
+  *n_out = n;
+  if (n > cap) return fail(AS_ERR_CAPACITY, "more neighbours than cap");
   return AS_OK;
 }
 

@@ -65,7 +65,22 @@ struct BatchArgs {
   float* d_scores;
   uint64_t* d_raw;
   uint64_t* d_valid_count;
+  const uint64_t* list;   // LIST mode: CVI positions (entries >= n_cvi are masked)
+  uint64_t n_cvi;
 };
+
+// a0: candidate j of the batch -> CVI position.  A LIST entry outside [0, n_cvi) is
+// replaced by position 0 and reported through `in` = false: the caller decodes unconditionally
+// (keeps the hot RANGE / SAMPLE code straight-line) and scores the candidate as masked.
+__device__ __forceinline__ uint64_t assign_pos(const BatchArgs& A, uint64_t j, bool& in) {
+  in = true;
+  if (A.mode == 2) {
+    const uint64_t p = __ldg(A.list + A.begin + j);
+    in = p < A.n_cvi;
+    return in ? p : 0;
+  }
+  return (A.mode == 0) ? A.begin + j : feistel_pi(A.fk, A.begin + j);
+}
 
 struct CtaOut {
   uint64_t* lists;     // [grid][KC]
@@ -467,13 +482,18 @@ score_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out) {
     double m0 = 0.0;
     DV dv;
     if (in) {
-      const uint64_t pcvi = (A.mode == 0) ? A.begin + j : feistel_pi(A.fk, A.begin + j);
+      bool pin;
+      const uint64_t pcvi = assign_pos(A, j, pin);
       pos = static_cast<uint32_t>(pcvi);
       uint32_t act;
       decode_dev(S, pcvi, dv, act, raw);
       double cost;
       sim_dev(S, dv, act, cost, ok);
       m0 = log(cost);
+      if (!pin) {
+        ok = false;
+        raw = ~0ull;
+      }
       if (A.d_raw) A.d_raw[j] = raw;
       if (!ok && A.d_scores) A.d_scores[j] = -INFINITY;
     }

@@ -56,10 +56,15 @@ gen_kernel(DevSpace S, BatchArgs A, uint64_t j0, uint64_t nj, CandList L, int ci
     double cost = 1.0;
     const uint64_t j = j0 + jj;
     if (in) {
-      pcvi = (A.mode == 0) ? A.begin + j : feistel_pi(A.fk, A.begin + j);
+      bool pin;
+      pcvi = assign_pos(A, j, pin);
       if (by_bucket) decode_dev_bucket(S, gen_cidx, gen_bkt, pcvi, dv, act, raw);
       else decode_dev_ci(S, gen_cidx, ci_n, pcvi, dv, act, raw);
       sim_dev(S, dv, act, cost, ok);
+      if (!pin) {
+        ok = false;
+        raw = ~0ull;
+      }
       if (A.d_raw) A.d_raw[j] = raw;
       if (!ok && A.d_scores) A.d_scores[j] = -INFINITY;
     }

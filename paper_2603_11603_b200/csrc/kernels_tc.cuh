@@ -326,13 +326,18 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
       const bool in = j < A.count;
       bool ok = false;
       if (in) {
-        const uint64_t pcvi = (A.mode == 0) ? A.begin + j : feistel_pi(A.fk, A.begin + j);
+        bool pin;
+        const uint64_t pcvi = assign_pos(A, j, pin);
         DV dv;
         uint32_t act;
         uint64_t raw;
         decode_dev_idx(S, sm.cidx, pcvi, dv, act, raw);
         double cost;
         sim_dev(S, dv, act, cost, ok);
+        if (!pin) {
+          ok = false;
+          raw = ~0ull;
+        }
         if (A.d_raw) A.d_raw[j] = raw;
         if (!ok && A.d_scores) A.d_scores[j] = -INFINITY;
         if (ok) {

@@ -215,6 +215,7 @@ Status build_space(const char* json, HostSpace& S) {
     const asj::Value* kind = f.get("kind");
     if (!kind || kind->kind != asj::Value::String || (kind->str != "sparse" && kind->str != "dense"))
       return err(E_SCHEMA, "feature " + F.name + ": kind must be sparse|dense");
+    F.dense = kind->str == "dense";
     const asj::Value* dom = f.get("domain");
     if (!dom || dom->kind != asj::Value::Array) return err(E_SCHEMA, "feature " + F.name + ": domain must be an array");
     if (dom->arr.empty()) return err(E_EMPTY, "feature " + F.name + " has an empty domain (SPEC.md:58)");
@@ -674,6 +675,37 @@ bool cvi_decode(const HostSpace& S, uint64_t p, DV& dv, uint32_t& act, uint64_t&
     raw += tu.raw;
   }
   return true;
+}
+
+// Number of CVI members with raw index < raw (raw <= n_raw), and whether raw itself is a member.
+// The CVI is ascending raw order (R4); the structural prefix is the most significant digit block,
+// so members below raw are: every member of a structure whose prefix raw part is smaller, plus,
+// inside the structure with an equal prefix, the tail combinations that compare lower group by
+// group (tail groups are contiguous digit blocks, the earlier group more significant).
+uint64_t cvi_rank(const HostSpace& S, uint64_t raw, bool* member) {
+  if (member) *member = false;
+  if (raw >= S.n_raw) return S.n_cvi;
+  const uint64_t raw_p = raw - raw % S.tail_span, raw_t = raw % S.tail_span;
+  const size_t i = static_cast<size_t>(std::lower_bound(S.s_raw.begin(), S.s_raw.end(), raw_p) - S.s_raw.begin());
+  uint64_t r = S.prefix[i];
+  if (i == static_cast<size_t>(S.n_struct) || S.s_raw[i] != raw_p) return r;
+  const int n_comp = static_cast<int>(S.comp_first.size());
+  for (int c = 0; c < n_comp; ++c) {
+    // raw contribution of group c's digits in raw_t
+    uint64_t contrib = 0;
+    for (int f = S.comp_first[c]; f < S.comp_first[c] + S.comp_width[c]; ++f)
+      contrib += ((raw_t / S.stride[f]) % S.feat[f].n) * S.stride[f];
+    const uint32_t off = S.s_off[i * n_comp + c], cnt = S.s_cnt[i * n_comp + c];
+    const Tuple* b = S.tuples.data() + off;
+    const Tuple* e = b + cnt;
+    const Tuple* lb = std::lower_bound(b, e, contrib, [](const Tuple& t, uint64_t v) { return t.raw < v; });
+    uint64_t mult = 1;
+    for (int h = c + 1; h < n_comp; ++h) mult *= S.s_cnt[i * n_comp + h];
+    r += static_cast<uint64_t>(lb - b) * mult;
+    if (lb == e || lb->raw != contrib) return r;
+  }
+  if (member) *member = true;
+  return r;
 }
 
 bool raw_decode(const HostSpace& S, uint64_t raw, int* dig, DV& dv, uint32_t& act, bool& structural) {

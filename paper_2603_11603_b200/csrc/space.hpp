@@ -26,6 +26,7 @@ struct FeatureH {
   int n = 0;
   int dflt = 0;
   int vkind = 0;              // 0 number, 1 bool, 2 string
+  bool dense = false;         // kind "dense" (coordinate-search knob)
   std::vector<double> num;    // numeric value of each digit (bool 0/1, string: index)
   std::vector<std::string> str;
   std::vector<Atom> req;
@@ -85,6 +86,7 @@ Status build_space(const char* json, HostSpace& S);
 void activity(const HostSpace& S, const int* dig, bool* act);
 bool cvi_decode(const HostSpace& S, uint64_t p, DV& dv, uint32_t& act, uint64_t& raw);  // p < n_cvi
 // raw -> digits; *structural = G1 + constraints (membership in the CVI); returns false if raw >= n_raw
+uint64_t cvi_rank(const HostSpace& S, uint64_t raw, bool* member);   // #members with raw index < raw
 bool raw_decode(const HostSpace& S, uint64_t raw, int* dig, DV& dv, uint32_t& act, bool& structural);
 void simulate_host(const HostSpace& S, const DV& dv, uint32_t act, double& cost, bool& ok, double& mem);
 

@@ -1,0 +1,96 @@
+"""GPU parity of the NEXT-2 batches (-m gpu): AS_MODE_LIST over coordinate-neighbour batches and
+random position lists, and AS_MODE_RANGE over an MCTS subtree range, through the C-ABI, against
+the oracle element by element (bars: DESIGN.md §4.3)."""
+
+import numpy as np
+import pytest
+
+from conftest import space_path
+from oracle import run
+from parity_util import ei_tolerance_ok, observed, oracle_space
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+A = pytest.importorskip("paper_2603_11603_b200.autoscout")
+
+U64MAX = np.uint64(np.iinfo(np.uint64).max)
+
+
+def _setup(name, M, seed=0):
+    o = oracle_space(name)
+    raws, costs = observed(o, M, seed)
+    fit = run.observed_fit(o, raws, costs)
+    sp = A.Space(space_path(name), 0)
+    sp.observe(raws, costs)
+    return o, fit, sp
+
+
+def _list_positions(o, sp, rng, n_base=12, n_rand=300):
+    n = o.n_cvi()
+    pos = []
+    for _ in range(n_base):
+        pos += sp.neighbors(sp.cvi_to_raw(int(rng.integers(n)))).tolist()
+    pos += rng.integers(0, n, n_rand).tolist()
+    pos = list(dict.fromkeys(pos))                     # distinct, first-seen order
+    pos.insert(len(pos) // 2, n + 5)                   # one entry outside [0, n_cvi): masked
+    return pos
+
+
+def _gpu(sp, d_pos, n, acq, kappa=None, k=32):
+    sc = torch.empty(n, dtype=torch.float32, device="cuda")
+    rw = torch.empty(n, dtype=torch.int64, device="cuda")
+    vc = torch.zeros(1, dtype=torch.int64, device="cuda")
+    sp.score_batch(mode="list", begin=0, count=n, acq=acq, kappa=kappa, k=k, d_scores=sc, d_raw=rw,
+                   d_valid_count=vc, d_positions=d_pos)
+    top = sp.topk(k)
+    torch.cuda.synchronize()
+    return sc.cpu().numpy(), rw.cpu().numpy().astype(np.uint64), int(vc.item()), top
+
+
+@pytest.mark.parametrize("name,M", [("C3", 32), ("C2", 64), ("C5", 128), ("C4", 256)])
+def test_list_mode_neighbors_parity(name, M):
+    o, fit, sp = _setup(name, M)
+    rng = np.random.default_rng(5)
+    pos = _list_positions(o, sp, rng)
+    d_pos = torch.tensor(np.array(pos, dtype=np.uint64).view(np.int64), device="cuda")
+    n = len(pos)
+    rec = run.score_batch(o, fit, "list", 0, n, acq="lcb", kappa=0.0, plist=pos)
+    # decode + mask: bit-exact
+    sc, rw, nv, top = _gpu(sp, d_pos, n, "lcb", kappa=0.0)
+    assert np.array_equal(rw, rec["raw"])
+    assert np.array_equal(np.isfinite(sc), rec["valid"])
+    assert nv == int(rec["valid"].sum())
+    v = rec["valid"]
+    mu = rec["mu"]
+    assert np.all(np.abs(-sc[v] - mu[v]) <= 1e-5 * np.maximum(1.0, np.abs(mu[v])))
+    assert [r for r, _ in top] == [r for r, _ in run.topk(rec, 32)]
+    # EI: tolerance of SURVEY A.7, top-k raw order exact, refined scores 1e-12
+    sc, rw, nv, top = _gpu(sp, d_pos, n, "ei")
+    ref = run.score_batch(o, fit, "list", 0, n, acq="ei", plist=pos)
+    ok = ei_tolerance_ok(sc[v].astype(np.float64), ref["score"][v], mu[v], rec["s2"][v], fit.fstar, fit.sf2)
+    assert ok.all()
+    want = run.topk(ref, 32)
+    assert [r for r, _ in top] == [r for r, _ in want]
+    for (_, a), (_, b) in zip(top, want):
+        assert a == pytest.approx(b, rel=1e-12, abs=1e-12)
+
+
+@pytest.mark.parametrize("name,M", [("C1", 16), ("C3", 32)])
+def test_subtree_range_best_completion(name, M):
+    """Scoring the subtree range returns the best completion of the partial assignment: the
+    oracle's top-k over the enumerated members with that prefix."""
+    o, fit, sp = _setup(name, M)
+    mem = list(o.enumerate_cvi())
+    rng = np.random.default_rng(2)
+    for _ in range(4):
+        x = mem[int(rng.integers(len(mem)))]
+        pre = x[: max(1, len(x) // 2)]
+        b, c = sp.subtree_range(pre)
+        assert c > 0
+        sp.score_batch(mode="range", begin=b, count=c, acq="ei", k=8)
+        got = sp.topk(8)
+        idx = [i for i, m in enumerate(mem) if m[: len(pre)] == pre]
+        ref = run.score_batch(o, fit, "range", idx[0], len(idx), acq="ei")
+        assert [r for r, _ in got] == [r for r, _ in run.topk(ref, 8)]
