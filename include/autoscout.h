@@ -144,6 +144,18 @@ as_status autoscout_topk_merge(const as_space* s, const void* pools, const int32
 as_status autoscout_decode(const as_space* s, uint64_t raw, int32_t* digits_out, int32_t* valid_out);
 as_status autoscout_cvi_to_raw(const as_space* s, uint64_t cvi, uint64_t* raw_out);
 as_status autoscout_sample_to_cvi(const as_space* s, uint64_t seed, uint64_t ordinal, uint64_t* cvi_out);
+/* GP prior mean m0 of a configuration under the current fit (host, FP64; R9, R20):
+ * source_out = 1 if it is the regression-simulator ensemble (space JSON gp.prior = "ensemble"
+ * and at least one simulator with holdout R^2 > 0 after the last observe; SURVEY.md §8(f) NEXT-1,
+ * PAPER.md:518-548), else 0 and m0 = ln cost_sim of the analytical simulator.  The same m0 is
+ * used on the device for every candidate.  AS_ERR_INDEX_RANGE if raw >= n_raw. */
+as_status autoscout_prior(const as_space* s, uint64_t raw, double* m0_out, int32_t* source_out);
+/* The four Table 2 simulators of the last fit (PAPER.md:524-531 order: 3D-Parallelism,
+ * 5D-Parallelism, DDP-Aware, Communication-Aware): holdout R^2 (-INF = not fitted: fewer than
+ * |subset|+2 training observations) and weights max(0,R^2)/sum;
+ * available_out = 0 when every R^2 <= 0 ("Unavailable") or gp.prior = "sim".
+ * Arrays are host, 4 entries each, nullable. */
+as_status autoscout_ensemble_info(const as_space* s, double* r2_out, double* w_out, int32_t* available_out);
 /* Exact CVI position of a raw index (host).  member_out = 1 iff raw is in the compact valid index
  * (G1 canonical + every non-resource constraint, R4), and then cvi_out is its position;
  * otherwise cvi_out = number of members with a smaller raw index.  AS_ERR_INDEX_RANGE if

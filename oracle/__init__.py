@@ -32,4 +32,4 @@ has no serving model (SURVEY §8(c) ledger #3) -- "parity partially unpinned" fo
 non-special-case values, as stated in DESIGN.md.
 """
 
-from . import space, sim, gp, acq, feistel, run  # noqa: F401
+from . import space, sim, gp, acq, feistel, ensemble, run  # noqa: F401

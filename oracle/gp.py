@@ -117,3 +117,9 @@ def fit_observed(space, digits_list, cost_obs, cost_sim_obs):
     O = features(space, digits_list) if len(digits_list) else np.zeros((0, len(space.features)))
     return Fit(space, O, np.log(np.asarray(cost_obs, dtype=np.float64)),
                np.log(np.asarray(cost_sim_obs, dtype=np.float64)))
+
+
+def fit_observed_prior(space, digits_list, cost_obs, m0_obs):
+    """observe() with an explicit prior mean at the observed points (NEXT-1 ensemble, R20)."""
+    O = features(space, digits_list) if len(digits_list) else np.zeros((0, len(space.features)))
+    return Fit(space, O, np.log(np.asarray(cost_obs, dtype=np.float64)), np.asarray(m0_obs, dtype=np.float64))

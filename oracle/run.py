@@ -15,6 +15,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import acq as _acq
+from . import ensemble as _ens
 from . import gp as _gp
 from . import sim as _sim
 from .feistel import Feistel
@@ -48,7 +49,19 @@ def observed_fit(space, raws, costs):
             raise ValueError("observed configuration violates the resource check (G4)")
     else:
         cs = np.zeros(0)
-    return _gp.fit_observed(space, digits, costs, cs)
+    ens = None
+    if space.gp.get("prior", "sim") == "ensemble" and len(digits):
+        # NEXT-1: the regression-simulator ensemble as the prior mean (R20);
+        # Unavailable -> the analytical simulator stays the prior
+        ens = _ens.Ensemble(space, digits, costs, int(space.gp.get("ensemble_seed", 0)))
+        if not ens.available:
+            ens = None
+    if ens is not None:
+        fit = _gp.fit_observed_prior(space, digits, costs, ens.predict(space, digits))
+    else:
+        fit = _gp.fit_observed(space, digits, costs, cs)
+    fit.ens = ens
+    return fit
 
 
 def evaluate(space, digits_list, fit, acq="ei", kappa=2.0, xi=0.0):
@@ -61,7 +74,8 @@ def evaluate(space, digits_list, fit, acq="ei", kappa=2.0, xi=0.0):
         rec["valid"] = np.zeros(0, dtype=bool)
         return rec
     cost, ok, mem = _sim.simulate(space, digits_list)
-    m0 = np.log(cost)
+    ens = getattr(fit, "ens", None)
+    m0 = ens.predict(space, digits_list) if ens is not None else np.log(cost)
     X = _gp.features(space, digits_list)
     mu, s2, _ = fit.posterior(X, m0)
     if acq == "ei":

@@ -59,6 +59,16 @@ class Feature:
     def n(self) -> int:
         return len(self.values)
 
+    def numeric(self, digit):
+        """Numeric encoding of a digit's value for the regression simulators (NEXT-1, reading
+        R20): numbers as themselves, booleans 0/1, strings by their domain index."""
+        v = self.values[digit]
+        if isinstance(v, bool):
+            return 1.0 if v else 0.0
+        if isinstance(v, str):
+            return float(digit)
+        return float(v)
+
 
 def _num(v):
     """Numeric view of a domain value: bools as 0/1 (S:452 'booleans as 0/1')."""

@@ -36,6 +36,7 @@ EXPORTS = ["autoscout_space_create", "autoscout_space_destroy", "autoscout_space
            "autoscout_topk_pool", "autoscout_topk_merge", "autoscout_decode", "autoscout_cvi_to_raw",
            "autoscout_sample_to_cvi", "autoscout_simulate", "autoscout_mask_range", "autoscout_set_path",
            "autoscout_set_timing", "autoscout_raw_to_cvi", "autoscout_subtree_range", "autoscout_neighbors",
+           "autoscout_prior", "autoscout_ensemble_info",
            "autoscout_last_kernel_ms", "autoscout_last_phase_ms", "autoscout_last_error"]
 
 
@@ -83,6 +84,8 @@ def _load():
         "autoscout_cvi_to_raw": ([P, U64, pU64], I32),
         "autoscout_sample_to_cvi": ([P, U64, U64, pU64], I32),
         "autoscout_raw_to_cvi": ([P, U64, pU64, pI32], I32),
+        "autoscout_prior": ([P, U64, pD, pI32], I32),
+        "autoscout_ensemble_info": ([P, pD, pD, pI32], I32),
         "autoscout_subtree_range": ([P, pI32, I32, pU64, pU64], I32),
         "autoscout_neighbors": ([P, U64, pU64, I32, pI32], I32),
         "autoscout_simulate": ([P, U64, pD, pD, pI32], I32),
@@ -184,6 +187,18 @@ class Space:
         r = ctypes.c_uint64()
         _check(_LIB.autoscout_cvi_to_raw(self.h, int(cvi), ctypes.byref(r)))
         return r.value
+
+    def prior(self, raw):
+        """-> (m0, source): GP prior mean of a configuration (source 1 = regression ensemble)."""
+        m, src = ctypes.c_double(), ctypes.c_int32()
+        _check(_LIB.autoscout_prior(self.h, int(raw), ctypes.byref(m), ctypes.byref(src)))
+        return m.value, int(src.value)
+
+    def ensemble_info(self):
+        """-> (r2[4], w[4], available) of the regression-simulator ensemble (NEXT-1)."""
+        r2, w, av = (ctypes.c_double * 4)(), (ctypes.c_double * 4)(), ctypes.c_int32()
+        _check(_LIB.autoscout_ensemble_info(self.h, r2, w, ctypes.byref(av)))
+        return list(r2), list(w), bool(av.value)
 
     def raw_to_cvi(self, raw):
         """-> (position, member): position of raw in the CVI if member, else #members below it."""
@@ -352,3 +367,11 @@ def autoscout_subtree_range(space, digits):
 
 def autoscout_neighbors(space, raw, cap=4096):
     return space.neighbors(raw, cap)
+
+
+def autoscout_prior(space, raw):
+    return space.prior(raw)
+
+
+def autoscout_ensemble_info(space):
+    return space.ensemble_info()

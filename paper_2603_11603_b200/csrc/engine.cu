@@ -170,6 +170,8 @@ struct as_space {
   std::vector<DV> obs_dv;
   std::vector<uint32_t> obs_act;
   GPFit fit;
+  EnsembleFit ens;                 // NEXT-1 regression-simulator ensemble (gp.prior = "ensemble")
+  double* d_ens_tab = nullptr;     // [DMAX * VMAX] its per-(feature, digit) table on the device
   DevGP G{};
   float *d_O = nullptr, *d_alpha = nullptr, *d_aabs = nullptr, *d_Wblk = nullptr;
   double *d_O64 = nullptr, *d_alpha64 = nullptr, *d_W64 = nullptr;
@@ -485,9 +487,10 @@ as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, b
   const int ci_n = by_bucket ? -1 : std::min(s->H.n_struct, GEN_CI_MAX);
   const size_t gen_smem = by_bucket ? (static_cast<size_t>(s->H.n_struct) + 1) * 8 + (s->D.n_bucket + 1) * 4
                                     : static_cast<size_t>(ci_n) * 8;
-  CUDA_TRY(cudaFuncSetAttribute(gen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gen_smem)));
+  auto gen_k = s->D.ens_on ? gen_kernel<true> : gen_kernel<false>;
+  CUDA_TRY(cudaFuncSetAttribute(gen_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gen_smem)));
   int occ = 1;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gen_kernel, GEN_THREADS, gen_smem));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gen_k, GEN_THREADS, gen_smem));
   const int grid_gen = s->n_sm * std::max(occ, 1);
   auto k2 = tc2_kernel_for(s->G.kernel, s->t2.nh);
   CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -502,7 +505,7 @@ as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, b
     if (nj > 0) {
       CUDA_TRY(cudaMemsetAsync(s->list.count, 0, sizeof(unsigned long long), st));
       if (ev) CUDA_TRY(cudaEventRecord(s->sev[s->sev_used], st));
-      gen_kernel<<<grid_gen, GEN_THREADS, gen_smem, st>>>(s->D, A, j0, nj, s->list, ci_n,
+      gen_k<<<grid_gen, GEN_THREADS, gen_smem, st>>>(s->D, A, j0, nj, s->list, ci_n,
                                                            reinterpret_cast<unsigned long long*>(s->d_valid));
       CUDA_TRY(cudaGetLastError());
       ++s->n_launches;
@@ -822,6 +825,9 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
     D.lg2 = p_lg2;
     D.xt64 = p_xt64;
     D.xt32 = p_xt32;
+    if ((r = dalloc(&s->d_ens_tab, static_cast<size_t>(DMAX) * VMAX, s->owned)) != AS_OK) return cleanup(r);
+    D.ens_tab = s->d_ens_tab;
+    D.ens_on = 0;
     // GP buffers at capacity
     const int Mc = MMAX, DPc = ((H.d + 3) / 4) * 4, nbc = Mc / 4;
     if ((r = dalloc(&s->d_O, static_cast<size_t>(Mc) * DPc, s->owned)) != AS_OK) return cleanup(r);
@@ -930,15 +936,32 @@ as_status autoscout_observe(as_space* s, const uint64_t* raw_idx, const double* 
   all_cost.insert(all_cost.end(), cost, cost + n);
   all_sim.insert(all_sim.end(), nsim.begin(), nsim.end());
   GPFit fit;
-  Status st = gp_fit(s->H, all_dv, all_act, all_cost, all_sim, fit);
+  EnsembleFit ens;
+  std::vector<double> m0_ens;
+  if (s->H.prior == 1) {
+    ensemble_fit(s->H, all_dv, all_cost, ens);
+    if (ens.on)
+      for (const DV& dv : all_dv) m0_ens.push_back(ensemble_m0(s->H, ens, dv));
+  }
+  Status st = gp_fit(s->H, all_dv, all_act, all_cost, all_sim, fit, ens.on ? &m0_ens : nullptr);
   if (!st.ok()) return fail(static_cast<as_status>(st.code), st.msg);
+  s->ens = std::move(ens);
+  if (s->device >= 0) {
+    if (s->ens.on) {
+      CUDA_TRY(cudaMemcpy(s->d_ens_tab, s->ens.tab.data(), s->ens.tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    s->D.ens_on = s->ens.on ? 1 : 0;
+    s->D.ens_c0 = s->ens.c0;
+  }
   s->obs_raw.insert(s->obs_raw.end(), raw_idx, raw_idx + n);
   s->obs_dv = std::move(all_dv);
   s->obs_act = std::move(all_act);
   s->obs_cost = std::move(all_cost);
   s->obs_sim = std::move(all_sim);
   s->fit = std::move(fit);
-  return upload_gp(s, static_cast<cudaStream_t>(cuda_stream));
+  const as_status ur = upload_gp(s, static_cast<cudaStream_t>(cuda_stream));
+  if (ur == AS_OK && s->ens.on) s->fit_upload_bytes += s->ens.tab.size() * sizeof(double);
+  return ur;
 }
 
 as_status autoscout_observe_clear(as_space* s) {
@@ -949,6 +972,8 @@ as_status autoscout_observe_clear(as_space* s) {
   s->obs_cost.clear();
   s->obs_sim.clear();
   gp_fit(s->H, {}, {}, {}, {}, s->fit);
+  s->ens = EnsembleFit{};
+  s->D.ens_on = 0;
   return upload_gp(s, nullptr);
 }
 
@@ -1091,6 +1116,35 @@ as_status autoscout_cvi_to_raw(const as_space* s, uint64_t cvi, uint64_t* raw_ou
   DV dv;
   uint32_t act;
   if (!cvi_decode(s->H, cvi, dv, act, *raw_out)) return fail(AS_ERR_INDEX_RANGE, "cvi >= n_cvi");
+  return AS_OK;
+}
+
+as_status autoscout_prior(const as_space* s, uint64_t raw, double* m0_out, int32_t* source_out) {
+  if (!s || !m0_out) return fail(AS_ERR_INVALID_ARG, "null argument");
+  int dig[DMAX];
+  DV dv;
+  uint32_t act;
+  bool structural;
+  if (!raw_decode(s->H, raw, dig, dv, act, structural)) return fail(AS_ERR_INDEX_RANGE, "raw >= n_raw");
+  if (s->ens.on) {
+    *m0_out = ensemble_m0(s->H, s->ens, dv);
+  } else {
+    double c, mem;
+    bool ok;
+    simulate_host(s->H, dv, act, c, ok, mem);
+    *m0_out = std::log(c);
+  }
+  if (source_out) *source_out = s->ens.on ? 1 : 0;
+  return AS_OK;
+}
+
+as_status autoscout_ensemble_info(const as_space* s, double* r2_out, double* w_out, int32_t* available_out) {
+  if (!s) return fail(AS_ERR_INVALID_ARG, "null argument");
+  for (int m = 0; m < 4; ++m) {
+    if (r2_out) r2_out[m] = s->ens.r2[m];
+    if (w_out) w_out[m] = s->ens.w[m];
+  }
+  if (available_out) *available_out = s->ens.on ? 1 : 0;
   return AS_OK;
 }
 

@@ -40,7 +40,27 @@ struct DevSpace {
   int comp_first[DMAX];
   int comp_width[DMAX];
   SimParams sim;
+  // GP prior mean (R9 / R20): ln cost_sim, or the regression-simulator ensemble (NEXT-1)
+  int ens_on;
+  double ens_c0;
+  const double* ens_tab;   // [d * VMAX]
 };
+
+// out of line: keeps the ensemble loop out of the register allocation of the hot kernels
+__device__ __noinline__ double ensemble_m0_dev(const double* tab, double c0, int d, uint64_t w0, uint64_t w1,
+                                               uint64_t w2) {
+  DV dv;
+  dv.w[0] = w0;
+  dv.w[1] = w1;
+  dv.w[2] = w2;
+  double m = c0;
+  for (int f = 0; f < d; ++f) m += __ldg(tab + f * VMAX + dv_get(dv, f));
+  return m;
+}
+__device__ __forceinline__ double prior_m0(const DevSpace& S, const DV& dv, double cost) {
+  if (!S.ens_on) return log(cost);
+  return ensemble_m0_dev(S.ens_tab, S.ens_c0, S.d, dv.w[0], dv.w[1], dv.w[2]);
+}
 
 struct DevGP {
   int M, Mp, DP, kernel;   // Mp: M padded to 4; DP: d padded to 4
@@ -489,7 +509,7 @@ score_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out) {
       decode_dev(S, pcvi, dv, act, raw);
       double cost;
       sim_dev(S, dv, act, cost, ok);
-      m0 = log(cost);
+      m0 = prior_m0(S, dv, cost);
       if (!pin) {
         ok = false;
         raw = ~0ull;
@@ -780,7 +800,7 @@ refine_kernel(DevSpace S, DevGP G, const uint64_t* pool, const int* pool_n, int 
   double cost;
   bool ok;
   sim_dev(S, dv, act, cost, ok);
-  const double m0 = log(cost);
+  const double m0 = prior_m0(S, dv, cost);
   double mu = m0 + G.b, s2 = G.sf2;
   if (G.M > 0 && acq != 2) {
     double kalpha, vsq;

@@ -27,6 +27,9 @@ struct CandList {
   unsigned long long* count;    // number of records
 };
 
+// ENS: GP prior mean from the regression-simulator ensemble (NEXT-1) instead of ln cost_sim; a
+// template parameter so the default instantiation carries no trace of it (register allocation)
+template <bool ENS>
 __global__ void __launch_bounds__(GEN_THREADS, 3)
 gen_kernel(DevSpace S, BatchArgs A, uint64_t j0, uint64_t nj, CandList L, int ci_n, unsigned long long* valid_total) {
   extern __shared__ __align__(16) uint64_t gen_cidx[];
@@ -78,7 +81,7 @@ gen_kernel(DevSpace S, BatchArgs A, uint64_t j0, uint64_t nj, CandList L, int ci
         const uint64_t slot = wbase + __popc(vb & ((1u << lane) - 1u));
         L.cvi[slot] = static_cast<uint32_t>(pcvi);
         L.j[slot] = static_cast<uint32_t>(j);
-        L.m0[slot] = log(cost);
+        L.m0[slot] = ENS ? ensemble_m0_dev(S.ens_tab, S.ens_c0, S.d, dv.w[0], dv.w[1], dv.w[2]) : log(cost);
         L.dv0[slot] = dv.w[0];
         L.dv1[slot] = dv.w[1];
         L.dv2[slot] = dv.w[2];

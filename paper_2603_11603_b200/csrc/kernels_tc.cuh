@@ -343,7 +343,7 @@ score_tc_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB) {
         if (ok) {
           const int slot = atomicAdd(&q_n, 1);
           sm.q_dv[slot] = dv;
-          sm.q_m0[slot] = log(cost);
+          sm.q_m0[slot] = prior_m0(S, dv, cost);
           sm.q_cvi[slot] = static_cast<uint32_t>(pcvi);
           sm.q_j[slot] = static_cast<uint32_t>(j);
         }

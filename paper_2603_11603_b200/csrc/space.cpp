@@ -639,6 +639,16 @@ Status build_space(const char* json, HostSpace& S) {
         return err(E_SCHEMA, "gp.onehot_max_width must be a non-negative integer");
       S.onehot_max = static_cast<int>(w->num);
     }
+    if (const asj::Value* pr = gp->get("prior")) {
+      if (pr->kind != asj::Value::String || (pr->str != "sim" && pr->str != "ensemble"))
+        return err(E_SCHEMA, "gp.prior must be sim|ensemble");
+      S.prior = pr->str == "ensemble" ? 1 : 0;
+    }
+    if (const asj::Value* es = gp->get("ensemble_seed")) {
+      if (es->kind != asj::Value::Number || !(es->num >= 0) || es->num != std::floor(es->num))
+        return err(E_SCHEMA, "gp.ensemble_seed must be a non-negative integer");
+      S.ens_seed = static_cast<uint64_t>(es->num);
+    }
   }
   for (double l : S.ls)
     if (!(l > 0)) return err(E_SCHEMA, "gp.lengthscale must be positive");
@@ -729,8 +739,165 @@ void simulate_host(const HostSpace& S, const DV& dv, uint32_t act, double& cost,
   simulate(S.sim, k, cost, ok, mem);
 }
 
+// ---------------------------------------------------------------- regression-simulator ensemble
+// NEXT-1; Appendix B Table 2 + weight equation, SPEC.md
+// fit_simulator / ensemble_predict; readings R20.
+namespace {
+const char* const kTable2[4][9] = {
+    {"a100", "a40", "mbs", "tp", "pp", "dp", nullptr},                       // 3D-Parallelism
+    {"a100", "a40", "mbs", "tp", "pp", "dp", "ep", "cp", "sp"},              // 5D-Parallelism
+    {"a100", "a40", "mbs", "tp", "pp", "dp", "ddp_optim", nullptr},          // DDP-Aware
+    {"a100", "a40", "mbs", "tp", "pp", "dp", "ar", "tp_comm", nullptr},      // Communication-Aware
+};
+
+std::vector<int> table2_columns(const HostSpace& S, int m) {
+  std::vector<int> cols;
+  for (int k = 0; k < 9 && kTable2[m][k]; ++k) {
+    const std::string knob = kTable2[m][k];
+    int f = -1;
+    if (knob == "ddp_optim") {
+      f = feature_index(S, "dopt");
+      if (f < 0) f = feature_index(S, "ddp");
+    } else {
+      f = feature_index(S, knob);
+    }
+    if (f >= 0 && std::find(cols.begin(), cols.end(), f) == cols.end()) cols.push_back(f);
+  }
+  std::sort(cols.begin(), cols.end());
+  return cols;
+}
+
+// (Z^T Z + 1e-6 I) g = Z^T (y - ybar) on standardised, non-constant columns (Cholesky)
+void ridge_fit(const std::vector<std::vector<double>>& X, const std::vector<double>& y, double& beta0,
+               std::vector<double>& beta) {
+  const size_t n = y.size(), p = X.empty() ? 0 : X[0].size();
+  double ybar = 0.0;
+  for (double v : y) ybar += v;
+  ybar /= static_cast<double>(n);
+  beta.assign(p, 0.0);
+  std::vector<double> mu(p, 0.0), sd(p, 0.0);
+  std::vector<int> keep;
+  for (size_t j = 0; j < p; ++j) {
+    for (size_t i = 0; i < n; ++i) mu[j] += X[i][j];
+    mu[j] /= static_cast<double>(n);
+    for (size_t i = 0; i < n; ++i) sd[j] += (X[i][j] - mu[j]) * (X[i][j] - mu[j]);
+    sd[j] = std::sqrt(sd[j] / static_cast<double>(n));
+    if (sd[j] > 1e-9 * std::fmax(1.0, std::fabs(mu[j]))) keep.push_back(static_cast<int>(j));
+  }
+  const size_t q = keep.size();
+  if (q > 0) {
+    std::vector<double> A(q * q, 0.0), r(q, 0.0);
+    for (size_t a = 0; a < q; ++a) {
+      for (size_t b = 0; b <= a; ++b) {
+        double acc = 0.0;
+        for (size_t i = 0; i < n; ++i)
+          acc += (X[i][keep[a]] - mu[keep[a]]) / sd[keep[a]] * ((X[i][keep[b]] - mu[keep[b]]) / sd[keep[b]]);
+        A[a * q + b] = A[b * q + a] = acc;
+      }
+      A[a * q + a] += 1e-6;
+      for (size_t i = 0; i < n; ++i) r[a] += (X[i][keep[a]] - mu[keep[a]]) / sd[keep[a]] * (y[i] - ybar);
+    }
+    for (size_t a = 0; a < q; ++a) {          // Cholesky A = L L^T in place (lower)
+      for (size_t b = 0; b <= a; ++b) {
+        double acc = A[a * q + b];
+        for (size_t c = 0; c < b; ++c) acc -= A[a * q + c] * A[b * q + c];
+        A[a * q + b] = (a == b) ? std::sqrt(acc) : acc / A[b * q + b];
+      }
+    }
+    std::vector<double> g(q);
+    for (size_t a = 0; a < q; ++a) {          // L z = r
+      double acc = r[a];
+      for (size_t c = 0; c < a; ++c) acc -= A[a * q + c] * g[c];
+      g[a] = acc / A[a * q + a];
+    }
+    for (size_t a = q; a-- > 0;) {            // L^T g = z
+      double acc = g[a];
+      for (size_t c = a + 1; c < q; ++c) acc -= A[c * q + a] * g[c];
+      g[a] = acc / A[a * q + a];
+    }
+    for (size_t a = 0; a < q; ++a) beta[keep[a]] = g[a] / sd[keep[a]];
+  }
+  beta0 = ybar;
+  for (size_t j = 0; j < p; ++j) beta0 -= beta[j] * mu[j];
+}
+}  // namespace
+
+void ensemble_fit(const HostSpace& S, const std::vector<DV>& dv, const std::vector<double>& cost, EnsembleFit& e) {
+  e = EnsembleFit{};
+  const int n = static_cast<int>(dv.size());
+  if (n == 0) return;
+  std::vector<double> y(n);
+  for (int i = 0; i < n; ++i) y[i] = std::log(cost[i]);
+  // seeded 80/20 split: holdout = the floor(n/5) (>= 1) smallest splitmix64(seed ^ 0xE45E ^ i)
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    return splitmix64(S.ens_seed ^ 0xE45Eull ^ static_cast<uint64_t>(a)) <
+           splitmix64(S.ens_seed ^ 0xE45Eull ^ static_cast<uint64_t>(b));
+  });
+  const int nh = std::max(1, n / 5);
+  std::vector<int> hold(order.begin(), order.begin() + std::min(nh, n)), train(order.begin() + std::min(nh, n), order.end());
+  std::sort(hold.begin(), hold.end());
+  std::sort(train.begin(), train.end());
+  auto x_of = [&](int i, int f) { return S.feat[f].num[dv_get(dv[i], f)]; };
+  double w_tot = 0.0;
+  std::vector<std::vector<double>> coef(4, std::vector<double>(S.d, 0.0));
+  double b0s[4] = {0, 0, 0, 0};
+  for (int m = 0; m < 4; ++m) {
+    const std::vector<int> cols = table2_columns(S, m);
+    e.r2[m] = -INFINITY;
+    if (static_cast<int>(train.size()) < static_cast<int>(cols.size()) + 2 || hold.empty()) continue;
+    std::vector<std::vector<double>> X(train.size(), std::vector<double>(cols.size()));
+    std::vector<double> yt(train.size());
+    for (size_t i = 0; i < train.size(); ++i) {
+      for (size_t j = 0; j < cols.size(); ++j) X[i][j] = x_of(train[i], cols[j]);
+      yt[i] = y[train[i]];
+    }
+    double b0;
+    std::vector<double> b;
+    ridge_fit(X, yt, b0, b);
+    // R^2 on the holdout; zero variance -> 0
+    double ym = 0.0, yy = 0.0;
+    for (int i : hold) {
+      ym += y[i];
+      yy += y[i] * y[i];
+    }
+    ym /= static_cast<double>(hold.size());
+    double sst = 0.0, ssr = 0.0;
+    for (int i : hold) {
+      double yh = b0;
+      for (size_t j = 0; j < cols.size(); ++j) yh += b[j] * x_of(i, cols[j]);
+      sst += (y[i] - ym) * (y[i] - ym);
+      ssr += (y[i] - yh) * (y[i] - yh);
+    }
+    e.r2[m] = (sst <= 1e-24 * yy) ? 0.0 : 1.0 - ssr / sst;
+    b0s[m] = b0;
+    for (size_t j = 0; j < cols.size(); ++j) coef[m][cols[j]] = b[j];
+    w_tot += std::fmax(0.0, e.r2[m]);
+  }
+  if (!(w_tot > 0.0)) return;   // Unavailable: the prior stays ln cost_sim
+  e.on = true;
+  e.c0 = 0.0;
+  std::vector<double> cf(S.d, 0.0);
+  for (int m = 0; m < 4; ++m) {
+    e.w[m] = std::fmax(0.0, e.r2[m]) / w_tot;
+    e.c0 += e.w[m] * b0s[m];
+    for (int f = 0; f < S.d; ++f) cf[f] += e.w[m] * coef[m][f];
+  }
+  e.tab.assign(static_cast<size_t>(S.d) * VMAX, 0.0);
+  for (int f = 0; f < S.d; ++f)
+    for (int v = 0; v < S.feat[f].n; ++v) e.tab[static_cast<size_t>(f) * VMAX + v] = cf[f] * S.feat[f].num[v];
+}
+
+double ensemble_m0(const HostSpace& S, const EnsembleFit& e, const DV& dv) {
+  double m = e.c0;
+  for (int f = 0; f < S.d; ++f) m += e.tab[static_cast<size_t>(f) * VMAX + dv_get(dv, f)];
+  return m;
+}
+
 Status gp_fit(const HostSpace& S, const std::vector<DV>& obs_dv, const std::vector<uint32_t>& obs_act,
-              const std::vector<double>& cost, const std::vector<double>& cost_sim, GPFit& fit) {
+              const std::vector<double>& cost, const std::vector<double>& cost_sim, GPFit& fit,
+              const std::vector<double>* m0_prior) {
   (void)obs_act;
   const int M = static_cast<int>(obs_dv.size());
   const int d = S.d;
@@ -742,7 +909,7 @@ Status gp_fit(const HostSpace& S, const std::vector<DV>& obs_dv, const std::vect
   for (int i = 0; i < M; ++i) {
     for (int j = 0; j < d; ++j) fit.X[i * d + j] = S.xt64[j * VMAX + dv_get(obs_dv[i], j)];
     y[i] = std::log(cost[i]);
-    m0[i] = std::log(cost_sim[i]);
+    m0[i] = m0_prior ? (*m0_prior)[i] : std::log(cost_sim[i]);
   }
   double sum = 0.0;
   for (int i = 0; i < M; ++i) sum += y[i] - m0[i];

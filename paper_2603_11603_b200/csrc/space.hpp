@@ -76,6 +76,8 @@ struct HostSpace {
   // GP hyper-parameters
   int kernel = 0;                 // 0 matern52, 1 rbf
   double sf2 = 0.1, sn2 = 1e-3, xi = 0.0, kappa = 2.0;
+  int prior = 0;                  // gp.prior: 0 "sim" (ln cost_sim, R9), 1 "ensemble" (NEXT-1, R20)
+  uint64_t ens_seed = 0;          // gp.ensemble_seed: holdout split of the regression simulators
   int onehot_max = 64;            // gp.onehot_max_width: one-hot r^2 width target of the TC kernel (impl. knob)
   std::vector<double> ls;
 };
@@ -100,6 +102,21 @@ struct GPFit {
   double w_fro = 0.0;           // ||L^-1||_F  (error bound of the FP32 screen)
 };
 Status gp_fit(const HostSpace& S, const std::vector<DV>& obs_dv, const std::vector<uint32_t>& obs_act,
-              const std::vector<double>& cost, const std::vector<double>& cost_sim, GPFit& fit);
+              const std::vector<double>& cost, const std::vector<double>& cost_sim, GPFit& fit,
+              const std::vector<double>* m0_prior = nullptr);
+
+// Regression-simulator ensemble (NEXT-1; reading R20): four ridge-stabilised
+// linear fits of ln c on the Table 2 knob subsets, R^2 on a seeded 20 % holdout, weights
+// max(0,R^2)/sum.  on = false when every R^2 <= 0 (Unavailable).  The weighted sum of linear
+// models is one linear model: m0(x) = c0 + sum_f tab[f][digit_f].
+struct EnsembleFit {
+  bool on = false;
+  double c0 = 0.0;
+  double r2[4] = {0, 0, 0, 0};
+  double w[4] = {0, 0, 0, 0};
+  std::vector<double> tab;        // [d * VMAX]
+};
+void ensemble_fit(const HostSpace& S, const std::vector<DV>& dv, const std::vector<double>& cost, EnsembleFit& e);
+double ensemble_m0(const HostSpace& S, const EnsembleFit& e, const DV& dv);
 
 }  // namespace as
