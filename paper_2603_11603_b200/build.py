@@ -50,7 +50,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         if force or _stale(o, [s] + hdrs):
-            log += _run(["g++", "-std=c++17", "-O2", "-fPIC", "-ffp-contract=off", "-fno-fast-math",
+            log += _run(["g++", "-std=c++17", "-O3", "-fPIC", "-ffp-contract=off", "-fno-fast-math",
                          "-I", "/usr/local/cuda/include", "-c", s, "-o", o], verbose)
         objs.append(o)
     for src in SOURCES_CU:

@@ -930,16 +930,25 @@ Status gp_fit(const HostSpace& S, const std::vector<DV>& obs_dv, const std::vect
       }
       L[i * M + j] = kernel64(S.kernel, S.sf2, r2) + (i == j ? S.sn2 : 0.0);
     }
-  for (int j = 0; j < M; ++j) {
-    double s = L[j * M + j];
-    for (int q = 0; q < j; ++q) s -= L[j * M + q] * L[j * M + q];
+  // Right-looking Cholesky: after column q is final, A[i][j] -= L[i][q] L[j][q] for q < j <= i.
+  // Each element still receives its updates in ascending q (the textbook left-looking order), so
+  // the result is identical; the update of row i runs unit-stride over j through Lt = L^T.
+  std::vector<double> Lt(static_cast<size_t>(M) * M, 0.0);
+  for (int q = 0; q < M; ++q) {
+    const double s = L[q * M + q];
     if (!(s > 0.0)) return err(E_NUM, "Cholesky of the GP covariance failed (not positive definite)");
-    const double ljj = std::sqrt(s);
-    L[j * M + j] = ljj;
-    for (int i = j + 1; i < M; ++i) {
-      double t = L[i * M + j];
-      for (int q = 0; q < j; ++q) t -= L[i * M + q] * L[j * M + q];
-      L[i * M + j] = t / ljj;
+    const double lqq = std::sqrt(s);
+    L[q * M + q] = lqq;
+    Lt[static_cast<size_t>(q) * M + q] = lqq;
+    for (int i = q + 1; i < M; ++i) {
+      L[i * M + q] /= lqq;
+      Lt[static_cast<size_t>(q) * M + i] = L[i * M + q];
+    }
+    const double* lq = Lt.data() + static_cast<size_t>(q) * M;
+    for (int i = q + 1; i < M; ++i) {
+      const double liq = L[i * M + q];
+      double* ai = L.data() + static_cast<size_t>(i) * M;
+      for (int j = q + 1; j <= i; ++j) ai[j] -= liq * lq[j];
     }
   }
   // alpha = L^-T L^-1 r
@@ -955,14 +964,21 @@ Status gp_fit(const HostSpace& S, const std::vector<DV>& obs_dv, const std::vect
     for (int q = i + 1; q < M; ++q) t -= L[q * M + i] * fit.alpha[q];
     fit.alpha[i] = t / L[i * M + i];
   }
-  // W = L^-1 (lower triangular), column by column
+  // W = L^-1 (lower triangular), row by row: W[i][c] = (delta_ic - sum_{q=c}^{i-1} L[i][q] W[q][c]) / L[i][i].
+  // The sum is accumulated for all c of the row at once (axpy over the contiguous row W[q][0..q],
+  // q ascending): the same operations in the same order per element as the column-by-column
+  // form, but unit-stride and vectorisable.
   fit.Wl.assign(static_cast<size_t>(M) * M, 0.0);
-  for (int c = 0; c < M; ++c) {
-    for (int i = c; i < M; ++i) {
-      double t = (i == c) ? 1.0 : 0.0;
-      for (int q = c; q < i; ++q) t -= L[i * M + q] * fit.Wl[q * M + c];
-      fit.Wl[i * M + c] = t / L[i * M + i];
+  std::vector<double> t(M);
+  for (int i = 0; i < M; ++i) {
+    for (int c = 0; c <= i; ++c) t[c] = (c == i) ? 1.0 : 0.0;
+    for (int q = 0; q < i; ++q) {
+      const double liq = L[i * M + q];
+      const double* wq = fit.Wl.data() + static_cast<size_t>(q) * M;
+      for (int c = 0; c <= q; ++c) t[c] -= liq * wq[c];
     }
+    const double lii = L[i * M + i];
+    for (int c = 0; c <= i; ++c) fit.Wl[static_cast<size_t>(i) * M + c] = t[c] / lii;
   }
   double fro = 0.0;
   for (double w : fit.Wl) fro += w * w;
