@@ -144,6 +144,25 @@ as_status autoscout_topk_merge(const as_space* s, const void* pools, const int32
 as_status autoscout_decode(const as_space* s, uint64_t raw, int32_t* digits_out, int32_t* valid_out);
 as_status autoscout_cvi_to_raw(const as_space* s, uint64_t cvi, uint64_t* raw_out);
 as_status autoscout_sample_to_cvi(const as_space* s, uint64_t seed, uint64_t ordinal, uint64_t* cvi_out);
+/* ML-II evidence of GP hyper-parameter settings, batched on the device (
+ * the paper fixes no surrogate and no hyper-parameters, R1, R21).  hyp: host,
+ * n_set x (d + 2) doubles per setting [lengthscale_0 .. lengthscale_{d-1}, sf2, sn2], all > 0.
+ * lml_out: host, n_set log marginal likelihoods of the current observed residuals
+ * r = y - m0 - b under N(0, k(x_i, x_j) + sn2 I) (the kernel of the space), -INF where the matrix is
+ * not positive definite.  Synchronous on cuda_stream.  AS_ERR_NO_OBSERVATIONS with M = 0,
+ * AS_ERR_STATE on a host-only handle, AS_ERR_INVALID_ARG for a non-positive entry. */
+as_status autoscout_gp_lml(as_space* s, const double* hyp, int32_t n_set, double* lml_out, void* cuda_stream);
+/* Replace the GP hyper-parameters (lengthscale: d host doubles; sf2, sn2 > 0) and refit the
+ * current observed set under them (as observe_clear + observe of the same observations). */
+as_status autoscout_set_gp_hyper(as_space* s, const double* lengthscale, double sf2, double sn2);
+/* ML-II by batched evidence (R21): setting 0 = the current hyper-parameters, settings
+ * 1..n_set-1 drawn log-uniformly (lengthscales in [0.1, 10], sf2 in [1e-3, 10], sn2/sf2 in
+ * [1e-6, 1e-1]) from counter-based splitmix64(seed ^ 0x3111 ^ (64 h + k)) uniforms; all evaluated
+ * by autoscout_gp_lml in one launch; the best (lowest index on ties) is returned through
+ * best_hyp_out (host, d + 2, nullable), best_lml_out, best_index_out and, if apply != 0, set with
+ * autoscout_set_gp_hyper. */
+as_status autoscout_ml2(as_space* s, int32_t n_set, uint64_t seed, int32_t apply, double* best_hyp_out,
+                        double* best_lml_out, int32_t* best_index_out, void* cuda_stream);
 /* GP prior mean m0 of a configuration under the current fit (host, FP64; R9, R20):
  * source_out = 1 if it is the regression-simulator ensemble (space JSON gp.prior = "ensemble"
  * and at least one simulator with holdout R^2 > 0 after the last observe; SURVEY.md §8(f) NEXT-1,

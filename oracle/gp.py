@@ -123,3 +123,47 @@ def fit_observed_prior(space, digits_list, cost_obs, m0_obs):
     """observe() with an explicit prior mean at the observed points (NEXT-1 ensemble, R20)."""
     O = features(space, digits_list) if len(digits_list) else np.zeros((0, len(space.features)))
     return Fit(space, O, np.log(np.asarray(cost_obs, dtype=np.float64)), np.asarray(m0_obs, dtype=np.float64))
+
+
+# ---------------------------------------------------------------- NEXT-4: ML-II evidence (reading R21)
+def phi_matrix(space, digits_list):
+    """phi_j = effective digit / (n_j - 1) of each observed configuration (lengthscale-free)."""
+    P = np.zeros((len(digits_list), len(space.features)), dtype=np.float64)
+    for b, dg in enumerate(digits_list):
+        act = space.activity(dg)
+        for j, f in enumerate(space.features):
+            de = dg[j] if act[j] else f.default_digit
+            P[b, j] = de / (f.n - 1) if f.n > 1 else 0.0
+    return P
+
+
+def log_marginal_likelihood(space, P, res, ls, sf2, sn2):
+    """ln N(res; 0, K) with K_ij = k(||(phi_i - phi_j) / l||) + sn2 delta_ij (the definition:
+    -1/2 res^T K^-1 res - 1/2 ln det K - M/2 ln 2 pi, by numpy slogdet and solve)."""
+    X = P / np.asarray(ls, dtype=np.float64)[None, :]
+    diff = X[:, None, :] - X[None, :, :]
+    r = np.sqrt(np.sum(diff * diff, axis=2))
+    kind = space.gp.get("kernel", "matern52")
+    if kind == "matern52":
+        K = sf2 * (1.0 + SQRT5 * r + (5.0 / 3.0) * r * r) * np.exp(-SQRT5 * r)
+    else:
+        K = sf2 * np.exp(-0.5 * r * r)
+    K = K + sn2 * np.eye(len(res))
+    sign, logdet = np.linalg.slogdet(K)
+    if sign <= 0:
+        return -math.inf
+    return float(-0.5 * res @ np.linalg.solve(K, res) - 0.5 * logdet - 0.5 * len(res) * math.log(2 * math.pi))
+
+
+def ml2_candidate(space, seed, h, ls0, sf20, sn20):
+    """ML-II search point h (R21): h = 0 the current setting; else log-uniform draws from the
+    counter-based uniforms u_k = (splitmix64(seed ^ 0x3111 ^ (64 h + k)) >> 11) * 2^-53."""
+    from .feistel import splitmix64
+    d = len(space.features)
+    if h == 0:
+        return np.concatenate([np.asarray(ls0, dtype=np.float64), [sf20, sn20]])
+    u = [(splitmix64(seed ^ 0x3111 ^ (64 * h + k)) >> 11) * 2.0 ** -53 for k in range(d + 2)]
+    ls = [math.exp(math.log(0.1) + u[j] * math.log(100.0)) for j in range(d)]
+    sf2 = math.exp(math.log(1e-3) + u[d] * math.log(1e4))
+    sn2 = sf2 * math.exp(math.log(1e-6) + u[d + 1] * math.log(1e5))
+    return np.array(ls + [sf2, sn2])

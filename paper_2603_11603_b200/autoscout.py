@@ -36,7 +36,8 @@ EXPORTS = ["autoscout_space_create", "autoscout_space_destroy", "autoscout_space
            "autoscout_topk_pool", "autoscout_topk_merge", "autoscout_decode", "autoscout_cvi_to_raw",
            "autoscout_sample_to_cvi", "autoscout_simulate", "autoscout_mask_range", "autoscout_set_path",
            "autoscout_set_timing", "autoscout_raw_to_cvi", "autoscout_subtree_range", "autoscout_neighbors",
-           "autoscout_prior", "autoscout_ensemble_info",
+           "autoscout_prior", "autoscout_ensemble_info", "autoscout_gp_lml", "autoscout_set_gp_hyper",
+           "autoscout_ml2",
            "autoscout_last_kernel_ms", "autoscout_last_phase_ms", "autoscout_last_error"]
 
 
@@ -85,6 +86,9 @@ def _load():
         "autoscout_sample_to_cvi": ([P, U64, U64, pU64], I32),
         "autoscout_raw_to_cvi": ([P, U64, pU64, pI32], I32),
         "autoscout_prior": ([P, U64, pD, pI32], I32),
+        "autoscout_gp_lml": ([P, pD, I32, pD, P], I32),
+        "autoscout_set_gp_hyper": ([P, pD, D, D], I32),
+        "autoscout_ml2": ([P, I32, U64, I32, pD, pD, pI32, P], I32),
         "autoscout_ensemble_info": ([P, pD, pD, pI32], I32),
         "autoscout_subtree_range": ([P, pI32, I32, pU64, pU64], I32),
         "autoscout_neighbors": ([P, U64, pU64, I32, pI32], I32),
@@ -187,6 +191,31 @@ class Space:
         r = ctypes.c_uint64()
         _check(_LIB.autoscout_cvi_to_raw(self.h, int(cvi), ctypes.byref(r)))
         return r.value
+
+    def gp_lml(self, hyp, stream=None):
+        """Log marginal likelihoods of hyper-parameter settings hyp [n, d + 2] (NEXT-4)."""
+        hyp = np.ascontiguousarray(hyp, dtype=np.float64)
+        n = hyp.shape[0]
+        out = np.zeros(max(n, 1))
+        _check(_LIB.autoscout_gp_lml(self.h, hyp.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), n,
+                                     out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _stream_ptr(stream)))
+        return out[:n]
+
+    def set_gp_hyper(self, lengthscale, sf2, sn2):
+        ls = np.ascontiguousarray(lengthscale, dtype=np.float64)
+        _check(_LIB.autoscout_set_gp_hyper(self.h, ls.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                           float(sf2), float(sn2)))
+        self.info = self.space_info()
+
+    def ml2(self, n_set=1024, seed=0, apply=True, stream=None):
+        """-> (best hyper-parameters [d + 2], best lml, best index) of a batched ML-II search."""
+        best = np.zeros(self.d + 2)
+        lml, idx = ctypes.c_double(), ctypes.c_int32()
+        _check(_LIB.autoscout_ml2(self.h, int(n_set), int(seed), 1 if apply else 0,
+                                  best.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(lml),
+                                  ctypes.byref(idx), _stream_ptr(stream)))
+        self.info = self.space_info()
+        return best, lml.value, idx.value
 
     def prior(self, raw):
         """-> (m0, source): GP prior mean of a configuration (source 1 = regression ensemble)."""
@@ -375,3 +404,15 @@ def autoscout_prior(space, raw):
 
 def autoscout_ensemble_info(space):
     return space.ensemble_info()
+
+
+def autoscout_gp_lml(space, hyp, stream=None):
+    return space.gp_lml(hyp, stream)
+
+
+def autoscout_set_gp_hyper(space, lengthscale, sf2, sn2):
+    return space.set_gp_hyper(lengthscale, sf2, sn2)
+
+
+def autoscout_ml2(space, n_set=1024, seed=0, apply=True, stream=None):
+    return space.ml2(n_set, seed, apply, stream)

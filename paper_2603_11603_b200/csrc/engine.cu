@@ -14,6 +14,7 @@
 #include "kernels.cuh"
 #include "kernels_tc.cuh"
 #include "kernels_tc2.cuh"
+#include "kernels_lml.cuh"
 #include "space.hpp"
 
 using namespace as;
@@ -1116,6 +1117,120 @@ as_status autoscout_cvi_to_raw(const as_space* s, uint64_t cvi, uint64_t* raw_ou
   DV dv;
   uint32_t act;
   if (!cvi_decode(s->H, cvi, dv, act, *raw_out)) return fail(AS_ERR_INDEX_RANGE, "cvi >= n_cvi");
+  return AS_OK;
+}
+
+// ---------------------------------------------------------------- NEXT-4: ML-II evidence on the device
+as_status autoscout_gp_lml(as_space* s, const double* hyp, int32_t n_set, double* lml_out, void* cuda_stream) {
+  if (!s || (n_set > 0 && (!hyp || !lml_out)) || n_set < 0) return fail(AS_ERR_INVALID_ARG, "bad arguments");
+  if (s->device < 0) return fail(AS_ERR_STATE, "host-only handle cannot launch (no CUDA device)");
+  const int M = s->fit.M, d = s->H.d;
+  if (M == 0) return fail(AS_ERR_NO_OBSERVATIONS, "the evidence needs observations");
+  for (int64_t i = 0; i < static_cast<int64_t>(n_set) * (d + 2); ++i)
+    if (!(hyp[i] > 0.0) || !std::isfinite(hyp[i])) return fail(AS_ERR_INVALID_ARG, "hyper-parameters must be finite and > 0");
+  if (n_set == 0) return AS_OK;
+  CUDA_TRY(cudaSetDevice(s->device));
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  std::vector<double> phi(static_cast<size_t>(M) * d);
+  for (int i = 0; i < M; ++i)
+    for (int j = 0; j < d; ++j) {
+      const int n = s->H.feat[j].n;
+      phi[static_cast<size_t>(i) * d + j] = n > 1 ? double(dv_get(s->obs_dv[i], j)) / double(n - 1) : 0.0;
+    }
+  const int grid = std::min<int>(n_set, s->n_sm * 2);
+  const size_t work = static_cast<size_t>(grid) * M * M;
+  double *d_phi = nullptr, *d_r = nullptr, *d_hyp = nullptr, *d_out = nullptr, *d_work = nullptr;
+  auto release = [&]() {
+    cudaFree(d_phi);
+    cudaFree(d_r);
+    cudaFree(d_hyp);
+    cudaFree(d_out);
+    cudaFree(d_work);
+  };
+  cudaError_t e = cudaMalloc(&d_phi, phi.size() * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&d_r, static_cast<size_t>(M) * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&d_hyp, static_cast<size_t>(n_set) * (d + 2) * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&d_out, static_cast<size_t>(n_set) * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&d_work, work * 8);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_phi, phi.data(), phi.size() * 8, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_r, s->fit.r.data(), static_cast<size_t>(M) * 8, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_hyp, hyp, static_cast<size_t>(n_set) * (d + 2) * 8, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    lml_kernel<<<grid, LML_THREADS, (2 * static_cast<size_t>(M) + d) * sizeof(double), st>>>(
+        d_phi, d_r, M, d, s->H.kernel, d_hyp, n_set, d_work, d_out);
+    e = cudaGetLastError();
+    ++s->n_launches;
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(lml_out, d_out, static_cast<size_t>(n_set) * 8, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  release();
+  if (e != cudaSuccess) return fail(AS_ERR_CUDA, std::string("gp_lml: ") + cudaGetErrorString(e));
+  return AS_OK;
+}
+
+as_status autoscout_set_gp_hyper(as_space* s, const double* lengthscale, double sf2, double sn2) {
+  if (!s || !lengthscale) return fail(AS_ERR_INVALID_ARG, "null argument");
+  for (int j = 0; j < s->H.d; ++j)
+    if (!(lengthscale[j] > 0.0) || !std::isfinite(lengthscale[j])) return fail(AS_ERR_INVALID_ARG, "lengthscale must be > 0");
+  if (!(sf2 > 0.0) || !(sn2 > 0.0) || !std::isfinite(sf2) || !std::isfinite(sn2))
+    return fail(AS_ERR_INVALID_ARG, "sf2 and sn2 must be finite and > 0");
+  s->H.ls.assign(lengthscale, lengthscale + s->H.d);
+  s->H.sf2 = sf2;
+  s->H.sn2 = sn2;
+  feature_tables(s->H);
+  if (s->device >= 0) {
+    CUDA_TRY(cudaSetDevice(s->device));
+    CUDA_TRY(cudaMemcpy(const_cast<double*>(s->D.xt64), s->H.xt64.data(), s->H.xt64.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(const_cast<float*>(s->D.xt32), s->H.xt32.data(), s->H.xt32.size() * sizeof(float), cudaMemcpyHostToDevice));
+  }
+  // refit the current observed set under the new hyper-parameters
+  const std::vector<uint64_t> raws = s->obs_raw;
+  const std::vector<double> costs = s->obs_cost;
+  as_status r = autoscout_observe_clear(s);
+  if (r != AS_OK || raws.empty()) return r;
+  return autoscout_observe(s, raws.data(), costs.data(), static_cast<int64_t>(raws.size()), nullptr);
+}
+
+namespace {
+// ML-II candidate h (R21): h = 0 is the current setting; h > 0 draws every coordinate
+// log-uniformly from counter-based uniforms u = (splitmix64(seed ^ 0x3111 ^ (64 h + k)) >> 11) 2^-53:
+// l_j in [0.1, 10], sf2 in [1e-3, 10], sn2 / sf2 in [1e-6, 1e-1].
+void ml2_candidate(const HostSpace& H, uint64_t seed, int h, double* out) {
+  const int d = H.d;
+  if (h == 0) {
+    for (int j = 0; j < d; ++j) out[j] = H.ls[j];
+    out[d] = H.sf2;
+    out[d + 1] = H.sn2;
+    return;
+  }
+  auto u = [&](int k) {
+    return static_cast<double>(splitmix64(seed ^ 0x3111ull ^ (64ull * static_cast<uint64_t>(h) + static_cast<uint64_t>(k))) >> 11) *
+           0x1.0p-53;
+  };
+  for (int j = 0; j < d; ++j) out[j] = std::exp(std::log(0.1) + u(j) * std::log(100.0));
+  out[d] = std::exp(std::log(1e-3) + u(d) * std::log(1e4));
+  out[d + 1] = out[d] * std::exp(std::log(1e-6) + u(d + 1) * std::log(1e5));
+}
+}  // namespace
+
+as_status autoscout_ml2(as_space* s, int32_t n_set, uint64_t seed, int32_t apply, double* best_hyp_out,
+                        double* best_lml_out, int32_t* best_index_out, void* cuda_stream) {
+  if (!s || n_set < 1) return fail(AS_ERR_INVALID_ARG, "n_set must be >= 1");
+  const int d = s->H.d;
+  std::vector<double> hyp(static_cast<size_t>(n_set) * (d + 2)), lml(n_set);
+  for (int h = 0; h < n_set; ++h) ml2_candidate(s->H, seed, h, hyp.data() + static_cast<size_t>(h) * (d + 2));
+  as_status r = autoscout_gp_lml(s, hyp.data(), n_set, lml.data(), cuda_stream);
+  if (r != AS_OK) return r;
+  int best = 0;
+  for (int h = 1; h < n_set; ++h)
+    if (lml[h] > lml[best]) best = h;          // ties / NaN: the lowest index stays
+  if (best_hyp_out) std::copy(hyp.begin() + static_cast<size_t>(best) * (d + 2), hyp.begin() + static_cast<size_t>(best + 1) * (d + 2), best_hyp_out);
+  if (best_lml_out) *best_lml_out = lml[best];
+  if (best_index_out) *best_index_out = best;
+  if (apply && best != 0) {
+    const double* b = hyp.data() + static_cast<size_t>(best) * (d + 2);
+    return autoscout_set_gp_hyper(s, b, b[d], b[d + 1]);
+  }
   return AS_OK;
 }
 

@@ -653,6 +653,11 @@ Status build_space(const char* json, HostSpace& S) {
   for (double l : S.ls)
     if (!(l > 0)) return err(E_SCHEMA, "gp.lengthscale must be positive");
   if (!(S.sf2 > 0) || !(S.sn2 > 0)) return err(E_SCHEMA, "gp.sf2 and gp.sn2 must be positive");
+  feature_tables(S);
+  return Status{};
+}
+
+void feature_tables(HostSpace& S) {
   S.xt64.assign(static_cast<size_t>(S.d) * VMAX, 0.0);
   S.xt32.assign(static_cast<size_t>(S.d) * VMAX, 0.0f);
   for (int j = 0; j < S.d; ++j)
@@ -661,7 +666,6 @@ Status build_space(const char* json, HostSpace& S) {
       S.xt64[j * VMAX + v] = phi / S.ls[j];
       S.xt32[j * VMAX + v] = static_cast<float>(phi / S.ls[j]);
     }
-  return Status{};
 }
 
 bool cvi_decode(const HostSpace& S, uint64_t p, DV& dv, uint32_t& act, uint64_t& raw) {
@@ -919,6 +923,7 @@ Status gp_fit(const HostSpace& S, const std::vector<DV>& obs_dv, const std::vect
     r[i] = (y[i] - m0[i]) - fit.b;
     fit.fstar = std::fmin(fit.fstar, y[i]);
   }
+  fit.r = r;
   // K = k(o_i, o_j) + sn2 I ; Cholesky K = L L^T
   std::vector<double> L(static_cast<size_t>(M) * M, 0.0);
   for (int i = 0; i < M; ++i)

@@ -83,6 +83,7 @@ struct HostSpace {
 };
 
 Status build_space(const char* json, HostSpace& S);
+void feature_tables(HostSpace& S);   // x~ = phi / l tables from S.ls (after a lengthscale change)
 
 // Exact host introspection.
 void activity(const HostSpace& S, const int* dig, bool* act);
@@ -98,6 +99,7 @@ struct GPFit {
   double b = 0.0, fstar = INFINITY;
   std::vector<double> X;        // [M][d] x~ of observed
   std::vector<double> alpha;    // [M] K^-1 r
+  std::vector<double> r;        // [M] residual y - m0 - b (the GP's observations; ML-II evidence)
   std::vector<double> Wl;       // [M][M] L^-1 (lower triangular, row-major)
   double w_fro = 0.0;           // ||L^-1||_F  (error bound of the FP32 screen)
 };
