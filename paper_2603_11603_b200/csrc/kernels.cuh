@@ -319,7 +319,9 @@ __device__ __forceinline__ void posterior64_warp(const DevSpace& S, const DevGP&
 // ---- FP32 acquisition for the screen (the upper bound adds acq32_margin; the refine is FP64)
 __device__ __forceinline__ float lnh_f(float z) {
   if (z >= -10.0f) {
-    const float phi = __expf(-0.5f * z * z) * 0.3989422804014327f;
+    // expf (<= 2 ulp), not __expf: its 2 + 1.17 |x| ulp error, amplified ~z^2 by the phi + z Phi
+    // cancellation for z < 0, would exceed the screen margin 1e-6 (1 + z^2) below z ~ -6
+    const float phi = expf(-0.5f * z * z) * 0.3989422804014327f;
     const float Phi = 0.5f * erfcf(-z * 0.7071067811865476f);
     return logf(fmaf(z, Phi, phi));
   }
