@@ -208,8 +208,9 @@ as_status autoscout_simulate(const as_space* s, uint64_t raw, double* cost_out, 
 as_status autoscout_mask_range(as_space* s, uint64_t raw_begin, uint64_t count, uint32_t* d_bits,
                                uint64_t* d_valid_count, void* cuda_stream);
 
-/* Posterior path of the score kernel: 0 = auto (when M >= 64: the one-hot tensor-core kernel if
- * its shared memory fits, else the SIMT-r^2 tensor-core kernel; SIMT FP32 kernel below M = 64),
+/* Posterior path of the score kernel: 0 = auto (the one-hot tensor-core kernel if its shared memory
+ * fits and M >= 64 or the batch has >= 2^20 candidates; else, for M >= 64, the SIMT-r^2 tensor-core
+ * kernel; else the fused SIMT FP32 kernel),
  * 1 = force SIMT, 2 = force tensor cores with r^2 on the SIMT pipes (3xTF32 L^-1 k),
  * 3 = force tensor cores for both r^2 (one-hot FP16 contraction) and L^-1 k.  All compute the
  * same quantities; the override exists for A/B parity tests and

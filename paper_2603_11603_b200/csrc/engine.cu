@@ -537,7 +537,11 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
   int P = next_pow2_h(s->KC + SCORE_THREADS);
   const int P_tc2 = next_pow2_h(s->KC + 4 * TC_ROWS);   // lazy admission: room for >= 3 tiles before a prune
   const bool tc2_fits = tc2_smem_bytes(s->tb.Mp16, s->t2.Kp, s->t2.nh, P_tc2) <= static_cast<size_t>(s->smem_optin);
-  const bool use_tc2 = gp && (s->path == 3 || (s->path == 0 && s->G.M >= 64 && tc2_fits && s->tc2_auto));
+  // auto: the one-hot tensor-core kernel for M >= 64, and below that for large batches too (its
+  // generation split beats the fused SIMT kernel there: C4, M = 48, 10^8 candidates 38.5 -> 15.3 ms;
+  // small batches keep the single-launch SIMT kernel for latency)
+  const bool big = a.count >= (1ull << 20);
+  const bool use_tc2 = gp && (s->path == 3 || (s->path == 0 && (s->G.M >= 64 || big) && tc2_fits && s->tc2_auto));
   const bool use_tc = !use_tc2 && gp && (s->path == 2 || (s->path == 0 && s->G.M >= 64));
   size_t smem = 0;
   if (use_tc2) {

@@ -279,6 +279,13 @@ VARIANTS = [
     ("C2", {"onehot_max_width": 0, "kernel": "rbf"}, 80, "range", 0, None),
     ("C5", {"lengthscale": [0.3 + 0.1 * (j % 7) for j in range(16)]}, 128, "range", 2_000_000, 40000),
     ("C4", {"onehot_max_width": 40, "sf2": 0.5, "sn2": 0.01}, 96, "sample", 0, 30000),
+    # the one-hot kernel below M = 64 (auto path for large batches): one R2 group,
+    # fewer chunks than A-ring stages, ragged Mp16
+    ("C4", {}, 48, "sample", 0, 30000),
+    ("C1", {}, 16, "range", 0, None),
+    ("C3", {}, 32, "range", 0, None),
+    ("C2", {}, 17, "range", 0, None),
+    ("C2", {"kernel": "rbf"}, 5, "range", 10000, 20000),
 ]
 
 
