@@ -318,3 +318,28 @@ def test_tc2_variants(base, gp, M, mode, begin, count):
     ok = ei_tolerance_ok(sc[v].astype(np.float64), ref[v], rec["mu"][v], rec["s2"][v], fit.fstar, fit.sf2)
     assert ok.all(), f"{(~ok).sum()} EI values out of tolerance"
     check_topk(top, oracle_topk(rec, ref, 32))
+
+
+@pytest.mark.parametrize("name,M,mode,count,seed", [("C2", 64, "range", None, 0), ("C4", 256, "sample", 2_000_000, 4),
+                                                  ("C4", 48, "sample", 2_000_000, 6), ("C5", 128, "range", None, 0)])
+def test_topk_without_per_candidate_outputs(name, M, mode, count, seed):
+    """The certified top-k without per-candidate outputs (the bench's call) equals the one with
+    d_scores (which also runs the FP64 sensitive-row path), and on C2 the oracle's."""
+    o = oracle_space(name)
+    raws, costs = observed(o, M, 0)
+    sp = A.Space(space_path(name), 0)
+    sp.observe(raws, costs)
+    n = o.n_cvi() if count is None else count
+    sp.score_batch(mode=mode, begin=0, count=n, seed=seed, acq="ei", k=32)
+    fast = sp.topk(32)
+    sc = torch.empty(n, dtype=torch.float32, device="cuda")
+    sp.score_batch(mode=mode, begin=0, count=n, seed=seed, acq="ei", k=32, d_scores=sc)
+    exact = sp.topk(32)
+    torch.cuda.synchronize()
+    assert [r for r, _ in fast] == [r for r, _ in exact]
+    for (_, a), (_, b) in zip(fast, exact):
+        assert a == b
+    if name == "C2":
+        fit = run.observed_fit(o, raws, costs)
+        rec = run.score_batch(o, fit, "range", 0, n, acq="ei")
+        check_topk(fast, run.topk(rec, 32))
