@@ -43,7 +43,7 @@ constexpr size_t TC2_O_ALPHA = TC2_O_BARS + 64 * 8;
 constexpr size_t TC2_O_OH = TC2_O_ALPHA + 2 * MMAX * 4;
 constexpr size_t TC2_O_MXH = TC2_O_OH + 4 * MMAX * 4;
 constexpr size_t TC2_O_MPART = TC2_O_MXH + 4 * TC_TI * TC_ROWS * 4;
-constexpr size_t TC2_O_VPART = TC2_O_MPART + TC_TI * 3 * TC_ROWS * 4;
+constexpr size_t TC2_O_VPART = TC2_O_MPART + TC_TI * 4 * 3 * TC_ROWS * 4;   // [TI][jq][3][128]: one slot per thread
 constexpr size_t TC2_O_MCVI = TC2_O_VPART + 4 * TC_ROWS * 4;
 constexpr size_t TC2_O_MJ = TC2_O_MCVI + TC_TI * TC_ROWS * 4;
 constexpr size_t TC2_O_MM0 = TC2_O_MJ + TC_TI * TC_ROWS * 4;
@@ -262,11 +262,15 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       bool sensitive = false;
       if (pt < TC_ROWS && pt < n) {
         const int row = pt;
-        const float* mp = m_part + us * 3 * TC_ROWS;
-        const float mu32 = mp[0 * TC_ROWS + row], sb = mp[1 * TC_ROWS + row], kk = mp[2 * TC_ROWS + row];
-        float vv = 0.f;
+        float mu32 = 0.f, sb = 0.f, kk = 0.f, vv = 0.f;
 #pragma unroll
-        for (int q = 0; q < TC_JQ; ++q) vv += vpart[q * TC_ROWS + row];
+        for (int q = 0; q < TC_JQ; ++q) {
+          const float* mp = m_part + (us * TC_JQ + q) * 3 * TC_ROWS;
+          mu32 += mp[row];
+          sb += mp[TC_ROWS + row];
+          kk += mp[2 * TC_ROWS + row];
+          vv += vpart[q * TC_ROWS + row];
+        }
         const double cm0 = m_m0[us * TC_ROWS + row];
         const float mu = static_cast<float>(cm0 + G.b) + mu32;
         const float vs = vv;
@@ -341,12 +345,6 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         n = static_cast<int>(n_list - r0 < TC_ROWS ? n_list - r0 : TC_ROWS);
         const unsigned char* sg = stg + (u & 1) * TC2_STG_BYTES;
         tc::mbar_wait(s_full + (u & 1), (u >> 1) & 1);
-        if (pt < TC_ROWS) {
-          float* mz = m_part + us * 3 * TC_ROWS;
-          mz[pt] = 0.f;
-          mz[TC_ROWS + pt] = 0.f;
-          mz[2 * TC_ROWS + pt] = 0.f;
-        }
         if (pt < n) {
           m_cvi[us * TC_ROWS + pt] = reinterpret_cast<const uint32_t*>(sg + TC2_STG_CVI)[pt];
           m_j[us * TC_ROWS + pt] = reinterpret_cast<const uint32_t*>(sg + TC2_STG_J)[pt];
@@ -519,10 +517,11 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     auto flush_part = [&](int u, unsigned long long mu2, unsigned long long sb2, unsigned long long kk2) {
       const float2 m_ = f2_unpack(mu2), s_ = f2_unpack(sb2), k_ = f2_unpack(kk2);
       const float mu_p = m_.x + m_.y, sb_p = s_.x + s_.y, kk_p = k_.x + k_.y;
-      float* mp = m_part + (u % TC_TI) * 3 * TC_ROWS;
-      atomicAdd(mp + cand, mu_p * T2.k_unscale);
-      atomicAdd(mp + TC_ROWS + cand, sb_p * T2.k_unscale);
-      atomicAdd(mp + 2 * TC_ROWS + cand, kk_p * (T2.k_unscale * T2.k_unscale));
+      // each thread owns its slot (no atomics: the four quarters of a candidate used to contend)
+      float* mp = m_part + ((u % TC_TI) * TC_JQ + jq) * 3 * TC_ROWS;
+      mp[cand] = mu_p * T2.k_unscale;
+      mp[TC_ROWS + cand] = sb_p * T2.k_unscale;
+      mp[2 * TC_ROWS + cand] = kk_p * (T2.k_unscale * T2.k_unscale);
     };
 
     // Tile loop.  Before the epilogue of tile t (which waits for all of t's MMAs) the producers
