@@ -182,6 +182,7 @@ struct as_space {
   std::vector<float> h_xh, h_oh;   // SIMT features of the one-hot kernel (scaled)
   std::vector<uint16_t> h_Wch;     // L^-1^T FP16 hi/lo chunks of the one-hot kernel (scaled by 2^ew)
   uint16_t* d_Tch = nullptr;
+  uint16_t* d_ezero = nullptr;   // zeros for the one-hot E buffers (bulk-copied by the loader warp)
   uint16_t* d_Wch = nullptr;
   float *d_xh = nullptr, *d_oh = nullptr;
   Tc2B t2{};
@@ -851,6 +852,9 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
                     s->owned)) != AS_OK)
       return cleanup(r);
     if ((r = dalloc(&s->d_oh, static_cast<size_t>(Mc) * 4, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = dalloc(&s->d_ezero, static_cast<size_t>(TC_ROWS) * s->t2.Kp, s->owned)) != AS_OK) return cleanup(r);
+    CUDA_TRY(cudaMemset(s->d_ezero, 0, static_cast<size_t>(TC_ROWS) * s->t2.Kp * sizeof(uint16_t)));
+    s->t2.ezero = s->d_ezero;
     // pool buffers at capacity
     s->KC_max = KC_CAP;
     if ((r = dalloc(&s->d_pool, KC_CAP, s->owned)) != AS_OK) return cleanup(r);

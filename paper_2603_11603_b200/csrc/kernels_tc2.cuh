@@ -70,6 +70,7 @@ struct Tc2B {
   float r_scale;                // 2^-s/2
   int eoff[DMAX];               // one-hot column of digit 0 of feature f (-1: SIMT feature)
   // v = L^-1 k in kind::f16: k scaled by 2^ek and L^-1 by 2^ew, each split into FP16 hi + lo
+  const uint16_t* ezero;        // >= 128 x Kp FP16 zeros: bulk-copied over a used E buffer by the loader
   const uint16_t* wch;          // L^-1^T chunks: chunk c = [hi (N_c x 16)][lo (N_c x 16)], kmajor_off16
   uint32_t woff[TC_MAXCH];      // element offset of chunk c
   int ek;                       // k scale exponent (kernel values leave the exp2 already scaled)
@@ -165,6 +166,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
   uint64_t* x_empty = x_full + TC2_NT;         // [NT] commit
   uint64_t* s_full = x_empty + TC2_NT;         // [2]  1 + tx  (tile records staged)
   uint64_t* s_empty = s_full + 2;              // [2]  count PW
+  uint64_t* ez_full = s_empty + 2;             // [2]  1 + tx  (E buffer zeroed again by a bulk copy)
 
   // ---- setup
   // point-pair layout: [al_2p, al_2p+1, |al_2p|, |al_2p+1|] so one LDS.128 feeds packed f32x2 math
@@ -180,6 +182,15 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     oh_s[(j >> 1) * 2 * NH + 2 * h + (j & 1)] = __ldg(T2.oh + i);
   }
   for (int i = tid; i < NH * VMAX; i += TC_THREADS) xh_s[i] = __ldg(T2.xh + i);
+  {
+    // both one-hot buffers start zeroed; afterwards the loader re-zeroes a buffer with a bulk copy
+    // as soon as the last R2 MMAs of its tile have completed (no zeroing pass, no barrier in publish)
+    unsigned char* E0z = sm0 + TC2_O_VAR + static_cast<size_t>(TC2_NB) * 2u * TB.Mp16 * TC_KCH * 2 +
+                         static_cast<size_t>(TC2_NT) * 2u * (TC2_RG * TC_KCH) * T2.Kp * 2;
+    for (uint32_t i = tid; i < 2u * TC_ROWS * T2.Kp * 2 / 16; i += TC_THREADS)
+      *reinterpret_cast<uint4*>(E0z + 16 * i) = make_uint4(0u, 0u, 0u, 0u);
+    tc::fence_proxy_async();
+  }
   if (tid == 0) {
     for (int s = 0; s < TC2_NA; ++s) {
       tc::mbar_init(a_full + s, TC_PROD_WARPS);
@@ -203,6 +214,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(s_full + s, 1);
       tc::mbar_init(s_empty + s, TC_PROD_WARPS);
+      tc::mbar_init(ez_full + s, 1);
     }
     tc::mbar_fence_init();
     ts.n_list = 0;
@@ -351,17 +363,19 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
           m_m0[us * TC_ROWS + pt] = reinterpret_cast<const double*>(sg + TC2_STG_M0)[pt];
         }
         unsigned char* E = E0 + (u & 1) * e_bytes;
-        for (uint32_t i = pt; i < e_bytes / 16; i += TC_PROD_THREADS)
-          *reinterpret_cast<uint4*>(E + 16 * i) = make_uint4(0u, 0u, 0u, 0u);
-        named_sync(1, TC_PROD_THREADS);
         if (cand < n) {
           DV cdv;
           cdv.w[0] = reinterpret_cast<const uint64_t*>(sg + TC2_STG_DV0)[cand];
           cdv.w[1] = reinterpret_cast<const uint64_t*>(sg + TC2_STG_DV1)[cand];
           cdv.w[2] = reinterpret_cast<const uint64_t*>(sg + TC2_STG_DV2)[cand];
-          for (int f = jq; f < S.d; f += TC_JQ) {
-            if (eoff_s[f] < 0) continue;
-            const uint32_t col = static_cast<uint32_t>(eoff_s[f]) + dv_get(cdv, f);
+          int eo[DMAX / TC_JQ];                                  // this thread's features, loads hoisted
+#pragma unroll
+          for (int q = 0; q < DMAX / TC_JQ; ++q) eo[q] = (jq + TC_JQ * q < S.d) ? eoff_s[jq + TC_JQ * q] : -1;
+          if (u >= 2) tc::mbar_wait(ez_full + (u & 1), ((u >> 1) + 1) & 1);   // buffer re-zeroed
+#pragma unroll
+          for (int q = 0; q < DMAX / TC_JQ; ++q) {
+            if (eo[q] < 0) continue;
+            const uint32_t col = static_cast<uint32_t>(eo[q]) + dv_get(cdv, jq + TC_JQ * q);
             *reinterpret_cast<uint16_t*>(E + tc::kmajor_off16(cand, col, Kp / 8)) = 0x3C00;   // FP16 1.0
           }
           if (jq < NH) {
@@ -675,6 +689,16 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         }
         if (xl < tot_T && tc::mbar_test(x_empty + (xl % TC2_NT), ((xl / TC2_NT) & 1u) ^ 1u)) {
           const int s_ = xl % TC2_NT;
+          if (xl >= TC2_NT) {
+            // R2 group xl - NT has completed; if it was the last group of its tile u, the one-hot
+            // buffer E[u & 1] is free: zero it for tile u + 2 (every u + 2 < my_tiles gets here)
+            const uint32_t xg = xl - TC2_NT;
+            const int u = static_cast<int>(xg / ng);
+            if (xg % ng == static_cast<uint32_t>(ng - 1) && u + 2 < my_tiles) {
+              tc::mbar_arrive_expect_tx(ez_full + (u & 1), e_bytes);
+              tc::bulk_g2s(E0 + (u & 1) * e_bytes, T2.ezero, e_bytes, ez_full + (u & 1));
+            }
+          }
           tc::mbar_arrive_expect_tx(x_full + s_, t_stage_bytes);
           tc::bulk_g2s(T0 + static_cast<size_t>(s_) * t_stage_bytes,
                        T2.tch + static_cast<size_t>(xc) * (t_stage_bytes / 2), t_stage_bytes, x_full + s_);
