@@ -558,7 +558,8 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         pre = head;
       }
       epilogue(t, vsq_t);
-      named_sync(1, TC_PROD_THREADS);
+      // (no barrier here: publish(t + 2)'s barrier already orders every reuse of tile t's slots --
+      // meta rows are rewritten by the threads that read them, tinfo / m_part / vpart only after it)
       n_cur = n_next;
     }
     // ---- CTA list (final prune: sorted, at most KC entries)
