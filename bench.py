@@ -164,12 +164,16 @@ def cpu_baseline(cfg, raws, costs, seconds, seed=0):
         t0 = time.perf_counter()
         done = 0
         chunk = 2048
+        n_all = o.n_cvi() if b["mode"] == "range" else int(b.get("count", o.n_cvi()))
         while time.perf_counter() - t0 < seconds:
-            run.score_batch(o, fit, b["mode"], done, chunk, seed, acq=b["acq"])
-            done += chunk
+            start = done % n_all                      # small spaces: wrap around the batch
+            c = min(chunk, n_all - start)
+            run.score_batch(o, fit, b["mode"], start, c, seed, acq=b["acq"])
+            done += c
         dt = time.perf_counter() - t0
     return {"value": done / dt, "unit": "candidates/s", "cores": 1, "kind": "oracle",
-            "sample": f"{cfg} {b['mode']} ordinals [0,{done}) of the bench batch (seed {seed}), "
+            "sample": f"{cfg} {b['mode']}: {done} candidates of the bench batch from ordinal 0"
+                      f"{' (wrapping around the whole space)' if done > n_all else ''} (seed {seed}), "
                       f"{dt:.1f} s, numpy/BLAS 1 thread; top-k sort excluded (bounded sample)"}
 
 
@@ -194,13 +198,15 @@ def run_reference(args):
     raws, costs = synthgen.observed_set(b["M"], 0, o.n_cvi(), [f.n for f in o.features], unrank,
                                         lambda r: bool(sim.simulate(o, [o.decode_raw(r)])[1][0]),
                                         lambda r: float(sim.simulate(o, [o.decode_raw(r)])[0][0]))
-    chunk = 1024
+    n_all = o.n_cvi() if b["mode"] == "range" else int(b.get("count", o.n_cvi()))
+    chunk = min(1024, n_all)
     with threadpool_limits(1):
         fit = run.observed_fit(o, raws, costs)
         times = []
         for i in range(args.warmup + args.steps):
             t0 = time.perf_counter()
-            rec = run.score_batch(o, fit, b["mode"], i * chunk, chunk, 0, acq=b["acq"])
+            start = (i * chunk) % n_all                 # small spaces: wrap around the batch
+            rec = run.score_batch(o, fit, b["mode"], start, min(chunk, n_all - start), 0, acq=b["acq"])
             run.topk(rec, b["k"])
             dt = time.perf_counter() - t0
             if i >= args.warmup:
