@@ -335,18 +335,20 @@ __device__ __forceinline__ float acquisition32(int acq, float mu, float s2, floa
     margin = 1e-6f * (1.0f + fabsf(m0));
     return -m0;
   }
-  const float sigma = sqrtf(fmaxf(s2, 0.0f));
   if (acq == 1) {
+    const float sigma = sqrtf(fmaxf(s2, 0.0f));
     margin = 1e-6f * (1.0f + fabsf(mu) + kappa * sigma);
     return kappa * sigma - mu;
   }
   const float u = fstar - mu - xi;
-  if (sigma == 0.0f) {
+  if (!(s2 > 0.0f)) {
     margin = 1e-6f * (1.0f + fabsf(u));
     return u > 0.0f ? logf(u) : -INFINITY;
   }
-  const float z = u / sigma;
-  const float r = logf(sigma) + lnh_f(z);
+  // z = u / sigma by one reciprocal square root (a few ulp: its effect on ln h, at most ~|z| per unit
+  // relative error of z, stays inside the 1e-6 (1 + z^2) term of the margin), ln sigma = ln(s2) / 2
+  const float z = u * rsqrtf(s2);
+  const float r = 0.5f * logf(s2) + lnh_f(z);
   // FP32 evaluation error: rounding of the terms + cancellation of phi + z Phi (~ u z^2 relative)
   margin = 2e-6f * (1.0f + fabsf(r)) + (z < -10.0f ? 0.0f : 1e-6f * (1.0f + z * z));
   return r;

@@ -291,7 +291,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         const float eps = 8.0f * static_cast<float>(G.eps);
         const float d_mu = eps * sb + 2e-7f * (1.0f + fabsf(mu));
         const float ew = eps * static_cast<float>(G.w_fro);
-        const float d_s2 = 2.5f * ew * sqrtf(vs) * sqrtf(kk) + ew * ew * kk + eps * vs + 8.0f * U32 * G.sf2f;
+        const float d_s2 = 2.5f * ew * sqrtf(vs * kk) + ew * ew * kk + eps * vs + 8.0f * U32 * G.sf2f;
         const float fstar = static_cast<float>(G.fstar), m0f = static_cast<float>(cm0);
         float m2;
         float ub = acquisition32(A.acq, mu - d_mu, s2 + d_s2, m0f, fstar, static_cast<float>(A.xi),
