@@ -218,6 +218,12 @@ as_status autoscout_mask_range(as_space* s, uint64_t raw_begin, uint64_t count, 
  * does not fit fails at score time with AS_ERR_CAPACITY. */
 as_status autoscout_set_path(as_space* s, int32_t path);
 
+/* Candidates per generate + score slice on the one-hot tensor-core path: each slice's
+ * compact list of valid candidates needs up to 40 B per candidate of device memory (default 2^27
+ * candidates = 5.4 GB worst case, one slice for the 10^8 bench batch).  Results do not depend on it.
+ * AS_ERR_INVALID_ARG outside [128, 2^31]. */
+as_status autoscout_set_slice(as_space* s, uint64_t max_candidates);
+
 /* Device-time of the last score kernel launch in ms (CUDA events on the launching stream,
  * recorded when `timing` was enabled), for the roofline report in bench.py. */
 as_status autoscout_set_timing(as_space* s, int32_t enable);

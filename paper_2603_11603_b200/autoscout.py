@@ -37,7 +37,7 @@ EXPORTS = ["autoscout_space_create", "autoscout_space_destroy", "autoscout_space
            "autoscout_sample_to_cvi", "autoscout_simulate", "autoscout_mask_range", "autoscout_set_path",
            "autoscout_set_timing", "autoscout_raw_to_cvi", "autoscout_subtree_range", "autoscout_neighbors",
            "autoscout_prior", "autoscout_ensemble_info", "autoscout_gp_lml", "autoscout_set_gp_hyper",
-           "autoscout_ml2",
+           "autoscout_ml2", "autoscout_set_slice",
            "autoscout_last_kernel_ms", "autoscout_last_phase_ms", "autoscout_last_error"]
 
 
@@ -96,6 +96,7 @@ def _load():
         "autoscout_mask_range": ([P, U64, U64, P, P, P], I32),
         "autoscout_set_path": ([P, I32], I32),
         "autoscout_set_timing": ([P, I32], I32),
+        "autoscout_set_slice": ([P, U64], I32),
         "autoscout_last_kernel_ms": ([P, pD, pD], I32),
         "autoscout_last_phase_ms": ([P, pD, pD], I32),
         "autoscout_last_error": ([], ctypes.c_char_p),
@@ -324,6 +325,10 @@ class Space:
         path = {"auto": 0, "simt": 1, "tc": 2, "tc2": 3}.get(path, path)
         _check(_LIB.autoscout_set_path(self.h, int(path)))
 
+    def set_slice(self, max_candidates):
+        """Candidates per generate + score slice of the one-hot path (list memory 40 B each)."""
+        _check(_LIB.autoscout_set_slice(self.h, int(max_candidates)))
+
     def set_timing(self, enable=True):
         _check(_LIB.autoscout_set_timing(self.h, 1 if enable else 0))
 
@@ -416,3 +421,7 @@ def autoscout_set_gp_hyper(space, lengthscale, sf2, sn2):
 
 def autoscout_ml2(space, n_set=1024, seed=0, apply=True, stream=None):
     return space.ml2(n_set, seed, apply, stream)
+
+
+def autoscout_set_slice(space, max_candidates):
+    return space.set_slice(max_candidates)

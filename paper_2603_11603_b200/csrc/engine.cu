@@ -195,6 +195,7 @@ struct as_space {
   size_t scratch_cap = 0;
   TcB tb{};
   int path = 0;                    // 0 auto, 1 SIMT, 2 tensor cores (SIMT r^2), 3 tensor cores (one-hot r^2)
+  uint64_t slice = 1ull << 27;     // candidates per generate + score slice of the one-hot path (GEN_SLICE)
   std::vector<double> h_O64, h_alpha64, h_W64;
   // pool state
   int KC = 0;
@@ -445,10 +446,11 @@ as_status ensure_lists(as_space* s, int grid) {
   return AS_OK;
 }
 
-// One-hot tensor-core path: the batch is processed in slices of up to 2^25 candidates; per slice
+// One-hot tensor-core path: the batch is processed in slices (default 2^27 candidates, a 5.4 GB worst-
+// case list; autoscout_set_slice lowers it); per slice
 // the generate kernel writes the compact list of valid candidates and the score kernel consumes
 // it (one CTA per SM), then the pool merge.
-constexpr uint64_t GEN_SLICE = 1ull << 25;
+constexpr uint64_t GEN_SLICE = 1ull << 27;   // default slice (one slice for the 10^8 bench batch)
 constexpr int SEV_MAX = 3 * 64;
 
 as_status ensure_cand_list(as_space* s, size_t cap) {
@@ -481,7 +483,7 @@ as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, b
   out.counts = s->d_counts;
   out.drop = s->d_drops;
   if (count > 0) {
-    r = ensure_cand_list(s, static_cast<size_t>(std::min<uint64_t>(count, GEN_SLICE)));
+    r = ensure_cand_list(s, static_cast<size_t>(std::min<uint64_t>(count, s->slice)));
     if (r != AS_OK) return r;
   }
   // whole prefix table + bucket index in SMEM when they fit, else a coarse index of GEN_CI_MAX entries
@@ -500,9 +502,10 @@ as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, b
   tb.scratch = s->d_scratch;
   const int P2 = next_pow2_h(s->KC + MERGE_THREADS);
   CUDA_TRY(cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P2 * 8));
-  const uint64_t n_slices = count == 0 ? 1 : (count + GEN_SLICE - 1) / GEN_SLICE;
+  const uint64_t SL = s->slice;
+  const uint64_t n_slices = count == 0 ? 1 : (count + SL - 1) / SL;
   for (uint64_t sl = 0; sl < n_slices; ++sl) {
-    const uint64_t j0 = sl * GEN_SLICE, nj = std::min<uint64_t>(GEN_SLICE, count - j0);
+    const uint64_t j0 = sl * SL, nj = std::min<uint64_t>(SL, count - j0);
     const bool ev = s->timing && s->sev_used + 3 <= static_cast<int>(s->sev.size());
     if (nj > 0) {
       CUDA_TRY(cudaMemsetAsync(s->list.count, 0, sizeof(unsigned long long), st));
@@ -1369,6 +1372,13 @@ as_status autoscout_set_path(as_space* s, int32_t path) {
   if (!s || path < 0 || path > 3)
     return fail(AS_ERR_INVALID_ARG, "path must be 0 (auto), 1 (SIMT), 2 (tensor cores) or 3 (tensor cores, one-hot r^2)");
   s->path = path;
+  return AS_OK;
+}
+
+as_status autoscout_set_slice(as_space* s, uint64_t max_candidates) {
+  if (!s || max_candidates < TC_ROWS || max_candidates > (1ull << 31))
+    return fail(AS_ERR_INVALID_ARG, "slice must be in [128, 2^31] candidates");
+  s->slice = max_candidates;
   return AS_OK;
 }
 

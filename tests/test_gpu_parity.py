@@ -343,3 +343,25 @@ def test_topk_without_per_candidate_outputs(name, M, mode, count, seed):
         fit = run.observed_fit(o, raws, costs)
         rec = run.score_batch(o, fit, "range", 0, n, acq="ei")
         check_topk(fast, run.topk(rec, 32))
+
+
+def test_slices_do_not_change_results():
+    """The one-hot path in many small slices (generate + score + merge per slice, pool accumulated
+    across slices) returns the same per-candidate scores and certified top-k as one slice."""
+    o = oracle_space("C4")
+    raws, costs = observed(o, 256, 0)
+    n = 3_000_000
+    out = []
+    for slice_ in (None, 1 << 20, 777_777):
+        sp = A.Space(space_path("C4"), 0)
+        sp.observe(raws, costs)
+        if slice_:
+            sp.set_slice(slice_)
+        sc = torch.empty(n, dtype=torch.float32, device="cuda")
+        sp.score_batch(mode="sample", begin=0, count=n, seed=2, acq="ei", k=32, d_scores=sc)
+        top = sp.topk(32)
+        torch.cuda.synchronize()
+        out.append((sc.cpu().numpy(), top))
+    for sc, top in out[1:]:
+        assert np.array_equal(sc, out[0][0])
+        assert top == out[0][1]
