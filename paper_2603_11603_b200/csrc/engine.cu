@@ -182,7 +182,8 @@ struct as_space {
   std::vector<float> h_xh, h_oh;   // SIMT features of the one-hot kernel (scaled)
   std::vector<uint16_t> h_Wch;     // L^-1^T FP16 hi/lo chunks of the one-hot kernel (scaled by 2^ew)
   uint16_t* d_Tch = nullptr;
-  uint16_t* d_ezero = nullptr;   // zeros for the one-hot E buffers (bulk-copied by the loader warp)
+  uint16_t* d_ezero = nullptr;
+  unsigned char* h_stage = nullptr;   // pinned host staging of the refined pool (one DMA per copy, no pageable bounce)   // zeros for the one-hot E buffers (bulk-copied by the loader warp)
   uint16_t* d_Wch = nullptr;
   float *d_xh = nullptr, *d_oh = nullptr;
   Tc2B t2{};
@@ -646,13 +647,17 @@ as_status refine_pool(as_space* s, int acq, double kappa, double xi, cudaStream_
                                                          s->d_ref_score, s->d_ref_raw);
   CUDA_TRY(cudaGetLastError());
   ++s->n_launches;
-  std::vector<double> sc(s->KC);
-  std::vector<uint64_t> rw(s->KC);
-  CUDA_TRY(cudaMemcpyAsync(&n_pool, s->d_pool_n, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(&cut, s->d_cut, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(sc.data(), s->d_ref_score, s->KC * sizeof(double), cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(rw.data(), s->d_ref_raw, s->KC * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  // into pinned staging: [cut u64][n_pool i32 (+pad)][KC scores][KC raws]
+  unsigned char* hs = s->h_stage;
+  double* sc = reinterpret_cast<double*>(hs + 16);
+  uint64_t* rw = reinterpret_cast<uint64_t*>(hs + 16 + static_cast<size_t>(s->KC) * 8);
+  CUDA_TRY(cudaMemcpyAsync(hs, s->d_cut, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(hs + 8, s->d_pool_n, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(sc, s->d_ref_score, s->KC * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(rw, s->d_ref_raw, s->KC * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  std::memcpy(&cut, hs, sizeof(uint64_t));
+  std::memcpy(&n_pool, hs + 8, sizeof(int));
   ent.clear();
   for (int e = 0; e < n_pool; ++e)
     if (std::isfinite(sc[e])) ent.push_back({sc[e], rw[e]});
@@ -866,6 +871,8 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
     if ((r = dalloc(&s->d_valid, 1, s->owned)) != AS_OK) return cleanup(r);
     if ((r = dalloc(&s->d_ref_score, KC_CAP, s->owned)) != AS_OK) return cleanup(r);
     if ((r = dalloc(&s->d_ref_raw, KC_CAP, s->owned)) != AS_OK) return cleanup(r);
+    if (cudaMallocHost(reinterpret_cast<void**>(&s->h_stage), 16 + static_cast<size_t>(KC_CAP) * 16) != cudaSuccess)
+      return cleanup(fail(AS_ERR_OOM, "pinned host staging allocation failed"));
     e = cudaMemset(s->d_pool_n, 0, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(s->d_valid, 0, sizeof(uint64_t));
     if (e != cudaSuccess) return cleanup(fail(AS_ERR_CUDA, cudaGetErrorString(e)));
@@ -884,6 +891,7 @@ void autoscout_space_destroy(as_space* s) {
   if (s->device >= 0) {
     cudaSetDevice(s->device);
     for (void* p : s->owned) cudaFree(p);
+    if (s->h_stage) cudaFreeHost(s->h_stage);
     if (s->d_lists) cudaFree(s->d_lists);
     if (s->d_counts) cudaFree(s->d_counts);
     if (s->d_drops) cudaFree(s->d_drops);
