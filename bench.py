@@ -92,24 +92,83 @@ def fp32_peak_tflops(sm_mhz, n_sm=148):
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock / throttle-reason sampler for the timed region (B200_PROFILING.md clocks line).
+
+    NVML (nvidia_ml_py) polled from a thread every 10 ms between mark() and stop(), plus one sample at
+    each end, so even a 0.2 s timed region has samples; nvidia-smi -lms 200 as the fallback."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index):
+        self.samples = []
+        self.active = False
+        self.nvml = None
         self.p = None
-        self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
         try:
-            self.fh = open(self.path, "w")
-            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-i", str(gpu_index), "-lms", "200"], stdout=self.fh,
-                                      stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                         "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                         "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                         "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            import threading
+            self.stop_evt = threading.Event()
+            self.th = threading.Thread(target=self._loop, daemon=True)
+            self.th.start()
         except Exception:
-            self.p = None
+            self.nvml = None
+            self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
+            try:
+                self.fh = open(self.path, "w")
+                self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                           "-i", str(gpu_index), "-lms", "200"], stdout=self.fh,
+                                          stderr=subprocess.DEVNULL)
+            except Exception:
+                self.p = None
+
+    def _sample(self):
+        try:
+            sm = self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM)
+            try:
+                r = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                r = self.nvml.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+            self.samples.append((float(sm), int(r)))
+        except Exception:
+            pass
+
+    def _loop(self):
+        while not self.stop_evt.wait(0.01):
+            if self.active:
+                self._sample()
+
+    def mark(self):
+        """Start of the timed region."""
+        if self.nvml is not None:
+            self._sample()
+            self.active = True
+        else:
+            try:
+                self.offset = os.path.getsize(self.path)
+            except Exception:
+                self.offset = 0
 
     def stop(self):
+        if self.nvml is not None:
+            self._sample()
+            self.active = False
+            self.stop_evt.set()
+            self.th.join(timeout=1)
+            if not self.samples:
+                return None
+            reasons = sorted({nm for _, r in self.samples for nm, b in self.bits.items() if r & b})
+            return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": float(self.max_sm),
+                    "samples": len(self.samples), "reasons": reasons, "source": "nvml"}
         if self.p is None:
             return None
         self.p.terminate()
@@ -121,22 +180,28 @@ class Clocks:
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         with open(self.path) as fh:
-            for line in fh:
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) < 9:
-                    continue
-                try:
-                    sm.append(float(parts[1]))
-                    mx.append(float(parts[2]))
-                except ValueError:
-                    continue
-                for nm, v in zip(names, parts[5:9]):
-                    if v.lower() == "active":
-                        reasons.add(nm)
+            text = fh.read()
+        off = getattr(self, "offset", 0)
+        lines = text[off:].splitlines()
+        if not any(len(x.split(",")) >= 9 for x in lines):
+            before = [x for x in text[:off].splitlines() if len(x.split(",")) >= 9]
+            lines = before[-1:]
+        for line in lines:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
         if not sm:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "samples": len(sm),
-                "reasons": sorted(reasons)}
+                "reasons": sorted(reasons), "source": "nvidia-smi"}
 
 
 def observed_with_library(sp, M, seed=0):
@@ -263,15 +328,16 @@ def run_ours(args):
         pool, npool, cut = sp.topk_pool(k, cap, stream=stream)
         return gather_merge(pool, npool, cut, k, device=dev)[0]
 
+    clocks = Clocks(local)                        # started before the warm-up: nvidia-smi needs ~0.2 s
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
     sp.set_timing(True)
     launches0 = sp.n_launches()
-    clocks = Clocks(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
+    clocks.mark()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     kern_ms, phase_ms = [], []
     vc.zero_()
