@@ -90,6 +90,12 @@ def simulate(space, digits_list, terms=False):
     """-> (cost [B] FP64 objective units, resource_ok [B] bool, mem_or_usable [B] FP64)
     [, dict of the named cost terms when terms=True]."""
     vals, acts, present = knob_arrays(space, digits_list)
+    return simulate_knobs(space, vals, acts, present, terms)
+
+
+def simulate_knobs(space, vals, acts, present, terms=False):
+    """simulate() on per-knob arrays of effective values / activity (knob_arrays' output, or
+    oracle/batch.py's vectorised equivalent for large batches)."""
     if space.sim_mode == "spec":
         out = _spec(space, vals, acts)
     elif space.sim_mode == "derived":

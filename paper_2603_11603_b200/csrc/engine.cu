@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -516,9 +517,26 @@ as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, b
       CUDA_TRY(cudaGetLastError());
       ++s->n_launches;
       if (ev) CUDA_TRY(cudaEventRecord(s->sev[s->sev_used + 1], st));
+      static unsigned long long* tr_buf = nullptr;
+      const char* tr_path = std::getenv("AS_TC2_TRACE");   // development aid: CTA-0 phase timeline
+      const size_t tr_n = static_cast<size_t>(TC2_TR_TILES) * TC2_TR_EV * 18;
+      if (tr_path != nullptr && tr_buf == nullptr) {
+        CUDA_TRY(cudaMalloc(&tr_buf, tr_n * 8));
+        CUDA_TRY(cudaMemcpyToSymbol(g_tc2_trace, &tr_buf, sizeof(tr_buf)));
+      }
+      if (tr_buf != nullptr) CUDA_TRY(cudaMemsetAsync(tr_buf, 0, tr_n * 8, st));
       k2<<<grid, TC_WARPS * 32 + 64, smem, st>>>(s->D, s->G, A, out, tb, s->t2, s->list);
       CUDA_TRY(cudaGetLastError());
       ++s->n_launches;
+      if (tr_buf != nullptr) {
+        std::vector<unsigned long long> h(tr_n);
+        CUDA_TRY(cudaMemcpyAsync(h.data(), tr_buf, tr_n * 8, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (FILE* f = std::fopen(tr_path, "ab")) {
+          std::fwrite(h.data(), 8, tr_n, f);
+          std::fclose(f);
+        }
+      }
       if (ev) {
         CUDA_TRY(cudaEventRecord(s->sev[s->sev_used + 2], st));
         s->sev_used += 3;

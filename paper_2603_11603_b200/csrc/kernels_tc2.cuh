@@ -34,6 +34,8 @@ constexpr int TC2_PF = TC2_NB - 2;           // chunks prefetched ahead of the M
                                              // waits for the MMAs two chunks back, not the previous one
 constexpr int TC2_NT = 2;                    // T group ring stages (refilled early by the loader warp)
 constexpr int TC2_KPMAX = 64;                // one-hot width the host aims for (features beyond go SIMT)
+constexpr int TC2_TI = 3;                    // meta slots (cvi, j, m0): read by finalize() one tile later
+constexpr int TC2_CB = 1;                    // chunks whose math is batched ahead of their A-stage waits (ILP)
 
 // Shared-memory carve-out: the fixed-size arrays first (compile-time offsets, so the hot loop
 // addresses them with immediates), then the rings whose size depends on M and Kp.
@@ -45,9 +47,9 @@ constexpr size_t TC2_O_MXH = TC2_O_OH + 4 * MMAX * 4;
 constexpr size_t TC2_O_MPART = TC2_O_MXH + 4 * TC_TI * TC_ROWS * 4;
 constexpr size_t TC2_O_VPART = TC2_O_MPART + TC_TI * 4 * 3 * TC_ROWS * 4;   // [TI][jq][3][128]: one slot per thread
 constexpr size_t TC2_O_MCVI = TC2_O_VPART + 4 * TC_ROWS * 4;
-constexpr size_t TC2_O_MJ = TC2_O_MCVI + TC_TI * TC_ROWS * 4;
-constexpr size_t TC2_O_MM0 = TC2_O_MJ + TC_TI * TC_ROWS * 4;
-constexpr size_t TC2_O_XH = TC2_O_MM0 + TC_TI * TC_ROWS * 8;
+constexpr size_t TC2_O_MJ = TC2_O_MCVI + TC2_TI * TC_ROWS * 4;
+constexpr size_t TC2_O_MM0 = TC2_O_MJ + TC2_TI * TC_ROWS * 4;
+constexpr size_t TC2_O_XH = TC2_O_MM0 + TC2_TI * TC_ROWS * 8;
 // staging of one tile of list records (bulk-copied by the loader): cvi | j | m0 | dv0 | dv1 | dv2
 constexpr size_t TC2_STG_CVI = 0, TC2_STG_J = 512, TC2_STG_M0 = 1024, TC2_STG_DV0 = 2048, TC2_STG_DV1 = 3072,
                  TC2_STG_DV2 = 4096, TC2_STG_BYTES = 5120;
@@ -58,6 +60,11 @@ __host__ __device__ constexpr size_t tc2_smem_total(int Mp16, int Kp, int P) {
   return TC2_O_VAR + static_cast<size_t>(TC2_NB) * 2 * Mp16 * 16 * 2 + static_cast<size_t>(TC2_NT) * 2 * 64 * Kp * 2 +
          2ull * 128 * Kp * 2 + static_cast<size_t>(P) * 8;
 }
+
+// Phase timeline of CTA 0 (development aid, off unless the host sets AS_TC2_TRACE): clock64 per
+// (tile < TC2_TR_TILES, event, warp); written by lane 0 of each warp.
+constexpr int TC2_TR_TILES = 64, TC2_TR_EV = 16;
+__device__ unsigned long long* g_tc2_trace = nullptr;
 
 struct Tc2B {
   const uint16_t* tch;          // T groups: [ng][2 pieces][64 x Kp] FP16, kmajor_off16 layout
@@ -78,10 +85,10 @@ struct Tc2B {
   float vsq_unscale;            // 2^-2(ek + ew)
 };
 
-// Lazy top-k' admission: keys below the (possibly stale) threshold tau are appended to the
-// unsorted tail of arr; the sort-and-prune to KC entries runs only when the next tile could
-// overflow arr (P - 128 entries), and once at the end.  tau only ever tightens, so a stale tau
-// admits more keys, never fewer; rejected keys update drop exactly as in group_admit.
+// Lazy top-k' admission (finalize() below): keys below the (possibly stale) threshold tau are
+// appended to the unsorted tail of arr; the sort-and-prune to KC entries runs only when the next
+// tile could overflow arr (P - 128 entries), and once at the end.  tau only ever tightens, so a
+// stale tau admits more keys, never fewer; rejected keys lower drop exactly as in group_admit.
 __device__ __forceinline__ void tc2_prune(uint64_t* arr, TopkSmem& ts, int KC, int t, int nt, int id) {
   const int n_tot = ts.n_list + ts.n_add;
   if (n_tot > 0) group_bitonic(arr, next_pow2(n_tot < 2 ? 2 : n_tot), t, nt, id);
@@ -95,20 +102,6 @@ __device__ __forceinline__ void tc2_prune(uint64_t* arr, TopkSmem& ts, int KC, i
   for (int i = keep + t; i < n_tot; i += nt) arr[i] = KEY_NONE;
   named_sync(id, nt);
 }
-__device__ __forceinline__ void tc2_admit(uint64_t key, uint64_t* arr, TopkSmem& ts, int KC, int P, int t, int nt,
-                                          int id) {
-  if (key != KEY_NONE) {
-    if (key < ts.tau) {
-      const int pos = atomicAdd(&ts.n_add, 1);
-      arr[ts.n_list + pos] = key;
-    } else {
-      atomicMin(reinterpret_cast<unsigned long long*>(&ts.drop), static_cast<unsigned long long>(key));
-    }
-  }
-  named_sync(id, nt);
-  if (ts.n_list + ts.n_add > P - 128) tc2_prune(arr, ts, KC, t, nt, id);
-}
-
 template <int PW, int KT, int NH>
 __global__ void __launch_bounds__(PW * 32 + 64, 1)
 score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, CandList L) {
@@ -126,6 +119,11 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int Mp16 = TB.Mp16, nch = TB.nch, Kp = T2.Kp;
+  unsigned long long* const trace = blockIdx.x == 0 ? g_tc2_trace : nullptr;
+  auto TR = [&](int u, int ev) {
+    if (trace != nullptr && lane == 0 && u < TC2_TR_TILES)
+      trace[(static_cast<size_t>(u) * TC2_TR_EV + ev) * 18 + warp] = clock64();
+  };
   const int ng = (nch + TC2_RG - 1) / TC2_RG;                         // R2 groups per tile
   const uint32_t A0col = static_cast<uint32_t>(Mp16);                 // TMEM column of A stage 0
   const uint32_t R0col = A0col + 16u * TC2_NA;                        // TMEM column of R2 stage 0
@@ -245,9 +243,11 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     double* scratch = TB.scratch + (static_cast<size_t>(blockIdx.x) * TC_EPI_WARPS + (warp & 3)) * Mp16;
 
     // ---- epilogue of tile u (column blocks < nch - NA were accumulated during the chunk loop)
-    auto epilogue = [&](int u, float vsq_run) {
-      const int us = u % TC_TI;
+    // ---- epilogue, part 1 (all producer warps): the last NA column blocks of D -> |v|^2 partial,
+    // release D.
+    auto epilogue_read = [&](int u, float vsq_run) {
       tc::mbar_wait(d_full, u & 1);
+      TR(u, 4);
       tc::fence_after_sync();
       float vsq = vsq_run;
       const uint32_t taddr = lane_base + TC_JPT * jq;
@@ -268,11 +268,18 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(d_empty);
-      named_sync(1, TC_PROD_THREADS);
-      const int n = tinfo[us];
+      TR(u, 5);
+    };
+
+    // ---- epilogue, part 2 (warps 0-3, row = pt): FP32 screen + bound of tile u's rows and lazy
+    // admission.  Keys that lose against tau lower this thread's drop_r instead of a shared atomicMin
+    // per row (min is order-free; reduced once at the end, and tc2_prune lowers ts.drop as before).
+    uint64_t drop_r = KEY_NONE;
+    auto finalize = [&](int u, int n) {
+      const int us = u % TC_TI, ms = u % TC2_TI;
       uint64_t key = KEY_NONE;
       bool sensitive = false;
-      if (pt < TC_ROWS && pt < n) {
+      if (pt < n) {
         const int row = pt;
         float mu32 = 0.f, sb = 0.f, kk = 0.f, vv = 0.f;
 #pragma unroll
@@ -283,7 +290,8 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
           kk += mp[2 * TC_ROWS + row];
           vv += vpart[q * TC_ROWS + row];
         }
-        const double cm0 = m_m0[us * TC_ROWS + row];
+        const double cm0 = m_m0[ms * TC_ROWS + row];
+        TR(u, 13);
         const float mu = static_cast<float>(cm0 + G.b) + mu32;
         const float vs = vv;
         const float s2 = static_cast<float>(G.sf2) - vs;
@@ -297,6 +305,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         float ub = acquisition32(A.acq, mu - d_mu, s2 + d_s2, m0f, fstar, static_cast<float>(A.xi),
                                  static_cast<float>(A.kappa), m2);
         ub += m2;
+        TR(u, 14);
         if (A.d_scores) {
           const double mud = cm0 + G.b + static_cast<double>(mu32);
           const double s2d = G.sf2 - static_cast<double>(vv);
@@ -317,18 +326,18 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
             }
           }
           if (!sensitive)
-            A.d_scores[m_j[us * TC_ROWS + row]] =
+            A.d_scores[m_j[ms * TC_ROWS + row]] =
                 static_cast<float>(acquisition(A.acq, mud, s2d, cm0, G.fstar, A.xi, A.kappa));
         }
-        if (!sensitive && ub > -INFINITY) key = make_key(ub, m_cvi[us * TC_ROWS + row]);
+        if (!sensitive && ub > -INFINITY) key = make_key(ub, m_cvi[ms * TC_ROWS + row]);
       }
-      if (warp < TC_EPI_WARPS) {
+      {
         unsigned fl = __ballot_sync(0xffffffffu, sensitive);
         while (fl) {
           const int src = __ffs(fl) - 1;
           fl &= fl - 1;
           const int row = warp * 32 + src;
-          const uint32_t cvi = m_cvi[us * TC_ROWS + row];
+          const uint32_t cvi = m_cvi[ms * TC_ROWS + row];
           DV dv;
           uint32_t act;
           uint64_t raw;
@@ -336,15 +345,24 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
           double kalpha, vq;
           posterior64_warp(S, G, dv, lane, scratch, kalpha, vq);
           if (lane == src) {
-            const double cm0 = m_m0[us * TC_ROWS + row];
+            const double cm0 = m_m0[ms * TC_ROWS + row];
             const double sc = acquisition(A.acq, cm0 + G.b + kalpha, G.sf2 - vq, cm0, G.fstar, A.xi, A.kappa);
             const double ub = sc + 1e-12 * fmax(1.0, fabs(sc));
-            A.d_scores[m_j[us * TC_ROWS + row]] = static_cast<float>(sc);
+            A.d_scores[m_j[ms * TC_ROWS + row]] = static_cast<float>(sc);
             if (ub > -INFINITY) key = make_key(__double2float_ru(ub), cvi);
           }
         }
       }
-      tc2_admit(key, arr, ts, out.KC, out.P, pt, TC_PROD_THREADS, 1);
+      TR(u, 6);
+      if (key != KEY_NONE) {
+        if (key < ts.tau) {
+          const int pos = atomicAdd(&ts.n_add, 1);
+          arr[ts.n_list + pos] = key;
+        } else if (key < drop_r) {
+          drop_r = key;
+        }
+      }
+      TR(u, 7);
     };
 
     // publish tile u: meta rows, zeroed partial sums, one-hot rows E[u & 1] and the SIMT-feature
@@ -358,9 +376,10 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         const unsigned char* sg = stg + (u & 1) * TC2_STG_BYTES;
         tc::mbar_wait(s_full + (u & 1), (u >> 1) & 1);
         if (pt < n) {
-          m_cvi[us * TC_ROWS + pt] = reinterpret_cast<const uint32_t*>(sg + TC2_STG_CVI)[pt];
-          m_j[us * TC_ROWS + pt] = reinterpret_cast<const uint32_t*>(sg + TC2_STG_J)[pt];
-          m_m0[us * TC_ROWS + pt] = reinterpret_cast<const double*>(sg + TC2_STG_M0)[pt];
+          const int ms = u % TC2_TI;
+          m_cvi[ms * TC_ROWS + pt] = reinterpret_cast<const uint32_t*>(sg + TC2_STG_CVI)[pt];
+          m_j[ms * TC_ROWS + pt] = reinterpret_cast<const uint32_t*>(sg + TC2_STG_J)[pt];
+          m_m0[ms * TC_ROWS + pt] = reinterpret_cast<const double*>(sg + TC2_STG_M0)[pt];
         }
         unsigned char* E = E0 + (u & 1) * e_bytes;
         if (cand < n) {
@@ -425,64 +444,79 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(r_empty + rs);
           ++gr;
-          // per chunk: k of the thread's 4 points (two packed pairs) -> FP16 hi/lo -> A stage; one
-          // st-wait and the a_full arrivals once per group
+          // The whole group's math first (4 chunks x 2 packed point pairs: eight independent chains
+          // the scheduler can interleave), then the A-stage waits and stores: the waits are asm
+          // volatile and would otherwise fence every chunk's two chains off from the next chunk's.
+          const int ncg = nch - c0 < TC2_RG ? nch - c0 : TC2_RG;
 #pragma unroll
-          for (int cg = 0; cg < TC2_RG; ++cg) {
-            const int c = c0 + cg;
-            if (c >= nch) break;
-            uint32_t hw[2], lw[2];
+          for (int hb = 0; hb < TC2_RG; hb += TC2_CB) {
+            if (hb >= ncg) break;
+            uint32_t hw[TC2_CB][2], lw[TC2_CB][2];
 #pragma unroll
-            for (int qp = 0; qp < TC_JPT / 2; ++qp) {
-              const int jo = c * TC_KCH + jq * TC_JPT + 2 * qp;      // even
-              // R2 >= 0 by construction (non-negative products, FP32 accumulation; squares)
-              unsigned long long r2p = f2_pack(rv[cg * TC_JPT + 2 * qp], rv[cg * TC_JPT + 2 * qp + 1]);
-              if (NH > 0) {
+            for (int cb = 0; cb < TC2_CB; ++cb) {
+              const int cg = hb + cb;
+              const int c = c0 + cg;
+              if (cg >= ncg) break;
 #pragma unroll
-                for (int h = 0; h < NH; h += 2) {
-                  unsigned long long o0, o1;
-                  tc::lds_u64x2(sOH + 4u * ((jo >> 1) * 2 * NH + 2 * h), o0, o1);
-                  const unsigned long long d0 = f2_sub(xb[h], o0), d1 = f2_sub(xb[h + 1], o1);
-                  r2p = f2_fma(d0, d0, r2p);
-                  r2p = f2_fma(d1, d1, r2p);
+              for (int qp = 0; qp < TC_JPT / 2; ++qp) {
+                const int jo = c * TC_KCH + jq * TC_JPT + 2 * qp;      // even
+                // R2 >= 0 by construction (non-negative products, FP32 accumulation; squares)
+                unsigned long long r2p = f2_pack(rv[cg * TC_JPT + 2 * qp], rv[cg * TC_JPT + 2 * qp + 1]);
+                if (NH > 0) {
+#pragma unroll
+                  for (int h = 0; h < NH; h += 2) {
+                    unsigned long long o0, o1;
+                    tc::lds_u64x2_nv(sOH + 4u * ((jo >> 1) * 2 * NH + 2 * h), o0, o1);
+                    const unsigned long long d0 = f2_sub(xb[h], o0), d1 = f2_sub(xb[h + 1], o1);
+                    r2p = f2_fma(d0, d0, r2p);
+                    r2p = f2_fma(d1, d1, r2p);
+                  }
                 }
+                unsigned long long argp, expp, polyp;
+                if (KT == 0) {
+                  const float2 r2 = f2_unpack(r2p);
+                  const unsigned long long rp = f2_pack(tc::sqrt_approx_ftz(r2.x), tc::sqrt_approx_ftz(r2.y));
+                  argp = f2_mul(rp, carg2);
+                  const float2 ea = f2_unpack(f2_fma(rp, c1_2, c0_2));
+                  expp = f2_pack(tc::ex2_approx(ea.x), tc::ex2_approx(ea.y));
+                  polyp = f2_fma(argp, f2_fma(argp, third2, one2), one2);
+                } else {
+                  argp = f2_mul(r2p, carg2);
+                  const float2 ea = f2_unpack(f2_fma(r2p, c1_2, c0_2));
+                  expp = f2_pack(tc::ex2_approx(ea.x), tc::ex2_approx(ea.y));
+                  polyp = one2;
+                }
+                const unsigned long long kvalp = f2_mul(polyp, expp);
+                const unsigned long long ccp = f2_fma(kvalp, argp, kvalp);
+                unsigned long long alp, aap;
+                tc::lds_u64x2_nv(sAl + 16u * (jo >> 1), alp, aap);
+                mu2 = f2_fma(kvalp, alp, mu2);
+                sb2 = f2_fma(ccp, aap, sb2);
+                kk2 = f2_fma(ccp, ccp, kk2);
+                // FP16 hi / lo split of the (2^ek-scaled) cross-covariances, packed two per column:
+                // hi = k with the low 13 mantissa bits cleared (an FP16 value: 11 significant bits,
+                // exponent inside the FP16 range by the 2^ek scale), lo = k - hi exactly in FP32, then
+                // both converted (hi exactly, lo rounded: |k - hi - lo16| <= 2^-22 |k|); the mask runs
+                // on the ALU pipe instead of two FP16->FP32 conversions on the FMA pipe
+                const float2 kk = f2_unpack(kvalp);
+                const float h0 = __uint_as_float(__float_as_uint(kk.x) & 0xFFFFE000u);
+                const float h1 = __uint_as_float(__float_as_uint(kk.y) & 0xFFFFE000u);
+                const float2 lo = f2_unpack(f2_sub(kvalp, f2_pack(h0, h1)));
+                hw[cb][qp] = tc::pack_f16x2(h0, h1);
+                lw[cb][qp] = tc::pack_f16x2(lo.x, lo.y);
               }
-              unsigned long long argp, expp, polyp;
-              if (KT == 0) {
-                const float2 r2 = f2_unpack(r2p);
-                const unsigned long long rp = f2_pack(tc::sqrt_approx_ftz(r2.x), tc::sqrt_approx_ftz(r2.y));
-                argp = f2_mul(rp, carg2);
-                const float2 ea = f2_unpack(f2_fma(rp, c1_2, c0_2));
-                expp = f2_pack(tc::ex2_approx(ea.x), tc::ex2_approx(ea.y));
-                polyp = f2_fma(argp, f2_fma(argp, third2, one2), one2);
-              } else {
-                argp = f2_mul(r2p, carg2);
-                const float2 ea = f2_unpack(f2_fma(r2p, c1_2, c0_2));
-                expp = f2_pack(tc::ex2_approx(ea.x), tc::ex2_approx(ea.y));
-                polyp = one2;
-              }
-              const unsigned long long kvalp = f2_mul(polyp, expp);
-              const unsigned long long ccp = f2_fma(kvalp, argp, kvalp);
-              unsigned long long alp, aap;
-              tc::lds_u64x2(sAl + 16u * (jo >> 1), alp, aap);
-              mu2 = f2_fma(kvalp, alp, mu2);
-              sb2 = f2_fma(ccp, aap, sb2);
-              kk2 = f2_fma(ccp, ccp, kk2);
-              // FP16 hi / lo split of the (2^ek-scaled) cross-covariances, packed two per column
-              const float2 kk = f2_unpack(kvalp);
-              const uint32_t hp = tc::pack_f16x2(kk.x, kk.y);
-              float f0, f1;
-              tc::unpack_f16x2(hp, f0, f1);
-              const float2 lo = f2_unpack(f2_sub(kvalp, f2_pack(f0, f1)));
-              hw[qp] = hp;
-              lw[qp] = tc::pack_f16x2(lo.x, lo.y);
             }
-            const int s = (g + cg) % TC2_NA;
-            tc::mbar_wait(a_empty + s, (((g + cg) / TC2_NA) & 1u) ^ 1u);
-            tc::fence_after_sync();
-            const uint32_t acol = lane_base + A0col + 16u * s + 2 * jq;
-            tc::tmem_st2(acol, hw[0], hw[1]);
-            tc::tmem_st2(acol + 8, lw[0], lw[1]);
+#pragma unroll
+            for (int cb = 0; cb < TC2_CB; ++cb) {
+              const int cg = hb + cb;
+              if (cg >= ncg) break;
+              const int s = (g + cg) % TC2_NA;
+              tc::mbar_wait(a_empty + s, (((g + cg) / TC2_NA) & 1u) ^ 1u);
+              tc::fence_after_sync();
+              const uint32_t acol = lane_base + A0col + 16u * s + 2 * jq;
+              tc::tmem_st2(acol, hw[cb][0], hw[cb][1]);
+              tc::tmem_st2(acol + 8, lw[cb][0], lw[cb][1]);
+            }
           }
           tc::tmem_st_wait();
           tc::fence_before_sync();
@@ -546,8 +580,11 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     float vsq_c = 0.f;
     int pre = 0;                                              // chunks of tile t already produced
     for (int t = 0; n_cur > 0; ++t) {
+      TR(t, 0);
       const int n_next = publish(t + 1);
+      TR(t, 1);
       produce(t, pre, nch, mu_c, sb_c, kk_c, vsq_c);
+      TR(t, 2);
       flush_part(t, mu_c, sb_c, kk_c);
       const float vsq_t = vsq_c;
       mu_c = sb_c = kk_c = 0ull;
@@ -557,12 +594,18 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         produce(t + 1, 0, head, mu_c, sb_c, kk_c, vsq_c);
         pre = head;
       }
-      epilogue(t, vsq_t);
-      // (no barrier here: publish(t + 2)'s barrier already orders every reuse of tile t's slots --
-      // meta rows are rewritten by the threads that read them, tinfo / m_part / vpart only after it)
+      TR(t, 3);
+      epilogue_read(t, vsq_t);
+      named_sync(1, TC_PROD_THREADS);       // partial sums and |v|^2 of tile t visible
+      if (warp < TC_EPI_WARPS) finalize(t, n_cur);
+      named_sync(1, TC_PROD_THREADS);       // admissions done: uniform prune decision
+      if (ts.n_list + ts.n_add > out.P - TC_ROWS) tc2_prune(arr, ts, out.KC, pt, TC_PROD_THREADS, 1);
+      // (no further barrier: publish(t + 2)'s barrier orders every reuse of tile t's slots)
       n_cur = n_next;
     }
-    // ---- CTA list (final prune: sorted, at most KC entries)
+    // ---- best dropped key, CTA list (final prune: sorted, at most KC entries)
+    if (drop_r != KEY_NONE)
+      atomicMin(reinterpret_cast<unsigned long long*>(&ts.drop), static_cast<unsigned long long>(drop_r));
     named_sync(1, TC_PROD_THREADS);
     tc2_prune(arr, ts, out.KC, pt, TC_PROD_THREADS, 1);
     const int n = ts.n_list;
@@ -605,10 +648,8 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       tc::fence_after_sync();
       const uint32_t dR = tmem + R0col + 64u * rs;
       const uint64_t ad = dE + (((ru & 1) * e_bytes) >> 4), bd = dT + ((st_ * t_stage_bytes) >> 4);
-      for (int ks = 0; ks < ksteps_r; ++ks) {
-        tc::mma_f16_w(dR, ad + 16 * ks, bd + 16 * ks, idesc_r, ks > 0 ? 1u : 0u);
-        tc::mma_f16_w(dR, ad + 16 * ks, bd + piece16 + 16 * ks, idesc_r, 1u);
-      }
+      for (int ks = 0; ks < ksteps_r; ++ks)
+        tc::mma2_f16_w(dR, ad + 16 * ks, bd + 16 * ks, bd + piece16 + 16 * ks, idesc_r, ks > 0 ? 1u : 0u);
       tc::mma_commit_w(r_full + rs);
       tc::mma_commit_w(x_empty + st_);
       ++x;
@@ -619,7 +660,9 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       return true;
     };
     for (int t = 0; tile_exists(t); ++t) {
+      TR(t, 8);
       tc::mbar_wait(d_empty, (t & 1) ^ 1);
+      TR(t, 9);
       tc::fence_after_sync();
       for (int c = 0; c < nch; ++c, ++g) {
         // R2 lookahead: the producers may run NA chunks ahead of M(g), so the group of chunk
@@ -635,6 +678,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         const int sa = g % TC2_NA, sbb = g % TC2_NB;
         tc::mbar_wait(a_full + sa, (g / TC2_NA) & 1);
         tc::mbar_wait(b_full + sbb, (g / TC2_NB) & 1);
+        if (c == TC2_NA) TR(t, 11);
         tc::fence_after_sync();
         const int N = Mp16 - c * TC_KCH;
         const uint32_t idesc = tc::idesc_f16(TC_ROWS, N);
@@ -642,14 +686,11 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         const uint64_t bh = dB + ((sbb * b_stage_bytes) >> 4);
         const uint64_t bl = bh + ((N * TC_KCH * 2) >> 4);
         const uint32_t d = tmem + c * TC_KCH;
-        // 3-term FP16 split: hi.hi + hi.lo + lo.hi (one K = 16 step each)
-        tc::mma_f16_ts_w(d, a_h, bh, idesc, c > 0 ? 1u : 0u);
-        tc::mma_f16_ts_w(d, a_h, bl, idesc, 1u);
-        tc::mma_f16_ts_w(d, a_l, bh, idesc, 1u);
-        tc::mma_commit_w(a_empty + sa);
-        tc::mma_commit_w(b_empty + sbb);
+        // 3-term FP16 split: hi.hi + hi.lo + lo.hi (one K = 16 step each), then release A and B
+        tc::mma3_f16_ts_commit2_w(d, a_h, a_l, bh, bl, idesc, c > 0 ? 1u : 0u, a_empty + sa, b_empty + sbb);
       }
       tc::mma_commit_w(d_full);
+      TR(t, 10);
     }
     __syncwarp();
   } else {

@@ -221,6 +221,36 @@ __device__ __forceinline__ void mma_f16_ts_w(uint32_t d_tmem, uint32_t a_tmem, u
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// One K = 16 step of the 3-term FP16 split with A from TMEM (hi.hi + hi.lo + lo.hi) and the two
+// commits that release its A stage and B stage: one elect for the five instructions.
+__device__ __forceinline__ void mma3_f16_ts_commit2_w(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo, uint64_t b_hi,
+                                                      uint64_t b_lo, uint32_t idesc, uint32_t accumulate,
+                                                      uint64_t* bar_a, uint64_t* bar_b) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %5, 1;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n\t}" ::"r"(d_tmem),
+      "r"(a_hi), "r"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(accumulate), "r"(smem_u32(bar_a)),
+      "r"(smem_u32(bar_b))
+      : "memory");
+}
+// One K = 16 step of the two-piece R2 contraction (E . T_hi + E . T_lo), smem descriptors
+__device__ __forceinline__ void mma2_f16_w(uint32_t d_tmem, uint64_t adesc, uint64_t b_hi, uint64_t b_lo,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %4, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %4, 1;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
