@@ -91,11 +91,16 @@ size_t tc_smem_bytes(int Mp16, int DP, int d, int P) {
 // one-hot R2 kernel (kernels_tc2.cuh): fixed arrays + B ring + T ring + E (2) + top-k' keys
 size_t tc2_smem_bytes(int Mp16, int Kp, int /*nh*/, int P) { return tc2_smem_total(Mp16, Kp, P); }
 using Tc2KernelFn = void (*)(DevSpace, DevGP, BatchArgs, CtaOut, TcB, Tc2B, CandList);
-template <int KT>
+template <int KT, int NCH>
 Tc2KernelFn tc2_kernel_kt(int nh) {
-  return nh == 0 ? score_tc2_kernel<16, KT, 0> : (nh == 2 ? score_tc2_kernel<16, KT, 2> : score_tc2_kernel<16, KT, 4>);
+  return nh == 0 ? score_tc2_kernel<16, KT, 0, NCH>
+                 : (nh == 2 ? score_tc2_kernel<16, KT, 2, NCH> : score_tc2_kernel<16, KT, 4, NCH>);
 }
-Tc2KernelFn tc2_kernel_for(int kernel, int nh) { return kernel == 0 ? tc2_kernel_kt<0>(nh) : tc2_kernel_kt<1>(nh); }
+// compile-time chunk counts for the Matern kernel at M in (240, 256] (C4) and (112, 128] (C5)
+Tc2KernelFn tc2_kernel_for(int kernel, int nh, int nch) {
+  if (kernel == 0) return nch == 16 ? tc2_kernel_kt<0, 16>(nh) : (nch == 8 ? tc2_kernel_kt<0, 8>(nh) : tc2_kernel_kt<0, 0>(nh));
+  return tc2_kernel_kt<1, 0>(nh);
+}
 
 using TcKernelFn = void (*)(DevSpace, DevGP, BatchArgs, CtaOut, TcB);
 template <int KT>
@@ -498,7 +503,7 @@ as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, b
   int occ = 1;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gen_k, GEN_THREADS, gen_smem));
   const int grid_gen = s->n_sm * std::max(occ, 1);
-  auto k2 = tc2_kernel_for(s->G.kernel, s->t2.nh);
+  auto k2 = tc2_kernel_for(s->G.kernel, s->t2.nh, s->tb.nch);
   CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   TcB tb = s->tb;
   tb.scratch = s->d_scratch;
@@ -582,7 +587,7 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
   if (a.count > 0) {
     int occ = 1;
     if (use_tc2) {
-      CUDA_TRY(cudaFuncSetAttribute(tc2_kernel_for(s->G.kernel, s->t2.nh), cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CUDA_TRY(cudaFuncSetAttribute(tc2_kernel_for(s->G.kernel, s->t2.nh, s->tb.nch), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
       occ = 1;
     } else if (use_tc) {

@@ -102,7 +102,11 @@ __device__ __forceinline__ void tc2_prune(uint64_t* arr, TopkSmem& ts, int KC, i
   for (int i = keep + t; i < n_tot; i += nt) arr[i] = KEY_NONE;
   named_sync(id, nt);
 }
-template <int PW, int KT, int NH>
+// NCH > 0: the number of K-chunks (Mp16 / 16) as a compile-time constant (16: M = 256, 8: M = 128);
+// the chunk loop then unrolls completely and every A-ring stage, R2 slot, mbarrier parity and TMEM
+// column offset becomes an immediate (no per-chunk address arithmetic on the FMA pipe).  NCH = 0:
+// any M <= 256, runtime indices.
+template <int PW, int KT, int NH, int NCH>
 __global__ void __launch_bounds__(PW * 32 + 64, 1)
 score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, CandList L) {
   constexpr int TC_PROD_WARPS = PW;
@@ -118,7 +122,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
   __shared__ int eoff_s[DMAX];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int Mp16 = TB.Mp16, nch = TB.nch, Kp = T2.Kp;
+  const int Mp16 = NCH > 0 ? NCH * TC_KCH : TB.Mp16, nch = NCH > 0 ? NCH : TB.nch, Kp = T2.Kp;
   unsigned long long* const trace = blockIdx.x == 0 ? g_tc2_trace : nullptr;
   auto TR = [&](int u, int ev) {
     if (trace != nullptr && lane == 0 && u < TC2_TR_TILES)
@@ -415,14 +419,17 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     };
 
     int n_cur = publish(0);
-    uint32_t g = 0;                                   // global chunk counter (A ring)
-    uint32_t gr = 0;                                  // global R2 group counter
     const uint32_t sOH = tc::smem_u32(oh_s);
     // Chunks [cb, ce) of tile u (cb a multiple of the R2 group size; ce == nch or a multiple of it):
     // R2 (+ SIMT features) -> k -> A ring; partial sums accumulate into the caller's registers.
+    // A-ring position of chunk c of tile u is u * nch + c and R2-group position u * ng + c / RG:
+    // derived, not counted, so that with a compile-time nch (multiple of NA and of 2 RG) every
+    // stage / slot / parity folds to a constant
     auto produce = [&](int u, int cb, int ce, unsigned long long& mu2, unsigned long long& sb2,
                        unsigned long long& kk2, float& vsq_run) {
       const uint32_t dq = lane_base + TC_JPT * jq;
+      const uint32_t gbase = static_cast<uint32_t>(u) * static_cast<uint32_t>(nch);
+      const uint32_t grbase = static_cast<uint32_t>(u) * static_cast<uint32_t>(ng);
       unsigned long long xb[NH > 0 ? NH : 1];                 // (x_h, x_h): broadcast over a point pair
 #pragma unroll
       for (int h = 0; h < NH; ++h) {
@@ -432,9 +439,11 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       const unsigned long long carg2 = f2_pack(c_arg, c_arg), c1_2 = f2_pack(ex_c1, ex_c1),
                                c0_2 = f2_pack(ex_c0, ex_c0), one2 = f2_pack(1.0f, 1.0f),
                                third2 = f2_pack(0.33333333333333333f, 0.33333333333333333f);
+#pragma unroll
         for (int c0 = cb; c0 < ce; c0 += TC2_RG) {
           // ---- one R2 group: the thread's 4 points of each of the 4 chunks are 16 contiguous
           // columns (T rows are permuted on the host), read with one load
+          const uint32_t gr = grbase + static_cast<uint32_t>(c0 / TC2_RG);
           const int rs = gr % TC2_RS;
           float rv[TC2_RG * TC_JPT];
           tc::mbar_wait(r_full + rs, (gr / TC2_RS) & 1u);
@@ -443,7 +452,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
           tc::fence_before_sync();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(r_empty + rs);
-          ++gr;
+          const uint32_t g = gbase + static_cast<uint32_t>(c0);
           // The whole group's math first (4 chunks x 2 packed point pairs: eight independent chains
           // the scheduler can interleave), then the A-stage waits and stores: the waits are asm
           // volatile and would otherwise fence every chunk's two chains off from the next chunk's.
@@ -524,8 +533,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
 #pragma unroll
           for (int cg = 0; cg < TC2_RG; ++cg) {
             if (c0 + cg >= nch) break;
-            if (lane == 0) tc::mbar_arrive(a_full + (g % TC2_NA));
-            ++g;
+            if (lane == 0) tc::mbar_arrive(a_full + ((g + cg) % TC2_NA));
           }
           // ---- accumulator column blocks made final by this group's a_empty waits:
           // [c0 - NA, c_last - NA]; one batched read (the last NA blocks are left to the epilogue)
@@ -583,7 +591,13 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       TR(t, 0);
       const int n_next = publish(t + 1);
       TR(t, 1);
-      produce(t, pre, nch, mu_c, sb_c, kk_c, vsq_c);
+      if (NCH > 0) {
+        constexpr int HEAD = NCH < TC2_NA ? NCH : TC2_NA;
+        if (pre == HEAD) produce(t, HEAD, NCH, mu_c, sb_c, kk_c, vsq_c);
+        else produce(t, 0, NCH, mu_c, sb_c, kk_c, vsq_c);
+      } else {
+        produce(t, pre, nch, mu_c, sb_c, kk_c, vsq_c);
+      }
       TR(t, 2);
       flush_part(t, mu_c, sb_c, kk_c);
       const float vsq_t = vsq_c;
@@ -591,7 +605,8 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       vsq_c = 0.f;
       pre = 0;
       if (n_next > 0) {
-        produce(t + 1, 0, head, mu_c, sb_c, kk_c, vsq_c);
+        if (NCH > 0) produce(t + 1, 0, NCH < TC2_NA ? NCH : TC2_NA, mu_c, sb_c, kk_c, vsq_c);
+        else produce(t + 1, 0, head, mu_c, sb_c, kk_c, vsq_c);
         pre = head;
       }
       TR(t, 3);
