@@ -93,6 +93,14 @@ typedef struct {
                             it must stay valid until the autoscout_topk / autoscout_topk_pool call
                             of this pool returns (certification may re-score recorded batches).
                             An entry >= n_cvi is scored as masked (-INF, raw UINT64_MAX). */
+  float* d_screen;       /* device, nullable, [4*count] in batch order, parity/debug output of the
+                            FP32 screen that admits candidates: mu, sigma^2, the
+                            screen score acq(mu, sigma^2) and its certified upper bound
+                            acq(mu - d_mu, sigma^2 + d_s2) + margin, exactly as the kernel uses them
+                            (independent of d_scores, which switches the kernel to an FP64
+                            acquisition).  Written by the one-hot tensor-core kernel (the path
+                            taken for M >= 64 or batches >= 2^20 candidates); untouched (NaN
+                            prefill is the caller's) for other paths and masked candidates. */
 } as_score_args;
 
 /* Parse and validate a space JSON document (schema: DESIGN.md §2), build the
@@ -100,6 +108,9 @@ typedef struct {
  * Source: SPEC.md:54-62 load_space; Table 1. */
 as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as_space** out);
 void autoscout_space_destroy(as_space* s);
+/* Sizes of the parsed space (host; out is caller-owned).  n_cvi counts the configurations that
+ * satisfy the canonical-inactive rule and the structural constraints ("each edge
+ * represents a valid refinement"; SPEC.md:90-98 enumerate, :109 world-size rule; reading R4). */
 as_status autoscout_space_info(const as_space* s, as_space_info* out);
 
 /* Append n profiled configurations (raw index, cost > 0 in objective units) and refit the GP on
@@ -113,12 +124,25 @@ as_status autoscout_observe_clear(as_space* s);
 /* Host introspection of the current fit: M, b (prior offset), f* (incumbent ln cost). */
 as_status autoscout_observe_info(const as_space* s, int32_t* m_out, double* b_out, double* fstar_out);
 
-/* Enqueue the scoring of a batch (one kernel launch + one pool-merge launch, asynchronous).
- * Candidates are generated from indices in registers; per-candidate outputs are optional.
- * Errors: INDEX_RANGE, NO_OBSERVATIONS, INVALID_ARG, STATE (host-only handle), CUDA. */
+/* Enqueue the scoring of a batch (generate + score + pool-merge launches, asynchronous): for every
+ * candidate index decode the configuration of the hierarchical space ("subsequent
+ * decisions are valid only under specific upstream decisions", :137, :171 masking function M(s)),
+ * apply validity (Table 1 gates PAPER.md:507, :510; SPEC.md:81-89 is_feasible; the resource check
+ * of the simulator), run the analytical simulator (reading R6: SPEC.md:486-497 and
+ * the paper's own simulators are regressions), score
+ * it against the profiled set (GP posterior + acquisition, readings R1, R9, R10; north_star), and
+ * keep the CTA top-k' for "the top-K configurations ... prioritized for re-evaluation"
+ * (PAPER.md:265).  Candidates are generated from indices in registers; per-candidate outputs are
+ * optional and caller-owned.  accumulate = 1 merges into the running pool and requires the same
+ * acq / kappa / xi as the pool's first batch.  A refit (observe, observe_clear, set_gp_hyper)
+ * empties the pool.
+ * Errors: INDEX_RANGE, NO_OBSERVATIONS, INVALID_ARG (also kappa < 0 or non-finite kappa / xi,
+ * mixed acquisition with accumulate), STATE (host-only handle), CUDA. */
 as_status autoscout_score_batch(as_space* s, const as_score_args* a, void* cuda_stream);
 
-/* Finalize: FP64 re-score of the running pool, order (score desc, raw asc), certification
+/* Finalize ("re-evaluation" of the top-K; ties by the lower index, SPEC.md:197,
+ * :506, reading R11): FP64 re-score of the running pool, order (score desc, raw asc), one entry
+ * per configuration (a configuration scored twice is returned once), certification
  * (doubles the pool and re-scores the recorded batches on failure).  Writes
  * n_out = min(k, #valid finite scores) entries to the host arrays raw_out/score_out (length >= k).
  * Synchronizes `cuda_stream`.  Errors: STATE (nothing scored), UNCERTIFIED, CUDA. */
@@ -140,7 +164,35 @@ as_status autoscout_topk_merge(const as_space* s, const void* pools, const int32
                                uint64_t* raw_out, double* score_out, int32_t* n_out,
                                int32_t* certified_out);
 
-/* Exact host introspection (parity and tests). */
+/* Device-resident sharding: the pools stay in device memory and
+ * are exchanged with ONE all_gather_into_tensor (NCCL over NVLink); only the final top-k is read
+ * back.  Packed pool = cap + 2 entries of {double score; uint64_t raw} (16 B):
+ *   [0] header: score = n (number of exported entries, as a double), raw = 1 if locally certified;
+ *   [1] cut: every candidate scored on this handle but not exported ranks after or equals it in
+ *       the total order (score desc, raw asc); score -INF if nothing was dropped;
+ *   [2, 2 + n) entries in the total order, one per configuration; the rest {-INF, UINT64_MAX}.
+ * topk_pool_device: FP64 refine of the running pool, device sort + de-duplication + pack into
+ *   d_pool_out (device, caller-owned, (cap + 2) * 16 bytes); grows k' and re-scores the recorded
+ *   batches while the local top-k is not certified (reads back 4 bytes per attempt).  Syncs the
+ *   stream.  Errors: STATE (nothing scored / host-only handle), INVALID_ARG, CUDA.
+ * topk_merge_device: merge n_pools packed pools laid out contiguously in d_pools (device,
+ *   n_pools * (cap + 2) entries: the all-gather output) into d_out (device, k + 2 entries, same
+ *   layout: header {n, certified}, the best cut of all pools, the global top-k).  Certified iff the
+ *   k-th merged entry ranks strictly before every pool's cut (PAPER.md:265 top-K re-evaluation;
+ *   ties SPEC.md:197).  Asynchronous on cuda_stream. */
+as_status autoscout_topk_pool_device(as_space* s, int32_t k, void* d_pool_out, int32_t cap, void* cuda_stream);
+as_status autoscout_topk_merge_device(as_space* s, const void* d_pools, int32_t n_pools, int32_t cap, int32_t k,
+                                      void* d_out, void* cuda_stream);
+
+/* Exact host introspection (parity and tests).
+ * decode: digits of a raw index by mixed radix, first-declared feature most significant (reading
+ *   R2, "deterministic order"); digits_out host [n_features]; valid_out = 1 iff the
+ *   configuration is canonical (inactive features at their default), meets
+ *   every constraint and passes the resource check.  AS_ERR_INDEX_RANGE if raw >= n_raw.
+ * cvi_to_raw: raw index of CVI position cvi (the cvi-th valid-structure configuration in raw
+ *   order, reading R4; SPEC.md:90-98 enumerate).  AS_ERR_INDEX_RANGE if cvi >= n_cvi.
+ * sample_to_cvi: the SAMPLE-mode position pi_seed(ordinal) (reading R3, a Feistel bijection of
+ *   [0, n_cvi)).  AS_ERR_INDEX_RANGE if ordinal >= n_cvi. */
 as_status autoscout_decode(const as_space* s, uint64_t raw, int32_t* digits_out, int32_t* valid_out);
 as_status autoscout_cvi_to_raw(const as_space* s, uint64_t cvi, uint64_t* raw_out);
 as_status autoscout_sample_to_cvi(const as_space* s, uint64_t seed, uint64_t ordinal, uint64_t* cvi_out);
@@ -199,12 +251,16 @@ as_status autoscout_subtree_range(const as_space* s, const int32_t* digits, int3
  * AS_ERR_CAPACITY (n_out still set) if n_out > cap; AS_ERR_INDEX_RANGE if raw >= n_raw.
  * The base configuration itself need not be valid.  Score the result with AS_MODE_LIST. */
 as_status autoscout_neighbors(const as_space* s, uint64_t raw, uint64_t* cvi_out, int32_t cap, int32_t* n_out);
-/* FP64 simulator + resource check of one configuration (host).  ok_out = G4 passes. */
+/* FP64 simulator + resource check of one configuration (host; reading R6: SPEC.md:486-497, SURVEY.md
+ * A.3/A.4).  ok_out = G4 passes (memory <= capacity).  AS_ERR_INDEX_RANGE if raw >= n_raw. */
 as_status autoscout_simulate(const as_space* s, uint64_t raw, double* cost_out, double* mem_out,
                              int32_t* ok_out);
-/* Mask kernel: validity bit of every raw index in [raw_begin, raw_begin+count) -> d_bits
- * (device, (count+31)/32 words, bit i of word w = raw_begin+32w+i); d_valid_count (device,
- * nullable) += number of valid.  Valid = canonical-inactive + structural constraints + resource. */
+/* Mask kernel (the masking function M(s) of PAPER.md:171 over raw index ranges, for exhaustive
+ * parity with enumeration): validity bit of every raw index in
+ * [raw_begin, raw_begin+count) -> d_bits (device, (count+31)/32 words, bit i of word w =
+ * raw_begin+32w+i); d_valid_count (device, nullable) += number of valid.  Valid = canonical-
+ * inactive + structural constraints (reading R5) + resource check
+ * (reading R7).  AS_ERR_INDEX_RANGE if the range exceeds n_raw. */
 as_status autoscout_mask_range(as_space* s, uint64_t raw_begin, uint64_t count, uint32_t* d_bits,
                                uint64_t* d_valid_count, void* cuda_stream);
 

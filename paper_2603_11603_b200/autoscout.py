@@ -53,7 +53,7 @@ class ScoreArgs(ctypes.Structure):
                 ("count", ctypes.c_uint64), ("seed", ctypes.c_uint64), ("kappa", ctypes.c_double),
                 ("xi", ctypes.c_double), ("k", ctypes.c_int32), ("accumulate", ctypes.c_int32),
                 ("d_scores", ctypes.c_void_p), ("d_raw", ctypes.c_void_p), ("d_valid_count", ctypes.c_void_p),
-                ("d_positions", ctypes.c_void_p)]
+                ("d_positions", ctypes.c_void_p), ("d_screen", ctypes.c_void_p)]
 
 
 class AutoscoutError(RuntimeError):
@@ -81,6 +81,8 @@ def _load():
         "autoscout_topk": ([P, I32, pU64, pD, pI32, P], I32),
         "autoscout_topk_pool": ([P, I32, P, I32, pI32, P, P], I32),
         "autoscout_topk_merge": ([P, P, pI32, P, I32, I32, I32, pU64, pD, pI32, pI32], I32),
+        "autoscout_topk_pool_device": ([P, I32, P, I32, P], I32),
+        "autoscout_topk_merge_device": ([P, P, I32, I32, I32, P, P], I32),
         "autoscout_decode": ([P, U64, pI32, pI32], I32),
         "autoscout_cvi_to_raw": ([P, U64, pU64], I32),
         "autoscout_sample_to_cvi": ([P, U64, U64, pU64], I32),
@@ -284,7 +286,7 @@ class Space:
     # --------------------------------------------------------------- scoring
     def score_batch(self, mode="range", begin=0, count=None, seed=0, acq="ei", k=32, kappa=None, xi=None,
                     accumulate=False, d_scores=None, d_raw=None, d_valid_count=None, d_positions=None,
-                    stream=None):
+                    d_screen=None, stream=None):
         """mode "list": candidate j is CVI position d_positions[begin + j] (device uint64 tensor the
         caller keeps alive until topk); count defaults to len(d_positions) - begin."""
         gp = self.doc.get("gp", {})
@@ -294,7 +296,7 @@ class Space:
                           if count is None else count), int(seed),
                       float(gp.get("kappa", 2.0) if kappa is None else kappa),
                       float(gp.get("xi", 0.0) if xi is None else xi), int(k), 1 if accumulate else 0,
-                      _ptr(d_scores), _ptr(d_raw), _ptr(d_valid_count), _ptr(d_positions))
+                      _ptr(d_scores), _ptr(d_raw), _ptr(d_valid_count), _ptr(d_positions), _ptr(d_screen))
         _check(_LIB.autoscout_score_batch(self.h, ctypes.byref(a), _stream_ptr(stream)))
 
     def topk(self, k, stream=None, allow_uncertified=False):
@@ -314,6 +316,26 @@ class Space:
         _check(_LIB.autoscout_topk_pool(self.h, int(k), buf.ctypes.data_as(ctypes.c_void_p), int(cap),
                                         ctypes.byref(n), cut.ctypes.data_as(ctypes.c_void_p), _stream_ptr(stream)))
         return buf, n.value, cut
+
+    def topk_pool_device(self, k, cap, out=None, stream=None):
+        """Refined local pool packed on the device -> int64 tensor [(cap + 2) * 2] (16-byte entries:
+        header {n, certified}, cut, cap entries; include/autoscout.h).  No host copy of the pool."""
+        import torch
+        if out is None:
+            out = torch.empty((cap + 2) * 2, dtype=torch.int64, device=torch.device("cuda", self.device))
+        _check(_LIB.autoscout_topk_pool_device(self.h, int(k), _ptr(out), int(cap), _stream_ptr(stream)))
+        return out
+
+    def topk_merge_device(self, d_pools, n_pools, cap, k, stream=None):
+        """Merge gathered packed pools on the device; one D2H of the (k + 2)-entry result.
+        -> (list[(raw, score)], certified)."""
+        import torch
+        out = torch.empty((k + 2) * 2, dtype=torch.int64, device=d_pools.device)
+        _check(_LIB.autoscout_topk_merge_device(self.h, _ptr(d_pools), int(n_pools), int(cap), int(k), _ptr(out),
+                                                _stream_ptr(stream)))
+        ent = np.ascontiguousarray(out.cpu().numpy()).view(ENTRY_DTYPE)
+        n, cert = int(ent[0]["score"]), bool(ent[0]["raw"])
+        return [(int(ent[2 + i]["raw"]), float(ent[2 + i]["score"])) for i in range(n)], cert
 
     def mask_range(self, raw_begin, count, d_bits, d_valid_count=None, stream=None):
         _check(_LIB.autoscout_mask_range(self.h, int(raw_begin), int(count), _ptr(d_bits), _ptr(d_valid_count),

@@ -16,6 +16,7 @@
 #include "kernels_tc.cuh"
 #include "kernels_tc2.cuh"
 #include "kernels_lml.cuh"
+#include "kernels_pool.cuh"
 #include "space.hpp"
 
 using namespace as;
@@ -215,6 +216,8 @@ struct as_space {
   uint64_t *d_pool = nullptr, *d_cut = nullptr, *d_valid = nullptr;
   int* d_pool_n = nullptr;
   double* d_ref_score = nullptr;
+  PoolEntry* d_merge_scratch = nullptr;   // device merge of large gathered pools (> 96 KB)
+  size_t merge_scratch_n = 0;
   uint64_t* d_ref_raw = nullptr;
   std::vector<as_score_args> batches;
   bool scored = false;
@@ -627,6 +630,7 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
   A.kappa = a.kappa;
   A.xi = a.xi;
   A.d_scores = a.d_scores;
+  A.d_screen = a.d_screen;
   A.d_raw = a.d_raw;
   A.d_valid_count = a.d_valid_count;
   CtaOut out{s->d_lists, s->d_counts, s->d_drops, s->d_valid, s->KC, P};
@@ -685,7 +689,18 @@ as_status refine_pool(as_space* s, int acq, double kappa, double xi, cudaStream_
   for (int e = 0; e < n_pool; ++e)
     if (std::isfinite(sc[e])) ent.push_back({sc[e], rw[e]});
   std::sort(ent.begin(), ent.end(), entry_less);
+  // a configuration scored more than once (repeated LIST positions, overlapping accumulated
+  // batches) has one FP64 score: equal raws are adjacent after the sort, keep one
+  ent.erase(std::unique(ent.begin(), ent.end(), [](const Entry& x, const Entry& y) { return x.raw == y.raw; }),
+            ent.end());
   return AS_OK;
+}
+
+// A refit (observe, observe_clear, set_gp_hyper) changes every score: the running pool and the
+// recorded batches belong to the previous fit, so topk needs a new score_batch first.
+void invalidate_pool(as_space* s) {
+  s->scored = false;
+  s->batches.clear();
 }
 
 as_status rescore_all(as_space* s, cudaStream_t st) {
@@ -891,7 +906,7 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
     if ((r = dalloc(&s->d_pool, KC_CAP, s->owned)) != AS_OK) return cleanup(r);
     if ((r = dalloc(&s->d_pool_n, 1, s->owned)) != AS_OK) return cleanup(r);
     if ((r = dalloc(&s->d_cut, 1, s->owned)) != AS_OK) return cleanup(r);
-    if ((r = dalloc(&s->d_valid, 1, s->owned)) != AS_OK) return cleanup(r);
+    if ((r = dalloc(&s->d_valid, 2, s->owned)) != AS_OK) return cleanup(r);   // [0] valid count, [1] pool flag
     if ((r = dalloc(&s->d_ref_score, KC_CAP, s->owned)) != AS_OK) return cleanup(r);
     if ((r = dalloc(&s->d_ref_raw, KC_CAP, s->owned)) != AS_OK) return cleanup(r);
     if (cudaMallocHost(reinterpret_cast<void**>(&s->h_stage), 16 + static_cast<size_t>(KC_CAP) * 16) != cudaSuccess)
@@ -915,6 +930,7 @@ void autoscout_space_destroy(as_space* s) {
     cudaSetDevice(s->device);
     for (void* p : s->owned) cudaFree(p);
     if (s->h_stage) cudaFreeHost(s->h_stage);
+    if (s->d_merge_scratch) cudaFree(s->d_merge_scratch);
     if (s->d_lists) cudaFree(s->d_lists);
     if (s->d_counts) cudaFree(s->d_counts);
     if (s->d_drops) cudaFree(s->d_drops);
@@ -1002,6 +1018,7 @@ as_status autoscout_observe(as_space* s, const uint64_t* raw_idx, const double* 
   s->obs_cost = std::move(all_cost);
   s->obs_sim = std::move(all_sim);
   s->fit = std::move(fit);
+  invalidate_pool(s);   // the running pool was screened under the previous fit
   const as_status ur = upload_gp(s, static_cast<cudaStream_t>(cuda_stream));
   if (ur == AS_OK && s->ens.on) s->fit_upload_bytes += s->ens.tab.size() * sizeof(double);
   return ur;
@@ -1017,6 +1034,7 @@ as_status autoscout_observe_clear(as_space* s) {
   gp_fit(s->H, {}, {}, {}, {}, s->fit);
   s->ens = EnsembleFit{};
   s->D.ens_on = 0;
+  invalidate_pool(s);
   return upload_gp(s, nullptr);
 }
 
@@ -1039,12 +1057,21 @@ as_status autoscout_score_batch(as_space* s, const as_score_args* a, void* cuda_
     return fail(AS_ERR_INDEX_RANGE, "LIST mode on a space without valid configurations");
   if (a->acq < AS_ACQ_EI || a->acq > AS_ACQ_SIM) return fail(AS_ERR_INVALID_ARG, "bad acquisition");
   if (a->k < 1 || a->k > 1024) return fail(AS_ERR_INVALID_ARG, "k must be in [1, 1024]");
+  // the screen's upper bound evaluates LCB at s2 + d_s2 and EI at mu - d_mu: monotone only for
+  // kappa >= 0; non-finite kappa / xi would void the certificate
+  if (!std::isfinite(a->kappa) || !std::isfinite(a->xi) || a->kappa < 0.0f)
+    return fail(AS_ERR_INVALID_ARG, "kappa must be finite and >= 0, xi finite");
   if (a->mode != AS_MODE_LIST && (a->begin > s->H.n_cvi || a->count > s->H.n_cvi - a->begin))
     return fail(AS_ERR_INDEX_RANGE, "batch exceeds [0, n_cvi)");
   if (a->acq == AS_ACQ_EI && s->G.M == 0) return fail(AS_ERR_NO_OBSERVATIONS, "EI needs at least one observation");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   CUDA_TRY(cudaSetDevice(s->device));
   const bool reset = !a->accumulate || !s->scored;
+  if (!reset) {
+    const as_score_args& b0 = s->batches.front();
+    if (a->acq != b0.acq || a->kappa != b0.kappa || a->xi != b0.xi)
+      return fail(AS_ERR_INVALID_ARG, "accumulate = 1 needs the acquisition, kappa and xi of the pool's first batch");
+  }
   if (reset) {
     s->batches.clear();
     s->KC = std::min(a->k + std::max(a->k, 64), s->KC_max);
@@ -1054,6 +1081,7 @@ as_status autoscout_score_batch(as_space* s, const as_score_args* a, void* cuda_
   rec.d_scores = nullptr;
   rec.d_raw = nullptr;
   rec.d_valid_count = nullptr;
+  rec.d_screen = nullptr;
   s->batches.push_back(rec);
   as_status r = launch_batch(s, *a, reset, st);
   if (r != AS_OK) return r;
@@ -1136,6 +1164,67 @@ as_status autoscout_topk_merge(const as_space* s, const void* pools, const int32
   return cert ? AS_OK : fail(AS_ERR_UNCERTIFIED, "merged top-k could not be certified");
 }
 
+as_status autoscout_topk_pool_device(as_space* s, int32_t k, void* d_pool_out, int32_t cap, void* cuda_stream) {
+  if (!s || !d_pool_out || cap < 1 || k < 1) return fail(AS_ERR_INVALID_ARG, "bad arguments");
+  if (s->device < 0) return fail(AS_ERR_STATE, "host-only handle");
+  if (!s->scored || s->batches.empty()) return fail(AS_ERR_STATE, "nothing scored");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  CUDA_TRY(cudaSetDevice(s->device));
+  const as_score_args& a0 = s->batches.front();
+  int* h_flag = reinterpret_cast<int*>(s->h_stage);   // pinned; refine_pool is not running concurrently
+  for (;;) {
+    const int blocks = (s->KC + REFINE_WARPS - 1) / REFINE_WARPS;
+    const size_t rsm = static_cast<size_t>(REFINE_WARPS) * std::max(s->G.M, 1) * sizeof(double);
+    refine_kernel<<<blocks, REFINE_WARPS * 32, rsm, st>>>(s->D, s->G, s->d_pool, s->d_pool_n, a0.acq, a0.kappa,
+                                                          a0.xi, s->d_ref_score, s->d_ref_raw);
+    CUDA_TRY(cudaGetLastError());
+    ++s->n_launches;
+    const int n2 = next_pow2_h(std::max(s->KC, 2));
+    CUDA_TRY(cudaFuncSetAttribute(pool_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, n2 * 16));
+    pool_pack_kernel<<<1, POOL_THREADS, static_cast<size_t>(n2) * 16, st>>>(
+        s->D, s->d_ref_score, s->d_ref_raw, s->d_pool_n, s->d_cut, n2, k, cap, static_cast<PoolEntry*>(d_pool_out),
+        reinterpret_cast<int*>(s->d_valid) + 2);
+    CUDA_TRY(cudaGetLastError());
+    ++s->n_launches;
+    // 4 bytes back (the local certificate), not the pool: grow k' and re-score if it failed
+    CUDA_TRY(cudaMemcpyAsync(h_flag, reinterpret_cast<int*>(s->d_valid) + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (*h_flag || s->KC * 2 > s->KC_max) return AS_OK;
+    s->KC *= 2;
+    as_status r = rescore_all(s, st);
+    if (r != AS_OK) return r;
+  }
+}
+
+as_status autoscout_topk_merge_device(as_space* s, const void* d_pools, int32_t n_pools, int32_t cap, int32_t k,
+                                      void* d_out, void* cuda_stream) {
+  if (!s || !d_pools || !d_out || n_pools < 1 || cap < 1 || k < 1) return fail(AS_ERR_INVALID_ARG, "bad arguments");
+  if (s->device < 0) return fail(AS_ERR_STATE, "host-only handle");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  CUDA_TRY(cudaSetDevice(s->device));
+  const int n2 = next_pow2_h(std::max(n_pools * cap, 2));
+  const size_t bytes = static_cast<size_t>(n2) * sizeof(PoolEntry);
+  PoolEntry* gbuf = nullptr;
+  size_t smem = 0;
+  if (bytes <= 96 * 1024) {
+    smem = bytes;
+    CUDA_TRY(cudaFuncSetAttribute(pool_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  } else {
+    if (s->merge_scratch_n < static_cast<size_t>(n2)) {
+      if (s->d_merge_scratch) cudaFree(s->d_merge_scratch);
+      s->d_merge_scratch = nullptr;
+      CUDA_TRY(cudaMalloc(&s->d_merge_scratch, bytes));
+      s->merge_scratch_n = n2;
+    }
+    gbuf = s->d_merge_scratch;
+  }
+  pool_merge_kernel<<<1, POOL_THREADS, smem, st>>>(static_cast<const PoolEntry*>(d_pools), n_pools, cap, k, n2, gbuf,
+                                                   static_cast<PoolEntry*>(d_out));
+  CUDA_TRY(cudaGetLastError());
+  ++s->n_launches;
+  return AS_OK;
+}
+
 as_status autoscout_decode(const as_space* s, uint64_t raw, int32_t* digits_out, int32_t* valid_out) {
   if (!s) return fail(AS_ERR_INVALID_ARG, "null argument");
   int dig[DMAX];
@@ -1210,12 +1299,9 @@ as_status autoscout_gp_lml(as_space* s, const double* hyp, int32_t n_set, double
   return AS_OK;
 }
 
-as_status autoscout_set_gp_hyper(as_space* s, const double* lengthscale, double sf2, double sn2) {
-  if (!s || !lengthscale) return fail(AS_ERR_INVALID_ARG, "null argument");
-  for (int j = 0; j < s->H.d; ++j)
-    if (!(lengthscale[j] > 0.0) || !std::isfinite(lengthscale[j])) return fail(AS_ERR_INVALID_ARG, "lengthscale must be > 0");
-  if (!(sf2 > 0.0) || !(sn2 > 0.0) || !std::isfinite(sf2) || !std::isfinite(sn2))
-    return fail(AS_ERR_INVALID_ARG, "sf2 and sn2 must be finite and > 0");
+namespace {
+// hyper-parameters -> host feature tables and their device copies
+as_status apply_gp_hyper(as_space* s, const double* lengthscale, double sf2, double sn2) {
   s->H.ls.assign(lengthscale, lengthscale + s->H.d);
   s->H.sf2 = sf2;
   s->H.sn2 = sn2;
@@ -1225,12 +1311,35 @@ as_status autoscout_set_gp_hyper(as_space* s, const double* lengthscale, double 
     CUDA_TRY(cudaMemcpy(const_cast<double*>(s->D.xt64), s->H.xt64.data(), s->H.xt64.size() * sizeof(double), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(const_cast<float*>(s->D.xt32), s->H.xt32.data(), s->H.xt32.size() * sizeof(float), cudaMemcpyHostToDevice));
   }
-  // refit the current observed set under the new hyper-parameters
+  return AS_OK;
+}
+}  // namespace
+
+as_status autoscout_set_gp_hyper(as_space* s, const double* lengthscale, double sf2, double sn2) {
+  if (!s || !lengthscale) return fail(AS_ERR_INVALID_ARG, "null argument");
+  for (int j = 0; j < s->H.d; ++j)
+    if (!(lengthscale[j] > 0.0) || !std::isfinite(lengthscale[j])) return fail(AS_ERR_INVALID_ARG, "lengthscale must be > 0");
+  if (!(sf2 > 0.0) || !(sn2 > 0.0) || !std::isfinite(sf2) || !std::isfinite(sn2))
+    return fail(AS_ERR_INVALID_ARG, "sf2 and sn2 must be finite and > 0");
+  const std::vector<double> old_ls = s->H.ls;
+  const double old_sf2 = s->H.sf2, old_sn2 = s->H.sn2;
   const std::vector<uint64_t> raws = s->obs_raw;
   const std::vector<double> costs = s->obs_cost;
-  as_status r = autoscout_observe_clear(s);
-  if (r != AS_OK || raws.empty()) return r;
-  return autoscout_observe(s, raws.data(), costs.data(), static_cast<int64_t>(raws.size()), nullptr);
+  as_status r = apply_gp_hyper(s, lengthscale, sf2, sn2);
+  // refit the current observed set under the new hyper-parameters (observe_clear + observe)
+  if (r == AS_OK) r = autoscout_observe_clear(s);
+  if (r == AS_OK && !raws.empty())
+    r = autoscout_observe(s, raws.data(), costs.data(), static_cast<int64_t>(raws.size()), nullptr);
+  if (r != AS_OK) {
+    // e.g. AS_ERR_NUMERIC from the Cholesky: restore the previous hyper-parameters and the
+    // previous fit of the same observations (which succeeded before), keep the error
+    const std::string why = g_err;
+    apply_gp_hyper(s, old_ls.data(), old_sf2, old_sn2);
+    autoscout_observe_clear(s);
+    if (!raws.empty()) autoscout_observe(s, raws.data(), costs.data(), static_cast<int64_t>(raws.size()), nullptr);
+    g_err = why;
+  }
+  return r;
 }
 
 namespace {

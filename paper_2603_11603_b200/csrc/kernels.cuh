@@ -87,6 +87,7 @@ struct BatchArgs {
   uint64_t* d_valid_count;
   const uint64_t* list;   // LIST mode: CVI positions (entries >= n_cvi are masked)
   uint64_t n_cvi;
+  float* d_screen;        // nullable [4 count]: mu, s2, screen, upper bound of the FP32 screen
 };
 
 // a0: candidate j of the batch -> CVI position.  A LIST entry outside [0, n_cvi) is

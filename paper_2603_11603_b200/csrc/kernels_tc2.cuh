@@ -8,18 +8,24 @@
 //       Kp <= 64) are added on the SIMT pipes instead: (x_f - o_jf)^2 in FP32, same 2^s scale.
 //       One R2 MMA group covers 4 K-chunks (N = 64): per-instruction cost is flat below N = 64
 //       (tools/mma_bench.cu), so wide groups are what keeps the tensor pipe and the issuing warp free.
-//   (2) v = L^-1 k  (kind::tf32, 3xTF32 split) exactly as score_tc_kernel (kernels_tc.cuh).
+//   (2) v = L^-1 k  (kind::f16, 3-term FP16 split hi.hi + hi.lo + lo.hi, FP32 accumulate): k is
+//       produced scaled by 2^ek and split by mantissa mask (hi) + exact remainder (lo), stored to
+//       TMEM as packed f16x2 (A operand from TMEM); L^-1^T chunks are host-split FP16 hi + lo.
 // The producers therefore no longer evaluate sum_f (x_f - o_jf)^2 on the FP32 pipe (2 d FP32 ops
-// per candidate x observed pair); they read R2 from TMEM and evaluate k(r) only.
+// per candidate x observed pair); they read R2 from TMEM and evaluate k(r) only.  Candidates come
+// from the compact list of gen_kernel (kernels_gen.cuh): decode, mask and simulator run there.
 //
-// Warp roles (544 threads, 1 CTA per SM):
-//   warps 0-15  producers: phase 0 (decode + mask + simulator -> queue), publish tile t+1 (meta +
-//               E rows) BEFORE the chunk loop of tile t, so the R2 MMAs of t+1 overlap tile t;
-//               chunk loop: R2 chunk from TMEM -> k -> TF32 hi/lo -> A ring (TMEM); epilogue.
+// Warp roles (576 threads, 1 CTA per SM):
+//   warps 0-15  producers: publish tile t+1 (meta + E rows + SIMT-feature values from the staged
+//               list records) BEFORE the chunk loop of tile t, so the R2 MMAs of t+1 overlap tile t;
+//               chunk loop: R2 group from TMEM -> k -> FP16 hi/lo -> A ring (TMEM); head start on
+//               tile t+1; epilogue (|v|^2 of the last column blocks; warps 0-3 finalise the rows:
+//               FP32 screen + certified bound, lazy CTA top-k').
 //   warp 16     MMA issuer (warp-converged, one elected lane issues): R2 groups ahead of the
 //               L^-1 chunks in one instruction stream.
-//   warp 17     loader: bulk copies of the L^-1 chunks, T groups and staged list records.
-// TMEM: D [Mp16] | A ring [4 x 32] | R2 ring [2 groups x 64]  (Mp16 <= 256 -> <= 512 columns).
+//   warp 17     loader: bulk copies of the L^-1 chunks, T groups and staged list records, and the
+//               zero-fill of used one-hot buffers.
+// TMEM: D [Mp16] | A ring [8 x 16] | R2 ring [2 groups x 64]  (Mp16 <= 256 -> <= 512 columns).
 #pragma once
 #include "kernels_gen.cuh"
 #include "kernels_tc.cuh"
@@ -309,6 +315,12 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         float ub = acquisition32(A.acq, mu - d_mu, s2 + d_s2, m0f, fstar, static_cast<float>(A.xi),
                                  static_cast<float>(A.kappa), m2);
         ub += m2;
+        if (A.d_screen) {   // parity / debug output of the screen (never on the bench path)
+          float m3;
+          const float scr = acquisition32(A.acq, mu, s2, m0f, fstar, static_cast<float>(A.xi),
+                                          static_cast<float>(A.kappa), m3);
+          *reinterpret_cast<float4*>(A.d_screen + 4ull * m_j[ms * TC_ROWS + row]) = make_float4(mu, s2, scr, ub);
+        }
         TR(u, 14);
         if (A.d_scores) {
           const double mud = cm0 + G.b + static_cast<double>(mu32);

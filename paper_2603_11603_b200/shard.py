@@ -3,10 +3,16 @@ the per-GPU top-k with ONE all-gather.
 
 The candidate positions [begin, begin+count) are cut into `world` contiguous shares (remainder to
 the lowest ranks); each rank scores its share on its own device, refines its pool in FP64 and
-exports it with an upper bound ("cut") on every candidate it dropped.  One
-`torch.distributed.all_gather` of the packed pools (NCCL over NVLink on GPUs, gloo in CPU tests)
-gives every rank all pools; `autoscout_topk_merge` (host C++) merges them with the total order
-(score desc, raw asc) and certifies globally.  Every rank ends with the identical top-k.
+exports it with an upper bound ("cut") on every candidate it dropped.
+
+Two exchanges, same result:
+  * device-resident (GPU ranks, the bench path): `topk_pool_device` packs the pool in device
+    memory, ONE `all_gather_into_tensor` (NCCL over NVLink / NVSwitch) concatenates the ranks'
+    buffers, `topk_merge_device` merges and certifies on the device; only the k-entry result is
+    read back -- no host bounce of any pool;
+  * host arrays (`gather_merge`; gloo in the CPU tests): `topk_pool` to host, `all_gather`, host
+    C++ `topk_merge`.
+Every rank ends with the identical top-k.
 """
 
 from __future__ import annotations
@@ -65,3 +71,25 @@ def score_topk_sharded(space, k, begin, count, rank, world, mode="sample", seed=
     cap = cap or (k + max(k, 64))
     pool, npool, cut = space.topk_pool(k, cap, stream=stream)
     return gather_merge(pool, npool, cut, k, group=group, device=device)
+
+
+def gather_merge_device(space, k, cap, group=None, stream=None):
+    """Device-resident exchange: pack the local pool on the device, one all_gather_into_tensor,
+    merge on the device.  -> (top-k list, certified)."""
+    import torch
+    import torch.distributed as dist
+
+    mine = space.topk_pool_device(k, cap, stream=stream)
+    world = dist.get_world_size(group)
+    gathered = torch.empty(world * mine.numel(), dtype=mine.dtype, device=mine.device)
+    dist.all_gather_into_tensor(gathered, mine, group=group)
+    return space.topk_merge_device(gathered, world, cap, k, stream=stream)
+
+
+def score_topk_sharded_device(space, k, begin, count, rank, world, mode="sample", seed=0, acq="ei", cap=None,
+                              group=None, stream=None):
+    """GPU ranks: score this rank's share, then the device-resident exchange.  -> (top-k, certified)."""
+    lo, n = shard_range(begin, count, rank, world)
+    space.score_batch(mode=mode, begin=lo, count=n, seed=seed, acq=acq, k=k, stream=stream)
+    cap = cap or (k + max(k, 64))
+    return gather_merge_device(space, k, cap, group=group, stream=stream)

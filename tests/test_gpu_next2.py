@@ -117,7 +117,13 @@ def test_list_mode_equals_sample_mode_at_scale():
     m = len(pos)
     sc_l = torch.empty(m, dtype=torch.float32, device="cuda")
     sp.score_batch(mode="list", begin=0, count=m, acq="ei", k=32, d_scores=sc_l, d_positions=d_pos)
-    sp.topk(32)
+    top_l = sp.topk(32)          # raises on AS_ERR_UNCERTIFIED
     torch.cuda.synchronize()
     assert np.array_equal(sc_l.cpu().numpy(), sc_s.cpu().numpy()[0:n:997])
     assert len(top_s) == 32
+    # the LIST pool's certified top-k equals the oracle's exact top-k over the same positions
+    from oracle import batch as OB, parallel as OP
+    rec = OP.score_positions(o, OB.Unranker(o), fit, pos.astype(np.int64), acq="ei")
+    ref = OP._topk_of(rec["raw"], rec["score"], 32)
+    assert [r for r, _ in top_l] == [r for r, _ in ref]
+    assert np.allclose([s for _, s in top_l], [s for _, s in ref], rtol=1e-12, atol=0)
