@@ -217,75 +217,102 @@ def observed_with_library(sp, M, seed=0):
                                  lambda r: sp.simulate(r)[0])
 
 
-def cpu_baseline(cfg, raws, costs, seconds, seed=0):
-    """The oracle as it stands, on a bounded sample of the same workload (BLAS pinned to 1 thread)."""
-    from threadpoolctl import threadpool_limits
-    from oracle import run, space as S
-    doc = load_doc(cfg)
-    b = doc["bench"]
-    with threadpool_limits(1):
-        o = S.load_space(os.path.join(ROOT, "spaces", f"{cfg}.json"))
-        fit = run.observed_fit(o, raws, costs)
-        t0 = time.perf_counter()
-        done = 0
-        chunk = 2048
-        n_all = o.n_cvi() if b["mode"] == "range" else int(b.get("count", o.n_cvi()))
-        while time.perf_counter() - t0 < seconds:
-            start = done % n_all                      # small spaces: wrap around the batch
-            c = min(chunk, n_all - start)
-            run.score_batch(o, fit, b["mode"], start, c, seed, acq=b["acq"])
-            done += c
-        dt = time.perf_counter() - t0
-    return {"value": done / dt, "unit": "candidates/s", "cores": 1, "kind": "oracle",
-            "sample": f"{cfg} {b['mode']}: {done} candidates of the bench batch from ordinal 0"
-                      f"{' (wrapping around the whole space)' if done > n_all else ''} (seed {seed}), "
-                      f"{dt:.1f} s, numpy/BLAS 1 thread; top-k sort excluded (bounded sample)"}
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
-def run_reference(args):
-    """--impl reference: the oracle, timed on bounded samples of the same workload."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    from threadpoolctl import threadpool_limits
-    from oracle import run, space as S
+def _oracle_setup(cfg, raws=None, costs=None):
+    from oracle import run, sim, space as S
     import synthgen
-    from oracle import sim
-    cfg = args.config
     doc = load_doc(cfg)
     b = doc["bench"]
     o = S.load_space(os.path.join(ROOT, "spaces", f"{cfg}.json"))
-
-    def unrank(p):
-        dg = o.cvi_unrank(p)
-        return o.encode_raw(dg), dg
-
-    raws, costs = synthgen.observed_set(b["M"], 0, o.n_cvi(), [f.n for f in o.features], unrank,
-                                        lambda r: bool(sim.simulate(o, [o.decode_raw(r)])[1][0]),
-                                        lambda r: float(sim.simulate(o, [o.decode_raw(r)])[0][0]))
+    if raws is None:
+        def unrank(p):
+            dg = o.cvi_unrank(p)
+            return o.encode_raw(dg), dg
+        raws, costs = synthgen.observed_set(b["M"], 0, o.n_cvi(), [f.n for f in o.features], unrank,
+                                            lambda r: bool(sim.simulate(o, [o.decode_raw(r)])[1][0]),
+                                            lambda r: float(sim.simulate(o, [o.decode_raw(r)])[0][0]))
+    fit = run.observed_fit(o, raws, costs)
     n_all = o.n_cvi() if b["mode"] == "range" else int(b.get("count", o.n_cvi()))
-    chunk = min(1024, n_all)
+    return o, fit, b, n_all
+
+
+def cpu_baseline(cfg, raws, costs, seconds, seed=0):
+    """The oracle as it stands on the host cores: the batch oracle (oracle/batch.py forms of the scalar
+    definitions, pinned to them) over ALL cores on a bounded sample of the bench batch, plus the scalar
+    oracle on one core (BLAS pinned to 1 thread) for reference."""
+    from threadpoolctl import threadpool_limits
+    from oracle import parallel as OP, run
+    o, fit, b, n_all = _oracle_setup(cfg, raws, costs)
+    cores = OP.cores()
+    # all cores: a fixed sample of contiguous ordinals (about `seconds` of work on a 16-core host)
+    sample = int(min(n_all, max(1 << 16, 400_000 * cores * seconds / 16.0)))
+    t0 = time.perf_counter()
+    OP.topk(o, fit, b["mode"], 0, sample, b["k"], seed=seed, acq=b["acq"], procs=cores)
+    dt = time.perf_counter() - t0
+    # one core, scalar oracle (round-1 figure), a few seconds
     with threadpool_limits(1):
-        fit = run.observed_fit(o, raws, costs)
-        times = []
-        for i in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            start = (i * chunk) % n_all                 # small spaces: wrap around the batch
-            rec = run.score_batch(o, fit, b["mode"], start, min(chunk, n_all - start), 0, acq=b["acq"])
-            run.topk(rec, b["k"])
-            dt = time.perf_counter() - t0
-            if i >= args.warmup:
-                times.append(dt)
-    ms = 1e3 * sum(times) / len(times)
-    v = chunk / (ms / 1e3)
+        t1 = time.perf_counter()
+        done = 0
+        chunk = 2048
+        while time.perf_counter() - t1 < min(seconds, 5.0):
+            start = done % n_all
+            c = min(chunk, n_all - start)
+            run.score_batch(o, fit, b["mode"], start, c, seed, acq=b["acq"])
+            done += c
+        dt1 = time.perf_counter() - t1
+    return {"value": sample / dt, "unit": "candidates/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "sample": f"{cfg} {b['mode']}: ordinals [0, {sample}) of the bench batch (seed {seed}), exact top-{b['k']} "
+                      f"included, oracle/parallel.py over {cores} processes (batch forms of the oracle, FP64), "
+                      f"{dt:.1f} s",
+            "one_core": {"value": done / dt1, "unit": "candidates/s", "cores": 1,
+                         "sample": f"{done} candidates, scalar oracle/run.py, numpy/BLAS 1 thread, {dt1:.1f} s"}}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (batch forms, all host cores), timed on bounded samples of the same
+    workload; each step = one sample of the batch scored exactly + its exact top-k."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import parallel as OP
+    cfg = args.config
+    o, fit, b, n_all = _oracle_setup(cfg)
+    cores = OP.cores()
+    chunk = int(min(n_all, 1 << 20))
+    times = []
+    for i in range(args.warmup + args.steps):
+        start = (i * chunk) % n_all                 # small spaces: wrap around the batch
+        c = min(chunk, n_all - start)
+        t0 = time.perf_counter()
+        OP.topk(o, fit, b["mode"], start, c, b["k"], seed=0, acq=b["acq"], procs=cores)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append((dt, c))
+    tot = sum(t for t, _ in times)
+    cand = sum(c for _, c in times)
+    ms = 1e3 * tot / len(times)
+    v = cand / tot
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "candidates/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD.get(cfg, cfg), "candidates_per_step": chunk,
-                       "note": "oracle/ (plain numpy FP64) on a bounded sample of the workload per step"},
-            "cpu_baseline": {"value": v, "unit": "candidates/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{chunk} candidates per step, sample ordinals [{args.warmup * chunk},"
-                                       f"{(args.warmup + args.steps) * chunk})"},
+                       "note": "oracle/ (plain numpy FP64, batch forms pinned to the scalar definitions) over all "
+                               "host cores on a bounded sample of the workload per step, exact top-k included"},
+            "cpu_baseline": {"value": v, "unit": "candidates/s", "cores": cores, "kind": "oracle",
+                             "cpu_model": cpu_model(),
+                             "sample": f"{chunk} candidates per step, sample ordinals from {args.warmup * chunk} "
+                                       f"(wrapping), {args.steps} steps"},
             "e2e": {"value": v, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -294,7 +321,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_2603_11603_b200.autoscout import Space
-    from paper_2603_11603_b200.shard import gather_merge, shard_range
+    from paper_2603_11603_b200.shard import gather_merge_device, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -325,8 +352,9 @@ def run_ours(args):
                        stream=stream)
         if world == 1:
             return sp.topk(k, stream=stream)
-        pool, npool, cut = sp.topk_pool(k, cap, stream=stream)
-        return gather_merge(pool, npool, cut, k, device=dev)[0]
+        # device-resident exchange: packed pool on the device, one all_gather_into_tensor (NCCL),
+        # device merge + global certificate; only the k-entry result comes back
+        return gather_merge_device(sp, k, cap, stream=stream)[0]
 
     clocks = Clocks(local)                        # started before the warm-up: nvidia-smi needs ~0.2 s
     for _ in range(args.warmup):
@@ -484,7 +512,7 @@ def run_ours(args):
                        "space": f"spaces/{cfg}.json", "mode": mode,
                        "candidates_per_step": count, "observed_M": M, "acq": acq, "k": k,
                        "valid_per_step": valid_per_step_all, "l2": "flushed (256 MiB write) before every timed step",
-                       "parallelism": f"dp{world} (candidate-range shards, one all-gather)",
+                       "parallelism": f"dp{world} (candidate-range shards, one all_gather_into_tensor of device pools)",
                        "arith": "decode int; simulator + resource check FP64; r^2 one-hot FP16 hi/lo MMA (FP32 accumulate); "
                                 "k FP32; L^-1 k 3-term FP16 MMA (FP32-accurate); screen FP32 + bound; refine FP64"},
             "valid_per_s": valid_per_step_all / (ms_per_step / 1e3),

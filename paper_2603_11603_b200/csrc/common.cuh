@@ -251,6 +251,88 @@ AS_HD void simulate(const SimParams& P, const Knobs& k, double& cost, bool& ok, 
   cost = pow(TPOT, P.w_tpot) * pow(thr, -(1.0 - P.w_tpot));
 }
 
+// ---- derived mode, partial evaluation per structure (gen kernel fast path).
+// Every derived-mode cost term is a product of factors that depend on the structural prefix only
+// (pp, vpp, tp, dp, cp, ep, mbs, ar, arl when they are prefix features) and per-candidate tail
+// factors (tp_comm steal / overlap, sp, bucket penalty, ovg, ovp, dispatcher).  The structural
+// products are evaluated once per structure on the host; the resource check of every structure
+// is tabulated over the tail features it reads (sp, dopt, ... and their tail gates), computed
+// with the normative FP64 order by the same simulate() (R7: bit-identical).  Costs agree with
+// simulate() to FP64 re-association (the refine kernel still evaluates simulate() itself).
+struct SimRec {
+  double comp;        // T_work r ipdc vi_tp / (1 + 0.1 lg mbs)      t_comp = comp (1 + steal)
+  double bub;         // (pp - 1) (dp mbs / GBS) vi_vpp              t_bubble = t_comp bub
+  double tp;          // tp > 1: C_tp ipdc inv_bw(tp) (1 - vi_tp)     x (1 - ov) (sp ? 0.8 : 1)
+  double dp;          // dp > 1: 4 P_loc inv_bw(tp cp dp) (1 - vi_dp) x (1 + 0.1 lb^2) ovg ovp
+  double ep;          // ep > 1: C_ep ipdc inv_bw(tp cp ep) (1 - vi_ep) x (sp ? vi_tp : 1) disp
+  double cp;          // t_cp
+  double vi_tp;       // 1 / tp (t_ep's sequence-parallel factor)
+  uint32_t tpgt1;     // tp > 1
+  uint32_t pad;
+  uint64_t memok;     // bit c: resource check passes for tail combination c
+  uint64_t pad2;      // 80 B: five 16-byte loads
+};
+constexpr int SR_MAXCF = 4;   // tail features in the resource-check combination
+struct SimFast {
+  int on;
+  int n_cf;
+  int cf_w[SR_MAXCF], cf_s[SR_MAXCF];   // digit word / bit shift of combination feature i
+  uint32_t cf_mul[SR_MAXCF];            // combination index = sum digit_i * cf_mul[i]
+};
+AS_HD uint32_t knob_digit(const SimParams& P, int i, const DV& dv) {
+  const int kw = P.kw[i];
+  const uint64_t w = kw == 0 ? dv.w[0] : (kw == 1 ? dv.w[1] : dv.w[2]);
+  return static_cast<uint32_t>((w >> P.ks[i]) & 0xFFu);
+}
+AS_HD double knob_val(const SimParams& P, const double* val, int i, const DV& dv) {
+  return P.kf[i] >= 0 ? val[P.ko[i] + static_cast<int>(knob_digit(P, i, dv))] : P.neutral[i];
+}
+// per-structure products from the structural knobs k (tail knob values in k are ignored)
+AS_HD void simrec_base(const SimParams& P, const Knobs& k, SimRec& r) {
+  const double pp = k.v[K_PP], tp = k.v[K_TP], dp = k.v[K_DP], cp = k.v[K_CP], ep = k.v[K_EP], mbs = k.v[K_MBS];
+  const double vpp = k.v[K_VPP], arc = k.v[K_AR];
+  const bool full = arc == 2.0, sel = arc == 1.0;
+  const double L_st = xdiv(P.L, xmul(pp, vpp));
+  const bool arl_active = (k.act >> K_ARL) & 1u;
+  const double f_rc = full ? (arl_active ? fmin(1.0, xdiv(k.v[K_ARL], L_st)) : 1.0) : 0.0;
+  const double rr = 1.0 + 0.33 * f_rc + (sel ? 0.03 : 0.0);
+  const double ipdc = k.vi[K_PP] * k.vi[K_DP] * k.vi[K_CP];
+  r.comp = P.T_work * rr * (ipdc * k.vi[K_TP]) / (1.0 + 0.1 * k.lg[K_MBS]);
+  r.bub = (pp - 1.0) * (dp * mbs * P.inv_GBS) * k.vi[K_VPP];
+  r.tp = tp > 1.0 ? P.C_tp * ipdc * inv_bw_of(P, tp) * (1.0 - k.vi[K_TP]) : 0.0;
+  const double P_loc = xdiv(xadd(P.P - P.P_exp, xdiv(P.P_exp, ep)), xmul(pp, tp));
+  r.dp = dp > 1.0 ? 4.0 * P_loc * inv_bw_of(P, tp * cp * dp) * (1.0 - k.vi[K_DP]) : 0.0;
+  r.ep = ep > 1.0 ? P.C_ep * ipdc * inv_bw_of(P, tp * cp * ep) * (1.0 - k.vi[K_EP]) : 0.0;
+  r.cp = cp > 1.0 ? P.C_cp * k.vi[K_PP] * k.vi[K_DP] * inv_bw_of(P, tp * cp) * (1.0 - k.vi[K_CP]) : 0.0;
+  r.vi_tp = k.vi[K_TP];
+  r.tpgt1 = tp > 1.0 ? 1u : 0u;
+  r.pad = 0;
+}
+// cost + resource check of a candidate of structure record r (digits dv, activity act)
+AS_HD void sim_fast(const SimParams& P, const SimFast& F, const double* val, const double* lg2, const SimRec& r,
+                    const DV& dv, uint32_t act, double& cost, bool& ok) {
+  const bool tpc_on = P.kf[K_TPCOMM] >= 0 && ((act & P.kbit[K_TPCOMM]) != 0u);
+  const double v_tpc = knob_val(P, val, K_TPCOMM, dv);
+  const bool sp = knob_val(P, val, K_SP, dv) == 1.0;
+  const double lgb = P.kf[K_BUCKET] >= 0 ? lg2[P.ko[K_BUCKET] + static_cast<int>(knob_digit(P, K_BUCKET, dv))]
+                                         : P.neutral_lg2[K_BUCKET];
+  const bool ovg = knob_val(P, val, K_OVG, dv) == 1.0, ovp = knob_val(P, val, K_OVP, dv) == 1.0;
+  const bool disp = knob_val(P, val, K_DISP, dv) == 1.0;
+  const double steal = tpc_on ? v_tpc * P.half_inv_nsm : 0.0;
+  const double t_comp = r.comp * (1.0 + steal);
+  const double ov = (r.tpgt1 && tpc_on) ? clamp((v_tpc - 12.0) * 0.0625, 0.0, 0.5) : 0.0;
+  const double lb = lgb - 2.0;
+  cost = t_comp + t_comp * r.bub + r.tp * (1.0 - ov) * (sp ? 0.8 : 1.0) +
+         r.dp * (1.0 + 0.1 * lb * lb) * (ovg ? 0.5 : 1.0) * (ovp ? 0.75 : 1.0) +
+         r.ep * (sp ? r.vi_tp : 1.0) * (disp ? 1.5 : 1.0) + r.cp;
+  uint32_t c = 0;
+  for (int i = 0; i < F.n_cf; ++i) {
+    const uint64_t w = F.cf_w[i] == 0 ? dv.w[0] : (F.cf_w[i] == 1 ? dv.w[1] : dv.w[2]);
+    c += static_cast<uint32_t>((w >> F.cf_s[i]) & 0xFFu) * F.cf_mul[i];
+  }
+  ok = (r.memok >> c) & 1ull;
+}
+
 // ---- acquisition in FP64 (R10)
 constexpr double LN_2PI = 1.8378770664093454835606594728112;
 constexpr double INV_SQRT_2PI = 0.39894228040143267793994605993438;

@@ -482,6 +482,95 @@ as_status ensure_cand_list(as_space* s, size_t cap) {
   return AS_OK;
 }
 
+// Per-structure partial evaluation of the derived simulator for the generation kernel (common.cuh
+// SimRec): false (generic path) unless every base-term knob is a structural-prefix feature (or
+// absent) and the resource check reads at most 64 combinations of tail digits.  Self-checked on
+// the host against simulate() before it is used.
+bool build_simrec(const HostSpace& H, std::vector<SimRec>& rec, SimFast& F) {
+  F = SimFast{};
+  rec.clear();
+  const SimParams& P = H.sim;
+  if (P.mode != 1 || H.n_struct <= 0) return false;
+  auto tail = [&](int kb) { return P.kf[kb] >= H.n_prefix; };
+  for (int kb : {K_PP, K_VPP, K_TP, K_DP, K_CP, K_EP, K_MBS, K_AR, K_ARL})
+    if (tail(kb)) return false;
+  // tail features the resource check reads (dopt, sp), with their tail gate ancestors so that the
+  // combination fixes their activity
+  std::vector<int> cf;
+  std::vector<int> stack;
+  for (int kb : {K_DOPT, K_SP})
+    if (tail(kb)) stack.push_back(P.kf[kb]);
+  while (!stack.empty()) {
+    const int f = stack.back();
+    stack.pop_back();
+    if (f < H.n_prefix || std::find(cf.begin(), cf.end(), f) != cf.end()) continue;
+    cf.push_back(f);
+    for (const Atom& a : H.feat[f].req) stack.push_back(a.ref);
+  }
+  std::sort(cf.begin(), cf.end());
+  uint64_t ncomb = 1;
+  for (int f : cf) ncomb *= static_cast<uint64_t>(H.feat[f].n);
+  if (cf.size() > static_cast<size_t>(SR_MAXCF) || ncomb > 64) return false;
+  F.n_cf = static_cast<int>(cf.size());
+  uint32_t mul = 1;
+  for (int i = F.n_cf - 1; i >= 0; --i) {
+    F.cf_w[i] = cf[i] >> 3;
+    F.cf_s[i] = (cf[i] & 7) * 8;
+    F.cf_mul[i] = mul;
+    mul *= static_cast<uint32_t>(H.feat[cf[i]].n);
+  }
+  rec.resize(H.n_struct);
+  for (int st = 0; st < H.n_struct; ++st) {
+    Knobs k;
+    load_knobs(P, H.val.data(), H.inv.data(), H.lg2.data(), H.s_dv[st], H.s_act[st], k);
+    SimRec& r = rec[st];
+    simrec_base(P, k, r);
+    r.memok = 0;
+    r.pad2 = 0;
+    for (uint64_t c = 0; c < ncomb; ++c) {
+      // the structure with combination c in the listed tail features and every other tail feature
+      // at its default digit
+      uint64_t raw = H.s_raw[st];
+      for (int f = H.n_prefix; f < H.d; ++f) raw += static_cast<uint64_t>(H.feat[f].dflt) * H.stride[f];
+      for (int i = 0; i < F.n_cf; ++i) {
+        const uint64_t dig = (c / F.cf_mul[i]) % static_cast<uint64_t>(H.feat[cf[i]].n);
+        raw += (dig - static_cast<uint64_t>(H.feat[cf[i]].dflt)) * H.stride[cf[i]];
+      }
+      int dg[DMAX];
+      DV dv;
+      uint32_t act;
+      bool structural;
+      if (!raw_decode(H, raw, dg, dv, act, structural) || !structural) continue;   // never occurs
+      double cost, mem;
+      bool ok;
+      simulate_host(H, dv, act, cost, ok, mem);
+      if (ok) r.memok |= 1ull << c;
+    }
+  }
+  F.on = 1;
+  // self-check on a sample of valid-structure configurations: the same resource bit, the cost to
+  // FP64 re-association
+  const uint64_t n_check = std::min<uint64_t>(H.n_cvi, 20000);
+  for (uint64_t i = 0; i < n_check; ++i) {
+    const uint64_t p = (H.n_cvi <= n_check) ? i : (splitmix64(0xC4EC ^ i) % H.n_cvi);
+    DV dv;
+    uint32_t act;
+    uint64_t raw;
+    if (!cvi_decode(H, p, dv, act, raw)) continue;
+    int st = static_cast<int>(std::upper_bound(H.prefix.begin(), H.prefix.begin() + H.n_struct + 1, p) - H.prefix.begin()) - 1;
+    double c1, m1, c2;
+    bool ok1, ok2;
+    simulate_host(H, dv, act, c1, ok1, m1);
+    sim_fast(P, F, H.val.data(), H.lg2.data(), rec[st], dv, act, c2, ok2);
+    if (ok1 != ok2 || !(std::fabs(c1 - c2) <= 1e-12 * std::fabs(c1))) {
+      F = SimFast{};
+      rec.clear();
+      return false;
+    }
+  }
+  return true;
+}
+
 as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, bool reset, cudaStream_t st) {
   s->sev_used = 0;
   if (s->timing) CUDA_TRY(cudaEventRecord(s->ev[0], st));
@@ -877,6 +966,18 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
     D.lg2 = p_lg2;
     D.xt64 = p_xt64;
     D.xt32 = p_xt32;
+    {
+      std::vector<SimRec> srec;
+      SimFast sf;
+      D.srec = nullptr;
+      D.sf = SimFast{};
+      if (build_simrec(H, srec, sf)) {
+        SimRec* p_srec;
+        if ((r = upload(&p_srec, srec, s->owned)) != AS_OK) return cleanup(r);
+        D.srec = p_srec;
+        D.sf = sf;
+      }
+    }
     if ((r = dalloc(&s->d_ens_tab, static_cast<size_t>(DMAX) * VMAX, s->owned)) != AS_OK) return cleanup(r);
     D.ens_tab = s->d_ens_tab;
     D.ens_on = 0;

@@ -44,6 +44,9 @@ struct DevSpace {
   int ens_on;
   double ens_c0;
   const double* ens_tab;   // [d * VMAX]
+  // derived-mode partial evaluation per structure (gen kernel fast path; srec == nullptr: off)
+  const SimRec* srec;      // [n_struct]
+  SimFast sf;
 };
 
 // out of line: keeps the ensemble loop out of the register allocation of the hot kernels
@@ -179,7 +182,7 @@ __device__ __forceinline__ void decode_tail(const DevSpace& S, int lo, uint32_t 
 // ci_n == n_struct the whole search runs in shared memory.
 constexpr int CI = 256;
 __device__ __forceinline__ void decode_dev_ci(const DevSpace& S, const uint64_t* cidx, int ci_n, uint64_t p, DV& dv,
-                                              uint32_t& act, uint64_t& raw) {
+                                              uint32_t& act, uint64_t& raw, int* sidx = nullptr) {
   int a = 0, b = ci_n;                       // largest k with cidx[k] <= p
   while (b - a > 1) {
     const int mid = (a + b) >> 1;
@@ -192,12 +195,13 @@ __device__ __forceinline__ void decode_dev_ci(const DevSpace& S, const uint64_t*
     const int mid = (lo + hi) >> 1;
     if (__ldg(S.prefix + mid) <= p) lo = mid; else hi = mid;
   }
+  if (sidx) *sidx = lo;
   decode_tail(S, lo, static_cast<uint32_t>(p - __ldg(S.prefix + lo)), dv, act, raw);
 }
 // Structure lookup from SMEM copies of the whole prefix table and of the bucket index: the
 // position's bucket brackets its structure, then a short binary search (typically 0-2 probes).
 __device__ __forceinline__ void decode_dev_bucket(const DevSpace& S, const uint64_t* pre, const uint32_t* bkt,
-                                                  uint64_t p, DV& dv, uint32_t& act, uint64_t& raw) {
+                                                  uint64_t p, DV& dv, uint32_t& act, uint64_t& raw, int* sidx = nullptr) {
   const int b = static_cast<int>(p >> S.bshift);
   int lo = static_cast<int>(bkt[b]), hi = static_cast<int>(bkt[b + 1]) + 1;
   if (hi > S.n_struct) hi = S.n_struct;
@@ -205,6 +209,7 @@ __device__ __forceinline__ void decode_dev_bucket(const DevSpace& S, const uint6
     const int mid = (lo + hi) >> 1;
     if (pre[mid] <= p) lo = mid; else hi = mid;
   }
+  if (sidx) *sidx = lo;
   decode_tail(S, lo, static_cast<uint32_t>(p - pre[lo]), dv, act, raw);
 }
 __device__ __forceinline__ void decode_dev_idx(const DevSpace& S, const uint64_t* cidx, uint64_t p, DV& dv,

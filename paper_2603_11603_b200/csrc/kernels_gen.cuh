@@ -61,9 +61,22 @@ gen_kernel(DevSpace S, BatchArgs A, uint64_t j0, uint64_t nj, CandList L, int ci
     if (in) {
       bool pin;
       pcvi = assign_pos(A, j, pin);
-      if (by_bucket) decode_dev_bucket(S, gen_cidx, gen_bkt, pcvi, dv, act, raw);
-      else decode_dev_ci(S, gen_cidx, ci_n, pcvi, dv, act, raw);
-      sim_dev(S, dv, act, cost, ok);
+      int sidx = 0;
+      if (by_bucket) decode_dev_bucket(S, gen_cidx, gen_bkt, pcvi, dv, act, raw, &sidx);
+      else decode_dev_ci(S, gen_cidx, ci_n, pcvi, dv, act, raw, &sidx);
+      if (S.srec != nullptr) {
+        // per-structure products + tabulated resource check (derived mode)
+        SimRec r;
+        const double2* rp = reinterpret_cast<const double2*>(S.srec + sidx);
+        const double2 a = __ldg(rp), b = __ldg(rp + 1), c = __ldg(rp + 2), e = __ldg(rp + 3);
+        const ulonglong2 f = __ldg(reinterpret_cast<const ulonglong2*>(rp + 4));
+        r.comp = a.x; r.bub = a.y; r.tp = b.x; r.dp = b.y; r.ep = c.x; r.cp = c.y; r.vi_tp = e.x;
+        r.tpgt1 = static_cast<uint32_t>(__double_as_longlong(e.y));
+        r.memok = f.x;
+        sim_fast(S.sim, S.sf, S.val, S.lg2, r, dv, act, cost, ok);
+      } else {
+        sim_dev(S, dv, act, cost, ok);
+      }
       if (!pin) {
         ok = false;
         raw = ~0ull;
