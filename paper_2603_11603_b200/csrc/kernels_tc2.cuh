@@ -289,9 +289,11 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       const int us = u % TC_TI, ms = u % TC2_TI;
       uint64_t key = KEY_NONE;
       bool sensitive = false;
+      const int row = pt;
+      float mu32 = 0.f, sb = 0.f, kk = 0.f, vv = 0.f, mu = 0.f, s2 = 0.f, d_mu = 0.f, d_s2 = 0.f;
+      double cm0 = 0.0;
+      bool early = false;
       if (pt < n) {
-        const int row = pt;
-        float mu32 = 0.f, sb = 0.f, kk = 0.f, vv = 0.f;
 #pragma unroll
         for (int q = 0; q < TC_JQ; ++q) {
           const float* mp = m_part + (us * TC_JQ + q) * 3 * TC_ROWS;
@@ -300,16 +302,42 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
           kk += mp[2 * TC_ROWS + row];
           vv += vpart[q * TC_ROWS + row];
         }
-        const double cm0 = m_m0[ms * TC_ROWS + row];
+        cm0 = m_m0[ms * TC_ROWS + row];
         TR(u, 13);
-        const float mu = static_cast<float>(cm0 + G.b) + mu32;
+        mu = static_cast<float>(cm0 + G.b) + mu32;
         const float vs = vv;
-        const float s2 = static_cast<float>(G.sf2) - vs;
+        s2 = static_cast<float>(G.sf2) - vs;
         // FP32 k + 3xTF32 contraction: error coefficient 8x the SIMT one
         const float eps = 8.0f * static_cast<float>(G.eps);
-        const float d_mu = eps * sb + 2e-7f * (1.0f + fabsf(mu));
+        d_mu = eps * sb + 2e-7f * (1.0f + fabsf(mu));
         const float ew = eps * static_cast<float>(G.w_fro);
-        const float d_s2 = 2.5f * ew * sqrtf(vs * kk) + ew * ew * kk + eps * vs + 8.0f * U32 * G.sf2f;
+        d_s2 = 2.5f * ew * sqrtf(vs * kk) + ew * ew * kk + eps * vs + 8.0f * U32 * G.sf2f;
+        // Early rejection (EI, bench path only): a cheap upper bound of the admission score,
+        //   ln sigma + ln h(z),  h(z) <= phi(z) / (1 + z^2) for z <= 0 (Mills ratio
+        //   Q(x) >= x phi(x) / (1 + x^2)),  h(z) <= z + phi(0) for z > 0,
+        // at the same (mu - d_mu, s2 + d_s2) as the exact screen, plus slack covering twice the
+        // screen's evaluation margin and its own MUFU rounding: its key never exceeds the exact
+        // admission key, so key >= tau rejects exactly the rows the exact screen would reject, and
+        // the (smaller) cheap key is a valid entry for the best-dropped bound.
+        const uint64_t tau = ts.tau;
+        if (A.acq == 0 && !A.d_scores && !A.d_screen && tau != KEY_NONE) {
+          const float s2p = s2 + d_s2;
+          if (s2p > 0.0f) {
+            const float z = (static_cast<float>(G.fstar) - (mu - d_mu) - static_cast<float>(A.xi)) * rsqrtf(s2p);
+            const float lnhb = z > 0.0f ? __logf(z + 0.3989422804014327f)
+                                        : -0.5f * z * z - 0.9189385332046727f - __logf(1.0f + z * z);
+            const float cheap = 0.5f * __logf(s2p) + lnhb;
+            const float cheap_ub = cheap + 2e-5f * (1.0f + fabsf(cheap) + z * z);
+            const uint64_t kc = make_key(cheap_ub, m_cvi[ms * TC_ROWS + row]);
+            if (kc >= tau) {
+              early = true;
+              if (kc < drop_r) drop_r = kc;
+            }
+          }
+        }
+      }
+      const bool warp_early = __all_sync(0xffffffffu, early || pt >= n);
+      if (pt < n && !early && !warp_early) {
         const float fstar = static_cast<float>(G.fstar), m0f = static_cast<float>(cm0);
         float m2;
         float ub = acquisition32(A.acq, mu - d_mu, s2 + d_s2, m0f, fstar, static_cast<float>(A.xi),
@@ -691,7 +719,11 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       tc::mbar_wait(d_empty, (t & 1) ^ 1);
       TR(t, 9);
       tc::fence_after_sync();
-      for (int c = 0; c < nch; ++c, ++g) {
+      // one chunk: R2 lookahead, operand waits, 3 MMAs + 2 commits.  With a compile-time chunk
+      // count the loop below unrolls, so N, idesc, the D / A columns and the A-stage parity are
+      // immediates (the MMA warp shares SM sub-partition 0 with four producer warps: its
+      // instruction count paces the lock-step pipeline)
+      auto mma_chunk = [&](int c) {
         // R2 lookahead: the producers may run NA chunks ahead of M(g), so the group of chunk
         // c + NA must be issued before M(g); never beyond the next tile (tile t+2 is published
         // only after the epilogue of tile t, which needs MMAs not issued yet).
@@ -702,8 +734,9 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
           while (x <= target && issue_R()) {
           }
         }
-        const int sa = g % TC2_NA, sbb = g % TC2_NB;
-        tc::mbar_wait(a_full + sa, (g / TC2_NA) & 1);
+        const uint32_t ga = static_cast<uint32_t>(t) * static_cast<uint32_t>(nch) + static_cast<uint32_t>(c);
+        const int sa = ga % TC2_NA, sbb = g % TC2_NB;
+        tc::mbar_wait(a_full + sa, (ga / TC2_NA) & 1);
         tc::mbar_wait(b_full + sbb, (g / TC2_NB) & 1);
         if (c == TC2_NA) TR(t, 11);
         tc::fence_after_sync();
@@ -715,6 +748,13 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         const uint32_t d = tmem + c * TC_KCH;
         // 3-term FP16 split: hi.hi + hi.lo + lo.hi (one K = 16 step each), then release A and B
         tc::mma3_f16_ts_commit2_w(d, a_h, a_l, bh, bl, idesc, c > 0 ? 1u : 0u, a_empty + sa, b_empty + sbb);
+        ++g;
+      };
+      if (NCH > 0) {
+#pragma unroll
+        for (int c = 0; c < (NCH > 0 ? NCH : 1); ++c) mma_chunk(c);
+      } else {
+        for (int c = 0; c < nch; ++c) mma_chunk(c);
       }
       tc::mma_commit_w(d_full);
       TR(t, 10);
