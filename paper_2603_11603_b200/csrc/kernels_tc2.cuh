@@ -113,17 +113,16 @@ __device__ __forceinline__ void tc2_prune(uint64_t* arr, TopkSmem& ts, int KC, i
 // column offset becomes an immediate (no per-chunk address arithmetic on the FMA pipe).  NCH = 0:
 // any M <= 256, runtime indices.
 template <int PW, int KT, int NH, int NCH>
-__global__ void __launch_bounds__(PW * 32 + 64, 1)
+__global__ void __launch_bounds__(PW * 32 + 96, 1)
 score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, CandList L) {
   constexpr int TC_PROD_WARPS = PW;
   constexpr int TC_PROD_THREADS = PW * 32;
-  constexpr int TC_THREADS = TC_PROD_THREADS + 64;   // + MMA warp + loader warp
+  constexpr int TC_THREADS = TC_PROD_THREADS + 96;   // + MMA warp + loader warp + R2 warp
   constexpr int TC_JQ = TC_PROD_THREADS / TC_ROWS;   // producer threads per candidate
   constexpr int TC_JPT = TC_KCH / TC_JQ;             // observed points per thread per chunk
   static_assert(TC_JQ == 4 && TC_JPT == 4, "R2 group columns are laid out for 16 producer warps");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ TopkSmem ts;
-  __shared__ int tinfo[TC_TI];
   __shared__ uint32_t tmem_base;
   __shared__ int eoff_s[DMAX];
 
@@ -451,10 +450,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         if (lane == 0) tc::mbar_arrive(s_empty + (u & 1));   // staged records consumed
       }
       named_sync(1, TC_PROD_THREADS);
-      if (pt == 0) {
-        tinfo[us] = n > 0 ? n : -1;
-        tc::mbar_arrive(t_ready + us);
-      }
+      if (pt == 0 && n > 0) tc::mbar_arrive(t_ready + us);   // E rows of tile u published (R2 warp)
       return n;
     };
 
@@ -676,64 +672,19 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     // MMAs / commits (elect.sync inside the asm).  All bulk copies are the loader warp's, so this
     // warp never waits on a ring refill.
     uint32_t g = 0;                  // L^-1 chunks consumed
-    uint32_t x = 0;                  // R2 groups issued
-    int ru = 0, rgi = 0;             // tile / group index of the next R2 group
-    int known = 0, end_tile = 0x7fffffff;
-    auto tile_exists = [&](int u) -> bool {
-      while (known <= u && known < end_tile) {
-        tc::mbar_wait(t_ready + (known % TC_TI), (known / TC_TI) & 1);
-        if (tinfo[known % TC_TI] < 0) end_tile = known;
-        ++known;
-      }
-      return u < end_tile;
-    };
+    auto tile_exists = [&](int u) -> bool { return u < my_tiles; };
     __syncwarp();
-    const uint32_t sbo16 = (Kp / 8) * 128;
-    const uint64_t dE = tc::sdesc(sE0, 128, sbo16), dT = tc::sdesc(sT0, 128, sbo16);
     const uint64_t dB = tc::sdesc(sB0, 128, (TC_KCH / 8) * 128);
-    const uint32_t piece16 = ((TC2_RG * TC_KCH) * Kp * 2) >> 4;   // descriptor units (16 B)
-    const uint32_t idesc_r = tc::idesc_f16(TC_ROWS, TC2_RG * TC_KCH);
-    const int ksteps_r = Kp / 16;
-    // R2 group x: D_R[x % RS] = E[tile & 1] T_g^T  (N = 64; 2 FP16 pieces x Kp/16 k-steps)
-    auto issue_R = [&]() -> bool {
-      if (!tile_exists(ru)) return false;
-      const int rs = x % TC2_RS, st_ = x % TC2_NT;
-      tc::mbar_wait(r_empty + rs, ((x / TC2_RS) & 1u) ^ 1u);
-      tc::mbar_wait(x_full + st_, (x / TC2_NT) & 1u);
-      tc::fence_after_sync();
-      const uint32_t dR = tmem + R0col + 64u * rs;
-      const uint64_t ad = dE + (((ru & 1) * e_bytes) >> 4), bd = dT + ((st_ * t_stage_bytes) >> 4);
-      for (int ks = 0; ks < ksteps_r; ++ks)
-        tc::mma2_f16_w(dR, ad + 16 * ks, bd + 16 * ks, bd + piece16 + 16 * ks, idesc_r, ks > 0 ? 1u : 0u);
-      tc::mma_commit_w(r_full + rs);
-      tc::mma_commit_w(x_empty + st_);
-      ++x;
-      if (++rgi == ng) {
-        rgi = 0;
-        ++ru;
-      }
-      return true;
-    };
     for (int t = 0; tile_exists(t); ++t) {
       TR(t, 8);
       tc::mbar_wait(d_empty, (t & 1) ^ 1);
       TR(t, 9);
       tc::fence_after_sync();
-      // one chunk: R2 lookahead, operand waits, 3 MMAs + 2 commits.  With a compile-time chunk
+      // one chunk: operand waits, 3 MMAs + 2 commits.  With a compile-time chunk
       // count the loop below unrolls, so N, idesc, the D / A columns and the A-stage parity are
       // immediates (the MMA warp shares SM sub-partition 0 with four producer warps: its
       // instruction count paces the lock-step pipeline)
       auto mma_chunk = [&](int c) {
-        // R2 lookahead: the producers may run NA chunks ahead of M(g), so the group of chunk
-        // c + NA must be issued before M(g); never beyond the next tile (tile t+2 is published
-        // only after the epilogue of tile t, which needs MMAs not issued yet).
-        {
-          const int cn = c + TC2_NA;
-          const uint32_t target = cn < nch ? static_cast<uint32_t>(t * ng + cn / TC2_RG)
-                                           : static_cast<uint32_t>((t + 1) * ng + min((cn - nch) / TC2_RG, ng - 1));
-          while (x <= target && issue_R()) {
-          }
-        }
         const uint32_t ga = static_cast<uint32_t>(t) * static_cast<uint32_t>(nch) + static_cast<uint32_t>(c);
         const int sa = ga % TC2_NA, sbb = g % TC2_NB;
         tc::mbar_wait(a_full + sa, (ga / TC2_NA) & 1);
@@ -758,6 +709,36 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       }
       tc::mma_commit_w(d_full);
       TR(t, 10);
+    }
+    __syncwarp();
+  } else if (warp == TC_PROD_WARPS + 2) {
+    // =========================================================== R2 issuer (sub-partition 2)
+    // R2 group x = D_R[x % RS] = E[tile & 1] T_g^T (N = 64; 2 FP16 pieces x Kp/16 k-steps), issued
+    // as soon as its tile's E rows are published, its TMEM slot is free and its T stage is loaded:
+    // an MMA stream independent of the L^-1 chunks (separate accumulators), on its own warp so
+    // that neither stream waits for the other and the MMA warp's sub-partition carries only the
+    // L^-1 issue.
+    __syncwarp();
+    const uint32_t sbo16 = (Kp / 8) * 128;
+    const uint64_t dE = tc::sdesc(sE0, 128, sbo16), dT = tc::sdesc(sT0, 128, sbo16);
+    const uint32_t piece16 = ((TC2_RG * TC_KCH) * Kp * 2) >> 4;   // descriptor units (16 B)
+    const uint32_t idesc_r = tc::idesc_f16(TC_ROWS, TC2_RG * TC_KCH);
+    const int ksteps_r = Kp / 16;
+    uint32_t x = 0;
+    for (int ru = 0; ru < my_tiles; ++ru) {
+      tc::mbar_wait(t_ready + (ru % TC_TI), (ru / TC_TI) & 1);
+      for (int rgi = 0; rgi < ng; ++rgi, ++x) {
+        const int rs = x % TC2_RS, st_ = x % TC2_NT;
+        tc::mbar_wait(r_empty + rs, ((x / TC2_RS) & 1u) ^ 1u);
+        tc::mbar_wait(x_full + st_, (x / TC2_NT) & 1u);
+        tc::fence_after_sync();
+        const uint32_t dR = tmem + R0col + 64u * rs;
+        const uint64_t ad = dE + (((ru & 1) * e_bytes) >> 4), bd = dT + ((st_ * t_stage_bytes) >> 4);
+        for (int ks = 0; ks < ksteps_r; ++ks)
+          tc::mma2_f16_w(dR, ad + 16 * ks, bd + 16 * ks, bd + piece16 + 16 * ks, idesc_r, ks > 0 ? 1u : 0u);
+        tc::mma_commit_w(r_full + rs);
+        tc::mma_commit_w(x_empty + st_);
+      }
     }
     __syncwarp();
   } else {
