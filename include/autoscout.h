@@ -194,6 +194,10 @@ as_status autoscout_topk_merge_device(as_space* s, const void* d_pools, int32_t 
  * sample_to_cvi: the SAMPLE-mode position pi_seed(ordinal) (reading R3, a Feistel bijection of
  *   [0, n_cvi)).  AS_ERR_INDEX_RANGE if ordinal >= n_cvi. */
 as_status autoscout_decode(const as_space* s, uint64_t raw, int32_t* digits_out, int32_t* valid_out);
+/* Activity of every feature of a raw index (host): bit j of *active_mask_out = feature j is active
+ * (its activation predicate holds over earlier features; PAPER.md:171 masking function
+ * M(s)).  AS_ERR_INDEX_RANGE if raw >= n_raw. */
+as_status autoscout_activity(const as_space* s, uint64_t raw, uint32_t* active_mask_out);
 as_status autoscout_cvi_to_raw(const as_space* s, uint64_t cvi, uint64_t* raw_out);
 as_status autoscout_sample_to_cvi(const as_space* s, uint64_t seed, uint64_t ordinal, uint64_t* cvi_out);
 /* ML-II evidence of GP hyper-parameter settings, batched on the device (

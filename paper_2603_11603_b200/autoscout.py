@@ -84,6 +84,7 @@ def _load():
         "autoscout_topk_pool_device": ([P, I32, P, I32, P], I32),
         "autoscout_topk_merge_device": ([P, P, I32, I32, I32, P, P], I32),
         "autoscout_decode": ([P, U64, pI32, pI32], I32),
+        "autoscout_activity": ([P, U64, ctypes.POINTER(ctypes.c_uint32)], I32),
         "autoscout_cvi_to_raw": ([P, U64, pU64], I32),
         "autoscout_sample_to_cvi": ([P, U64, U64, pU64], I32),
         "autoscout_raw_to_cvi": ([P, U64, pU64, pI32], I32),
@@ -189,6 +190,12 @@ class Space:
         valid = ctypes.c_int32()
         _check(_LIB.autoscout_decode(self.h, int(raw), dig, ctypes.byref(valid)))
         return list(dig), bool(valid.value)
+
+    def activity(self, raw):
+        """-> list[bool]: feature j active for this raw index."""
+        m = ctypes.c_uint32()
+        _check(_LIB.autoscout_activity(self.h, int(raw), ctypes.byref(m)))
+        return [bool((m.value >> j) & 1) for j in range(self.d)]
 
     def cvi_to_raw(self, cvi):
         r = ctypes.c_uint64()

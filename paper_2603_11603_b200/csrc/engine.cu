@@ -1344,6 +1344,17 @@ as_status autoscout_decode(const as_space* s, uint64_t raw, int32_t* digits_out,
   return AS_OK;
 }
 
+as_status autoscout_activity(const as_space* s, uint64_t raw, uint32_t* active_mask_out) {
+  if (!s || !active_mask_out) return fail(AS_ERR_INVALID_ARG, "null argument");
+  int dig[DMAX];
+  DV dv;
+  uint32_t act;
+  bool structural;
+  if (!raw_decode(s->H, raw, dig, dv, act, structural)) return fail(AS_ERR_INDEX_RANGE, "raw >= n_raw");
+  *active_mask_out = act;
+  return AS_OK;
+}
+
 as_status autoscout_cvi_to_raw(const as_space* s, uint64_t cvi, uint64_t* raw_out) {
   if (!s || !raw_out) return fail(AS_ERR_INVALID_ARG, "null argument");
   DV dv;

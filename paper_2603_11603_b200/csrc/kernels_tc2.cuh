@@ -97,7 +97,10 @@ struct Tc2B {
 // stale tau admits more keys, never fewer; rejected keys lower drop exactly as in group_admit.
 __device__ __forceinline__ void tc2_prune(uint64_t* arr, TopkSmem& ts, int KC, int t, int nt, int id) {
   const int n_tot = ts.n_list + ts.n_add;
+  // every thread has read n_tot before thread 0 rewrites ts (bitonic's barriers, or this one when
+  // there is nothing to sort -- compute-sanitizer racecheck)
   if (n_tot > 0) group_bitonic(arr, next_pow2(n_tot < 2 ? 2 : n_tot), t, nt, id);
+  else named_sync(id, nt);
   const int keep = n_tot < KC ? n_tot : KC;
   if (t == 0) {
     if (n_tot > KC && arr[KC] < ts.drop) ts.drop = arr[KC];
