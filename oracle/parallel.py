@@ -1,5 +1,5 @@
 """Oracle over all host cores: a full-size batch cut into contiguous shares, each share evaluated
-by oracle/batch.py in a forked worker process, the per-share results merged.
+by oracle/batch.py in a spawned worker process, the per-share results merged.
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Used by the full-size parity tests and by
 bench.py's cpu_baseline / --impl reference legs.  Merging is exact: valid counts add, and the
@@ -21,7 +21,7 @@ import numpy as np
 from . import acq as _acq
 from . import batch as _batch
 
-_CTX = {}      # inherited by the forked workers
+_CTX = {}      # per-process context (set by _init in every spawned worker)
 CHUNK = 1 << 15
 
 
@@ -122,29 +122,76 @@ def _shares(count, parts):
     return [(edges[i], edges[i + 1]) for i in range(parts) if edges[i + 1] > edges[i]]
 
 
-def _pool_map(fn, shares, procs):
-    if procs <= 1 or len(shares) == 1:
+def _init(ctx, worker=True):
+    """Worker start-up (spawned, not forked: the caller may hold a CUDA context and a threaded
+    BLAS, and a fork of such a process deadlocked the parent's next multithreaded LAPACK call)."""
+    if worker:
         _one_thread_blas()
-        return [fn(s) for s in shares]
-    with mp.get_context("fork").Pool(procs, initializer=_one_thread_blas) as pool:
-        return pool.map(fn, shares, chunksize=1)
+    _CTX.clear()
+    _CTX.update(ctx)
+    _CTX["unranker"] = _batch.Unranker(ctx["space"])
+
+
+class Pool:
+    """A persistent set of `procs` spawned oracle workers for one space and fit."""
+
+    def __init__(self, space, fit=None, procs=None):
+        self.procs = procs or cores()
+        self.ctx = dict(space=space, fit=fit)
+        self.pool = None
+        if self.procs > 1:
+            self.pool = mp.get_context("spawn").Pool(self.procs, initializer=_init, initargs=(self.ctx,))
+        else:
+            _init(self.ctx, worker=False)
+
+    def _map(self, fn, shares, extra):
+        if self.pool is None:
+            _CTX.update(extra)
+            return [fn(x) for x in shares]
+        return self.pool.map(fn, [(extra, x) for x in shares], chunksize=1)
+
+    def topk(self, mode, begin, count, k, seed=0, acq="ei", kappa=2.0, xi=0.0):
+        extra = dict(mode=mode, begin=begin, seed=seed, acq=acq, kappa=kappa, xi=xi, k=k)
+        fn = _work_score if self.pool is None else _work_score_x
+        res = self._map(fn, _shares(count, self.procs * 4), extra)
+        return _merge([r[0] for r in res], k), sum(r[1] for r in res)
+
+    def count_valid(self, begin, end):
+        fn = _work_valid if self.pool is None else _work_valid_x
+        return sum(self._map(fn, [(begin + a, begin + b) for a, b in _shares(end - begin, self.procs * 4)], {}))
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.close()
+            self.pool.join()
+            self.pool = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def _work_score_x(arg):
+    extra, share = arg
+    _CTX.update(extra)
+    return _work_score(share)
+
+
+def _work_valid_x(arg):
+    _, share = arg
+    return _work_valid(share)
 
 
 def topk(space, fit, mode, begin, count, k, seed=0, acq="ei", kappa=2.0, xi=0.0, procs=None):
     """Exact top-k (raw, score) and the valid count of a batch, over `procs` host processes."""
-    procs = procs or cores()
-    _CTX.clear()
-    _CTX.update(space=space, unranker=_batch.Unranker(space), fit=fit, mode=mode, begin=begin, seed=seed,
-                acq=acq, kappa=kappa, xi=xi, k=k)
-    res = _pool_map(_work_score, _shares(count, procs * 4), procs)
-    return _merge([r[0] for r in res], k), sum(r[1] for r in res)
+    with Pool(space, fit, procs) as P:
+        return P.topk(mode, begin, count, k, seed, acq, kappa, xi)
 
 
 def count_valid(space, begin=0, end=None, procs=None):
     """Number of CVI positions in [begin, end) that pass the resource check (G4)."""
-    procs = procs or cores()
     end = space.n_cvi() if end is None else end
-    _CTX.clear()
-    _CTX.update(space=space, unranker=_batch.Unranker(space))
-    res = _pool_map(_work_valid, [(begin + a, begin + b) for a, b in _shares(end - begin, procs * 4)], procs)
-    return sum(res)
+    with Pool(space, None, procs) as P:
+        return P.count_valid(begin, end)
