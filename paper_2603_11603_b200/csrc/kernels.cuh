@@ -154,11 +154,9 @@ __device__ __forceinline__ void decode_dev(const DevSpace& S, uint64_t p, DV& dv
 }
 
 // Tail of the CVI decode: structure record, then one mixed-radix digit (multiply-shift division)
-// and one tuple per gating group, OR-ed into the digit vector.  The per-group records of the
-// structure do not depend on each other and the division chain is a few integer ops, so for up to
-// DT_UNROLL groups every load is issued before any result is consumed: two memory round trips per
-// candidate instead of two per group (the generation kernel is load-latency bound).
-constexpr int DT_UNROLL = 6;
+// and one tuple per gating group, OR-ed into the digit vector.  (Issuing every group's loads ahead
+// of use was tried: with the unrolled register footprint the 3-block generation kernel spills and
+// the 2-block one loses latency hiding -- 5.56 -> 7.40 / 6.94 ms on C4.)
 __device__ __forceinline__ void decode_tail(const DevSpace& S, int lo, uint32_t t, DV& dv, uint32_t& act, uint64_t& raw) {
   const DV* sd = S.s_dv + lo;
   dv.w[0] = __ldg(&sd->w[0]);
@@ -166,35 +164,8 @@ __device__ __forceinline__ void decode_tail(const DevSpace& S, int lo, uint32_t 
   dv.w[2] = __ldg(&sd->w[2]);
   act = __ldg(S.s_act + lo);
   raw = __ldg(S.s_raw + lo);
-  const uint4* soc = S.s_oc + static_cast<size_t>(lo) * S.n_comp;
-  if (S.n_comp <= DT_UNROLL) {
-    uint4 oc[DT_UNROLL];
-#pragma unroll
-    for (int c = 0; c < DT_UNROLL; ++c)
-      if (c < S.n_comp) oc[c] = __ldg(soc + c);
-    uint32_t ti[DT_UNROLL];
-#pragma unroll
-    for (int c = DT_UNROLL - 1; c >= 0; --c)
-      if (c < S.n_comp) {
-        const uint32_t hi = __umulhi(oc[c].z, t);
-        const uint32_t q = (hi + ((t - hi) >> (oc[c].w & 0xFFu))) >> (oc[c].w >> 8);
-        ti[c] = oc[c].x + (t - q * oc[c].y);
-        t = q;
-      }
-#pragma unroll
-    for (int c = 0; c < DT_UNROLL; ++c)
-      if (c < S.n_comp) {
-        const Tuple* tu = S.tuples + ti[c];
-        dv.w[0] |= __ldg(&tu->dv.w[0]);
-        dv.w[1] |= __ldg(&tu->dv.w[1]);
-        dv.w[2] |= __ldg(&tu->dv.w[2]);
-        act |= __ldg(&tu->act);
-        raw += __ldg(&tu->raw);
-      }
-    return;
-  }
   for (int c = S.n_comp - 1; c >= 0; --c) {
-    const uint4 oc = __ldg(soc + c);
+    const uint4 oc = __ldg(S.s_oc + static_cast<size_t>(lo) * S.n_comp + c);
     const uint32_t hi = __umulhi(oc.z, t);
     const uint32_t q = (hi + ((t - hi) >> (oc.w & 0xFFu))) >> (oc.w >> 8);
     const uint32_t r = t - q * oc.y;
