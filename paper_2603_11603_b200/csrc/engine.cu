@@ -622,7 +622,7 @@ as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, b
         CUDA_TRY(cudaMemcpyToSymbol(g_tc2_trace, &tr_buf, sizeof(tr_buf)));
       }
       if (tr_buf != nullptr) CUDA_TRY(cudaMemsetAsync(tr_buf, 0, tr_n * 8, st));
-      k2<<<grid, TC_WARPS * 32 + 96, smem, st>>>(s->D, s->G, A, out, tb, s->t2, s->list);
+      k2<<<grid, TC_WARPS * 32 + 128, smem, st>>>(s->D, s->G, A, out, tb, s->t2, s->list);
       CUDA_TRY(cudaGetLastError());
       ++s->n_launches;
       if (tr_buf != nullptr) {

@@ -116,11 +116,11 @@ __device__ __forceinline__ void tc2_prune(uint64_t* arr, TopkSmem& ts, int KC, i
 // column offset becomes an immediate (no per-chunk address arithmetic on the FMA pipe).  NCH = 0:
 // any M <= 256, runtime indices.
 template <int PW, int KT, int NH, int NCH>
-__global__ void __launch_bounds__(PW * 32 + 96, 1)
+__global__ void __launch_bounds__(PW * 32 + 128, 1)
 score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, CandList L) {
   constexpr int TC_PROD_WARPS = PW;
   constexpr int TC_PROD_THREADS = PW * 32;
-  constexpr int TC_THREADS = TC_PROD_THREADS + 96;   // + MMA warp + loader warp + R2 warp
+  constexpr int TC_THREADS = TC_PROD_THREADS + 128;  // + MMA warp + loader warp + R2 warp + L^-1 loader warp
   constexpr int TC_JQ = TC_PROD_THREADS / TC_ROWS;   // producer threads per candidate
   constexpr int TC_JPT = TC_KCH / TC_JQ;             // observed points per thread per chunk
   static_assert(TC_JQ == 4 && TC_JPT == 4, "R2 group columns are laid out for 16 producer warps");
@@ -678,6 +678,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     auto tile_exists = [&](int u) -> bool { return u < my_tiles; };
     __syncwarp();
     const uint64_t dB = tc::sdesc(sB0, 128, (TC_KCH / 8) * 128);
+    long long wa_acc = 0, wb_acc = 0;
     for (int t = 0; tile_exists(t); ++t) {
       TR(t, 8);
       tc::mbar_wait(d_empty, (t & 1) ^ 1);
@@ -690,8 +691,14 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       auto mma_chunk = [&](int c) {
         const uint32_t ga = static_cast<uint32_t>(t) * static_cast<uint32_t>(nch) + static_cast<uint32_t>(c);
         const int sa = ga % TC2_NA, sbb = g % TC2_NB;
+        const long long w0 = trace != nullptr ? clock64() : 0;
         tc::mbar_wait(a_full + sa, (ga / TC2_NA) & 1);
+        const long long w1 = trace != nullptr ? clock64() : 0;
         tc::mbar_wait(b_full + sbb, (g / TC2_NB) & 1);
+        if (trace != nullptr) {
+          wa_acc += w1 - w0;
+          wb_acc += clock64() - w1;
+        }
         if (c == TC2_NA) TR(t, 11);
         tc::fence_after_sync();
         const int N = Mp16 - c * TC_KCH;
@@ -712,6 +719,11 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       }
       tc::mma_commit_w(d_full);
       TR(t, 10);
+      if (trace != nullptr && lane == 0 && t < TC2_TR_TILES) {   // MMA warp: cycles waiting on A / B per tile
+        trace[(static_cast<size_t>(t) * TC2_TR_EV + 12) * 18 + warp] = static_cast<unsigned long long>(wa_acc);
+        trace[(static_cast<size_t>(t) * TC2_TR_EV + 13) * 18 + warp] = static_cast<unsigned long long>(wb_acc);
+      }
+      wa_acc = wb_acc = 0;
     }
     __syncwarp();
   } else if (warp == TC_PROD_WARPS + 2) {
@@ -744,16 +756,34 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       }
     }
     __syncwarp();
+  } else if (warp == TC_PROD_WARPS + 3) {
+    // =========================================================== L^-1 chunk loader (sub-partition 3)
+    // The MMA warp's critical operand: refill a ring slot the moment its MMAs complete (blocking
+    // wait, no polling back-off) -- the polling loader made the MMA warp wait ~7300 cycles per
+    // tile on b_full (CTA-0 trace), three times its wait for the producers' A stages.
+    if (lane == 0) {
+      const uint32_t tot_L = static_cast<uint32_t>(my_tiles) * nch;
+      int lc = 0;
+      for (uint32_t gl = 0; gl < tot_L; ++gl) {
+        const int s_ = gl % TC2_NB;
+        tc::mbar_wait(b_empty + s_, ((gl / TC2_NB) & 1u) ^ 1u);
+        const uint32_t bytes = 2u * (Mp16 - lc * TC_KCH) * TC_KCH * 2;
+        tc::mbar_arrive_expect_tx(b_full + s_, bytes);
+        tc::bulk_g2s(B0 + static_cast<size_t>(s_) * b_stage_bytes, T2.wch + T2.woff[lc], bytes, b_full + s_);
+        if (++lc == nch) lc = 0;
+      }
+    }
+    __syncwarp();
   } else {
     // =========================================================== loader (lane 0)
     // Keeps the three bulk-copy rings full with non-blocking tests: L^-1 chunks (refill of a slot
     // once its MMAs completed), T groups (once their R2 MMAs completed), staged list records (once
     // published).  Exactly the CTA's totals are loaded, so nothing is left in flight at exit.
     if (lane == 0) {
-      const uint32_t tot_L = static_cast<uint32_t>(my_tiles) * nch, tot_T = static_cast<uint32_t>(my_tiles) * ng;
-      uint32_t gl = 0, xl = 0;
-      int lc = 0, xc = 0, sl = 0;
-      while (gl < tot_L || xl < tot_T || sl < my_tiles) {
+      const uint32_t tot_T = static_cast<uint32_t>(my_tiles) * ng;
+      uint32_t xl = 0;
+      int xc = 0, sl = 0;
+      while (xl < tot_T || sl < my_tiles) {
         bool prog = false;
         if (sl < my_tiles && tc::mbar_test(s_empty + (sl & 1), ((sl >> 1) & 1u) ^ 1u)) {
           const uint64_t r0 = (blockIdx.x + static_cast<uint64_t>(sl) * gridDim.x) * TC_ROWS;
@@ -769,15 +799,6 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
           tc::bulk_g2s(sg + TC2_STG_DV1, L.dv1 + r0, b8, bar);
           tc::bulk_g2s(sg + TC2_STG_DV2, L.dv2 + r0, b8, bar);
           ++sl;
-          prog = true;
-        }
-        if (gl < tot_L && tc::mbar_test(b_empty + (gl % TC2_NB), ((gl / TC2_NB) & 1u) ^ 1u)) {
-          const int s_ = gl % TC2_NB;
-          const uint32_t bytes = 2u * (Mp16 - lc * TC_KCH) * TC_KCH * 2;
-          tc::mbar_arrive_expect_tx(b_full + s_, bytes);
-          tc::bulk_g2s(B0 + static_cast<size_t>(s_) * b_stage_bytes, T2.wch + T2.woff[lc], bytes, b_full + s_);
-          ++gl;
-          if (++lc == nch) lc = 0;
           prog = true;
         }
         if (xl < tot_T && tc::mbar_test(x_empty + (xl % TC2_NT), ((xl / TC2_NT) & 1u) ^ 1u)) {

@@ -32,3 +32,5 @@ pe = [(5, 13, "finalize: sums"), (13, 14, "finalize: acq32"), (14, 6, "finalize:
 for a_, b_, nm in pe:
     d = np.array([prod[t, b_, :4] - prod[t, a_, :4] for t in ok])
     print(f"  {nm:18s} warps 0-3 mean %7.0f  max %7.0f" % (d.mean(), d.max(axis=1).mean()))
+wa = np.array([x[t, 12, 16] for t in ok]); wb = np.array([x[t, 13, 16] for t in ok])
+print("  MMA warp per tile: waiting a_full %.0f cycles, waiting b_full %.0f cycles" % (wa.mean(), wb.mean()))
