@@ -34,3 +34,5 @@ for a_, b_, nm in pe:
     print(f"  {nm:18s} warps 0-3 mean %7.0f  max %7.0f" % (d.mean(), d.max(axis=1).mean()))
 wa = np.array([x[t, 12, 16] for t in ok]); wb = np.array([x[t, 13, 16] for t in ok])
 print("  MMA warp per tile: waiting a_full %.0f cycles, waiting b_full %.0f cycles" % (wa.mean(), wb.mean()))
+r_t = np.array([x[t, 12, 17] for t in ok]); r_r = np.array([x[t, 13, 17] for t in ok]); r_x = np.array([x[t, 14, 17] for t in ok])
+print("  R2 warp per tile: waiting t_ready %.0f, r_empty %.0f, x_full (T stage) %.0f cycles" % (r_t.mean(), r_r.mean(), r_x.mean()))
