@@ -37,7 +37,8 @@ EXPORTS = ["autoscout_space_create", "autoscout_space_destroy", "autoscout_space
            "autoscout_sample_to_cvi", "autoscout_simulate", "autoscout_mask_range", "autoscout_set_path",
            "autoscout_set_timing", "autoscout_raw_to_cvi", "autoscout_subtree_range", "autoscout_neighbors",
            "autoscout_prior", "autoscout_ensemble_info", "autoscout_gp_lml", "autoscout_set_gp_hyper",
-           "autoscout_ml2", "autoscout_set_slice",
+           "autoscout_ml2", "autoscout_set_slice", "autoscout_topk_pool_device", "autoscout_topk_merge_device",
+           "autoscout_activity",
            "autoscout_last_kernel_ms", "autoscout_last_phase_ms", "autoscout_last_error"]
 
 
