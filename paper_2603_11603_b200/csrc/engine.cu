@@ -616,13 +616,13 @@ as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, b
       if (ev) CUDA_TRY(cudaEventRecord(s->sev[s->sev_used + 1], st));
       static unsigned long long* tr_buf = nullptr;
       const char* tr_path = std::getenv("AS_TC2_TRACE");   // development aid: CTA-0 phase timeline
-      const size_t tr_n = static_cast<size_t>(TC2_TR_TILES) * TC2_TR_EV * 18;
+      const size_t tr_n = static_cast<size_t>(TC2_TR_TILES) * TC2_TR_EV * TC2_TR_W;
       if (tr_path != nullptr && tr_buf == nullptr) {
         CUDA_TRY(cudaMalloc(&tr_buf, tr_n * 8));
         CUDA_TRY(cudaMemcpyToSymbol(g_tc2_trace, &tr_buf, sizeof(tr_buf)));
       }
       if (tr_buf != nullptr) CUDA_TRY(cudaMemsetAsync(tr_buf, 0, tr_n * 8, st));
-      k2<<<grid, TC_WARPS * 32 + 128, smem, st>>>(s->D, s->G, A, out, tb, s->t2, s->list);
+      k2<<<grid, TC2_THREADS, smem, st>>>(s->D, s->G, A, out, tb, s->t2, s->list);
       CUDA_TRY(cudaGetLastError());
       ++s->n_launches;
       if (tr_buf != nullptr) {

@@ -15,16 +15,20 @@
 // per candidate x observed pair); they read R2 from TMEM and evaluate k(r) only.  Candidates come
 // from the compact list of gen_kernel (kernels_gen.cuh): decode, mask and simulator run there.
 //
-// Warp roles (576 threads, 1 CTA per SM):
+// Warp roles (768 threads, 1 CTA per SM; registers rebalanced by setmaxnreg: producers 96, the
+// other two warpgroups 48):
 //   warps 0-15  producers: publish tile t+1 (meta + E rows + SIMT-feature values from the staged
 //               list records) BEFORE the chunk loop of tile t, so the R2 MMAs of t+1 overlap tile t;
 //               chunk loop: R2 group from TMEM -> k -> FP16 hi/lo -> A ring (TMEM); head start on
-//               tile t+1; epilogue (|v|^2 of the last column blocks; warps 0-3 finalise the rows:
-//               FP32 screen + certified bound, lazy CTA top-k').
-//   warp 16     MMA issuer (warp-converged, one elected lane issues): R2 groups ahead of the
-//               L^-1 chunks in one instruction stream.
-//   warp 17     loader: bulk copies of the L^-1 chunks, T groups and staged list records, and the
-//               zero-fill of used one-hot buffers.
+//               tile t+1; epilogue read (|v|^2 of the last column blocks), then tile t is handed to
+//               the finalize warps through an mbarrier (f_ready) -- no CTA barrier.
+//   warp 16     L^-1 MMA issuer (warp-converged, one elected lane issues).
+//   warp 17     loader: bulk copies of the T groups and staged list records, and the zero-fill of
+//               used one-hot buffers.
+//   warp 18     R2 MMA issuer.        warp 19  L^-1 chunk loader.
+//   warps 20-23 finalize (one per SM sub-partition, row = 32 (warp - 20) + lane): FP32 screen +
+//               certified bound, lazy CTA top-k' of tile t while the producers run tile t+1; they
+//               release the tile's slots (partial sums, |v|^2, meta) through f_free.
 // TMEM: D [Mp16] | A ring [8 x 16] | R2 ring [2 groups x 64]  (Mp16 <= 256 -> <= 512 columns).
 #pragma once
 #include "kernels_gen.cuh"
@@ -42,6 +46,10 @@ constexpr int TC2_NT = 2;                    // T group ring stages (refilled ea
 constexpr int TC2_KPMAX = 64;                // one-hot width the host aims for (features beyond go SIMT)
 constexpr int TC2_TI = 3;                    // meta slots (cvi, j, m0): read by finalize() one tile later
 constexpr int TC2_CB = 1;                    // chunks whose math is batched ahead of their A-stage waits (ILP)
+constexpr int TC2_XW = 8;                    // non-producer warps (MMA, loader, R2, L^-1 loader, 4 finalize)
+constexpr int TC2_THREADS = 16 * 32 + TC2_XW * 32;
+constexpr int TC2_PROD_REGS = 96;            // setmaxnreg: producers 96, the others 48 (80 at launch)
+constexpr int TC2_AUX_REGS = 48;
 
 // Shared-memory carve-out: the fixed-size arrays first (compile-time offsets, so the hot loop
 // addresses them with immediates), then the rings whose size depends on M and Kp.
@@ -52,7 +60,7 @@ constexpr size_t TC2_O_OH = TC2_O_ALPHA + 2 * MMAX * 4;
 constexpr size_t TC2_O_MXH = TC2_O_OH + 4 * MMAX * 4;
 constexpr size_t TC2_O_MPART = TC2_O_MXH + 4 * TC_TI * TC_ROWS * 4;
 constexpr size_t TC2_O_VPART = TC2_O_MPART + TC_TI * 4 * 3 * TC_ROWS * 4;   // [TI][jq][3][128]: one slot per thread
-constexpr size_t TC2_O_MCVI = TC2_O_VPART + 4 * TC_ROWS * 4;
+constexpr size_t TC2_O_MCVI = TC2_O_VPART + 2 * 4 * TC_ROWS * 4;   // vpart: [2 slots][jq][128]
 constexpr size_t TC2_O_MJ = TC2_O_MCVI + TC2_TI * TC_ROWS * 4;
 constexpr size_t TC2_O_MM0 = TC2_O_MJ + TC2_TI * TC_ROWS * 4;
 constexpr size_t TC2_O_XH = TC2_O_MM0 + TC2_TI * TC_ROWS * 8;
@@ -69,7 +77,7 @@ __host__ __device__ constexpr size_t tc2_smem_total(int Mp16, int Kp, int P) {
 
 // Phase timeline of CTA 0 (development aid, off unless the host sets AS_TC2_TRACE): clock64 per
 // (tile < TC2_TR_TILES, event, warp); written by lane 0 of each warp.
-constexpr int TC2_TR_TILES = 64, TC2_TR_EV = 16;
+constexpr int TC2_TR_TILES = 64, TC2_TR_EV = 16, TC2_TR_W = 24;
 __device__ unsigned long long* g_tc2_trace = nullptr;
 
 struct Tc2B {
@@ -111,16 +119,16 @@ __device__ __forceinline__ void tc2_prune(uint64_t* arr, TopkSmem& ts, int KC, i
   for (int i = keep + t; i < n_tot; i += nt) arr[i] = KEY_NONE;
   named_sync(id, nt);
 }
-// NCH > 0: the number of K-chunks (Mp16 / 16) as a compile-time constant (16: M = 256, 8: M = 128);
-// the chunk loop then unrolls completely and every A-ring stage, R2 slot, mbarrier parity and TMEM
-// column offset becomes an immediate (no per-chunk address arithmetic on the FMA pipe).  NCH = 0:
-// any M <= 256, runtime indices.
+// NCH > 0: the number of K-chunks (Mp16 / 16) as a compile-time constant (16: M = 256, 8: M = 128):
+// ring stages, parities and TMEM offsets reduce to cheap functions of the group index (the group
+// and chunk loops themselves stay rolled for the instruction cache).  NCH = 0: any M <= 256.
 template <int PW, int KT, int NH, int NCH>
-__global__ void __launch_bounds__(PW * 32 + 128, 1)
+__global__ void __launch_bounds__(PW * 32 + TC2_XW * 32, 1)
 score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, CandList L) {
   constexpr int TC_PROD_WARPS = PW;
   constexpr int TC_PROD_THREADS = PW * 32;
-  constexpr int TC_THREADS = TC_PROD_THREADS + 128;  // + MMA warp + loader warp + R2 warp + L^-1 loader warp
+  constexpr int TC_THREADS = TC_PROD_THREADS + TC2_XW * 32;  // + MMA, loader, R2, L^-1 loader, 4 finalize warps
+  constexpr int FW0 = PW + 4;                                // first finalize warp
   constexpr int TC_JQ = TC_PROD_THREADS / TC_ROWS;   // producer threads per candidate
   constexpr int TC_JPT = TC_KCH / TC_JQ;             // observed points per thread per chunk
   static_assert(TC_JQ == 4 && TC_JPT == 4, "R2 group columns are laid out for 16 producer warps");
@@ -134,7 +142,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
   unsigned long long* const trace = blockIdx.x == 0 ? g_tc2_trace : nullptr;
   auto TR = [&](int u, int ev) {
     if (trace != nullptr && lane == 0 && u < TC2_TR_TILES)
-      trace[(static_cast<size_t>(u) * TC2_TR_EV + ev) * 18 + warp] = clock64();
+      trace[(static_cast<size_t>(u) * TC2_TR_EV + ev) * TC2_TR_W + warp] = clock64();
   };
   const int ng = (nch + TC2_RG - 1) / TC2_RG;                         // R2 groups per tile
   const uint32_t A0col = static_cast<uint32_t>(Mp16);                 // TMEM column of A stage 0
@@ -177,6 +185,8 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
   uint64_t* s_full = x_empty + TC2_NT;         // [2]  1 + tx  (tile records staged)
   uint64_t* s_empty = s_full + 2;              // [2]  count PW
   uint64_t* ez_full = s_empty + 2;             // [2]  1 + tx  (E buffer zeroed again by a bulk copy)
+  uint64_t* f_ready = ez_full + 2;             // [2]  count PW  (tile partial sums + |v|^2 written)
+  uint64_t* f_free = f_ready + 2;              // [2]  count 4   (finalize done with the tile's slots)
 
   // ---- setup
   // point-pair layout: [al_2p, al_2p+1, |al_2p|, |al_2p+1|] so one LDS.128 feeds packed f32x2 math
@@ -225,6 +235,8 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       tc::mbar_init(s_full + s, 1);
       tc::mbar_init(s_empty + s, TC_PROD_WARPS);
       tc::mbar_init(ez_full + s, 1);
+      tc::mbar_init(f_ready + s, TC_PROD_WARPS);
+      tc::mbar_init(f_free + s, TC_EPI_WARPS);
     }
     tc::mbar_fence_init();
     ts.n_list = 0;
@@ -240,7 +252,8 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
   const uint32_t tmem = tmem_base;
 
   if (warp < TC_PROD_WARPS) {
-    // =========================================================== producers (+ epilogue)
+    // =========================================================== producers (+ epilogue read)
+    tc::setmaxnreg_inc<TC2_PROD_REGS>();
     const int pt = tid;
     const int cand = pt & (TC_ROWS - 1);
     const int jq = pt >> 7;
@@ -252,7 +265,6 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     const float c_arg = (KT == 0) ? 2.2360679774997896f * T2.r_scale : 0.5f * T2.r2_scale;
     const float ex_c1 = -c_arg * 1.4426950408889634f;
     const float ex_c0 = log2f(G.sf2f) + static_cast<float>(T2.ek);   // k leaves the exp2 scaled by 2^ek
-    double* scratch = TB.scratch + (static_cast<size_t>(blockIdx.x) * TC_EPI_WARPS + (warp & 3)) * Mp16;
 
     // ---- epilogue of tile u (column blocks < nch - NA were accumulated during the chunk loop)
     // ---- epilogue, part 1 (all producer warps): the last NA column blocks of D -> |v|^2 partial,
@@ -276,139 +288,14 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
             vsq = fmaf(v[4 * i], v[4 * i],
                        fmaf(v[4 * i + 1], v[4 * i + 1], fmaf(v[4 * i + 2], v[4 * i + 2], fmaf(v[4 * i + 3], v[4 * i + 3], vsq))));
       }
-      vpart[jq * TC_ROWS + quad * 32 + lane] = vsq * T2.vsq_unscale;
+      vpart[((u & 1) * TC_JQ + jq) * TC_ROWS + quad * 32 + lane] = vsq * T2.vsq_unscale;
       tc::fence_before_sync();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(d_empty);
+      if (lane == 0) {
+        tc::mbar_arrive(d_empty);
+        tc::mbar_arrive(f_ready + (u & 1));   // partial sums (flush_part) + |v|^2 of tile u -> finalize warps
+      }
       TR(u, 5);
-    };
-
-    // ---- epilogue, part 2 (warps 0-3, row = pt): FP32 screen + bound of tile u's rows and lazy
-    // admission.  Keys that lose against tau lower this thread's drop_r instead of a shared atomicMin
-    // per row (min is order-free; reduced once at the end, and tc2_prune lowers ts.drop as before).
-    uint64_t drop_r = KEY_NONE;
-    auto finalize = [&](int u, int n) {
-      const int us = u % TC_TI, ms = u % TC2_TI;
-      uint64_t key = KEY_NONE;
-      bool sensitive = false;
-      const int row = pt;
-      float mu32 = 0.f, sb = 0.f, kk = 0.f, vv = 0.f, mu = 0.f, s2 = 0.f, d_mu = 0.f, d_s2 = 0.f;
-      double cm0 = 0.0;
-      bool early = false;
-      if (pt < n) {
-#pragma unroll
-        for (int q = 0; q < TC_JQ; ++q) {
-          const float* mp = m_part + (us * TC_JQ + q) * 3 * TC_ROWS;
-          mu32 += mp[row];
-          sb += mp[TC_ROWS + row];
-          kk += mp[2 * TC_ROWS + row];
-          vv += vpart[q * TC_ROWS + row];
-        }
-        cm0 = m_m0[ms * TC_ROWS + row];
-        TR(u, 13);
-        mu = static_cast<float>(cm0 + G.b) + mu32;
-        const float vs = vv;
-        s2 = static_cast<float>(G.sf2) - vs;
-        // FP32 k + 3xTF32 contraction: error coefficient 8x the SIMT one (DESIGN.md §5.6)
-        const float eps = 8.0f * static_cast<float>(G.eps);
-        d_mu = eps * sb + 2e-7f * (1.0f + fabsf(mu));
-        const float ew = eps * static_cast<float>(G.w_fro);
-        d_s2 = 2.5f * ew * sqrtf(vs * kk) + ew * ew * kk + eps * vs + 8.0f * U32 * G.sf2f;
-        // Early rejection (EI, bench path only): a cheap upper bound of the admission score,
-        //   ln sigma + ln h(z),  h(z) <= phi(z) / (1 + z^2) for z <= 0 (Mills ratio
-        //   Q(x) >= x phi(x) / (1 + x^2)),  h(z) <= z + phi(0) for z > 0,
-        // at the same (mu - d_mu, s2 + d_s2) as the exact screen, plus slack covering twice the
-        // screen's evaluation margin and its own MUFU rounding: its key never exceeds the exact
-        // admission key, so key >= tau rejects exactly the rows the exact screen would reject, and
-        // the (smaller) cheap key is a valid entry for the best-dropped bound.
-        const uint64_t tau = ts.tau;
-        if (A.acq == 0 && !A.d_scores && !A.d_screen && tau != KEY_NONE) {
-          const float s2p = s2 + d_s2;
-          if (s2p > 0.0f) {
-            const float z = (static_cast<float>(G.fstar) - (mu - d_mu) - static_cast<float>(A.xi)) * rsqrtf(s2p);
-            const float lnhb = z > 0.0f ? __logf(z + 0.3989422804014327f)
-                                        : -0.5f * z * z - 0.9189385332046727f - __logf(1.0f + z * z);
-            const float cheap = 0.5f * __logf(s2p) + lnhb;
-            const float cheap_ub = cheap + 2e-5f * (1.0f + fabsf(cheap) + z * z);
-            const uint64_t kc = make_key(cheap_ub, m_cvi[ms * TC_ROWS + row]);
-            if (kc >= tau) {
-              early = true;
-              if (kc < drop_r) drop_r = kc;
-            }
-          }
-        }
-      }
-      const bool warp_early = __all_sync(0xffffffffu, early || pt >= n);
-      if (pt < n && !early && !warp_early) {
-        const float fstar = static_cast<float>(G.fstar), m0f = static_cast<float>(cm0);
-        float m2;
-        float ub = acquisition32(A.acq, mu - d_mu, s2 + d_s2, m0f, fstar, static_cast<float>(A.xi),
-                                 static_cast<float>(A.kappa), m2);
-        ub += m2;
-        if (A.d_screen) {   // parity / debug output of the screen (never on the bench path)
-          float m3;
-          const float scr = acquisition32(A.acq, mu, s2, m0f, fstar, static_cast<float>(A.xi),
-                                          static_cast<float>(A.kappa), m3);
-          *reinterpret_cast<float4*>(A.d_screen + 4ull * m_j[ms * TC_ROWS + row]) = make_float4(mu, s2, scr, ub);
-        }
-        TR(u, 14);
-        if (A.d_scores) {
-          const double mud = cm0 + G.b + static_cast<double>(mu32);
-          const double s2d = G.sf2 - static_cast<double>(vv);
-          if (A.acq == 0) {
-            if (s2d > 0.0) {
-              const double sg = sqrt(s2d), z = (G.fstar - mud - A.xi) / sg;
-              if (z >= -3.2) {
-                const double Phi = 0.5 * erfc(-z * INV_SQRT2);
-                const double h = exp(-0.5 * z * z) * INV_SQRT_2PI + z * Phi;
-                const double uu = static_cast<double>(U32);
-                // R2 from the tensor cores: mu error model 4u(1 + sb) (DESIGN.md §5.9)
-                const double e_s = (1.0 - z * Phi / h) / (2.0 * s2d) * 160.0 * uu * static_cast<double>(vv) +
-                                   Phi / (sg * h) * 4.0 * uu * (1.0 + static_cast<double>(sb));
-                sensitive = e_s > 5e-6;
-              }
-            } else {
-              sensitive = true;
-            }
-          }
-          if (!sensitive)
-            A.d_scores[m_j[ms * TC_ROWS + row]] =
-                static_cast<float>(acquisition(A.acq, mud, s2d, cm0, G.fstar, A.xi, A.kappa));
-        }
-        if (!sensitive && ub > -INFINITY) key = make_key(ub, m_cvi[ms * TC_ROWS + row]);
-      }
-      {
-        unsigned fl = __ballot_sync(0xffffffffu, sensitive);
-        while (fl) {
-          const int src = __ffs(fl) - 1;
-          fl &= fl - 1;
-          const int row = warp * 32 + src;
-          const uint32_t cvi = m_cvi[ms * TC_ROWS + row];
-          DV dv;
-          uint32_t act;
-          uint64_t raw;
-          decode_dev(S, cvi, dv, act, raw);
-          double kalpha, vq;
-          posterior64_warp(S, G, dv, lane, scratch, kalpha, vq);
-          if (lane == src) {
-            const double cm0 = m_m0[ms * TC_ROWS + row];
-            const double sc = acquisition(A.acq, cm0 + G.b + kalpha, G.sf2 - vq, cm0, G.fstar, A.xi, A.kappa);
-            const double ub = sc + 1e-12 * fmax(1.0, fabs(sc));
-            A.d_scores[m_j[ms * TC_ROWS + row]] = static_cast<float>(sc);
-            if (ub > -INFINITY) key = make_key(__double2float_ru(ub), cvi);
-          }
-        }
-      }
-      TR(u, 6);
-      if (key != KEY_NONE) {
-        if (key < ts.tau) {
-          const int pos = atomicAdd(&ts.n_add, 1);
-          arr[ts.n_list + pos] = key;
-        } else if (key < drop_r) {
-          drop_r = key;
-        }
-      }
-      TR(u, 7);
     };
 
     // publish tile u: meta rows, zeroed partial sums, one-hot rows E[u & 1] and the SIMT-feature
@@ -478,7 +365,10 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       const unsigned long long carg2 = f2_pack(c_arg, c_arg), c1_2 = f2_pack(ex_c1, ex_c1),
                                c0_2 = f2_pack(ex_c0, ex_c0), one2 = f2_pack(1.0f, 1.0f),
                                third2 = f2_pack(0.33333333333333333f, 0.33333333333333333f);
-#pragma unroll
+        // R2 groups are NOT unrolled: one group body (~360 instructions) keeps the producers' hot
+        // loop inside the instruction cache (the fully unrolled 16-chunk loop was 26-43 KB of code and
+        // stalled every warp on instruction fetch, ncu no_inst 19 % of samples)
+#pragma unroll 1
         for (int c0 = cb; c0 < ce; c0 += TC2_RG) {
           // ---- one R2 group: the thread's 4 points of each of the 4 chunks are 16 contiguous
           // columns (T rows are permuted on the host), read with one load
@@ -622,54 +512,42 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     // Tile loop.  Before the epilogue of tile t (which waits for all of t's MMAs) the producers
     // already produce the first NA chunks of tile t+1 into the A ring, so the MMA drain of tile t
     // overlaps useful work and the MMAs of t+1 start as soon as the accumulator is read out.
-    const int head = nch < TC2_NA ? nch : TC2_NA;    // multiple of the R2 group size, or all of nch
+    // One instruction copy of each chunk range (the chunk loop is unrolled, and the code must stay
+    // small for the instruction cache): iteration t = -1 only produces the head of tile 0.
+    constexpr int HEADC = NCH < TC2_NA ? NCH : TC2_NA;
+    const int head = NCH > 0 ? HEADC : (nch < TC2_NA ? nch : TC2_NA);   // multiple of the R2 group size, or all of nch
     unsigned long long mu_c = 0ull, sb_c = 0ull, kk_c = 0ull;  // tile t's running sums (packed pairs)
-    float vsq_c = 0.f;
-    int pre = 0;                                              // chunks of tile t already produced
-    for (int t = 0; n_cur > 0; ++t) {
-      TR(t, 0);
-      const int n_next = publish(t + 1);
-      TR(t, 1);
-      if (NCH > 0) {
-        constexpr int HEAD = NCH < TC2_NA ? NCH : TC2_NA;
-        if (pre == HEAD) produce(t, HEAD, NCH, mu_c, sb_c, kk_c, vsq_c);
-        else produce(t, 0, NCH, mu_c, sb_c, kk_c, vsq_c);
-      } else {
-        produce(t, pre, nch, mu_c, sb_c, kk_c, vsq_c);
+    float vsq_c = 0.f, vsq_t = 0.f;
+    int n_next = n_cur;                                       // rows of tile t + 1
+    n_cur = 0;                                                // rows of tile t
+    for (int t = -1; t < 0 || n_cur > 0; ++t) {
+      if (t >= 0) {
+        TR(t, 0);
+        // slots of tile t - 2 (meta (t + 1) % 3, partial sums and |v|^2 t & 1) released by the finalize warps
+        if (t >= 2) tc::mbar_wait(f_free + (t & 1), ((t >> 1) + 1) & 1);
+        n_next = publish(t + 1);
+        TR(t, 1);
+        if (NCH > 0) produce(t, HEADC, NCH, mu_c, sb_c, kk_c, vsq_c);
+        else produce(t, head, nch, mu_c, sb_c, kk_c, vsq_c);
+        TR(t, 2);
+        flush_part(t, mu_c, sb_c, kk_c);
+        vsq_t = vsq_c;
+        mu_c = sb_c = kk_c = 0ull;
+        vsq_c = 0.f;
       }
-      TR(t, 2);
-      flush_part(t, mu_c, sb_c, kk_c);
-      const float vsq_t = vsq_c;
-      mu_c = sb_c = kk_c = 0ull;
-      vsq_c = 0.f;
-      pre = 0;
       if (n_next > 0) {
-        if (NCH > 0) produce(t + 1, 0, NCH < TC2_NA ? NCH : TC2_NA, mu_c, sb_c, kk_c, vsq_c);
+        if (NCH > 0) produce(t + 1, 0, HEADC, mu_c, sb_c, kk_c, vsq_c);
         else produce(t + 1, 0, head, mu_c, sb_c, kk_c, vsq_c);
-        pre = head;
       }
-      TR(t, 3);
-      epilogue_read(t, vsq_t);
-      named_sync(1, TC_PROD_THREADS);       // partial sums and |v|^2 of tile t visible
-      if (warp < TC_EPI_WARPS) finalize(t, n_cur);
-      named_sync(1, TC_PROD_THREADS);       // admissions done: uniform prune decision
-      if (ts.n_list + ts.n_add > out.P - TC_ROWS) tc2_prune(arr, ts, out.KC, pt, TC_PROD_THREADS, 1);
-      // (no further barrier: publish(t + 2)'s barrier orders every reuse of tile t's slots)
+      if (t >= 0) {
+        TR(t, 3);
+        epilogue_read(t, vsq_t);              // hands tile t to the finalize warps (f_ready)
+      }
       n_cur = n_next;
     }
-    // ---- best dropped key, CTA list (final prune: sorted, at most KC entries)
-    if (drop_r != KEY_NONE)
-      atomicMin(reinterpret_cast<unsigned long long*>(&ts.drop), static_cast<unsigned long long>(drop_r));
-    named_sync(1, TC_PROD_THREADS);
-    tc2_prune(arr, ts, out.KC, pt, TC_PROD_THREADS, 1);
-    const int n = ts.n_list;
-    uint64_t* dst = out.lists + static_cast<size_t>(blockIdx.x) * out.KC;
-    for (int i = pt; i < n; i += TC_PROD_THREADS) dst[i] = arr[i];
-    if (pt == 0) {
-      out.counts[blockIdx.x] = n;
-      out.drop[blockIdx.x] = ts.drop;
-    }
-  } else if (warp == TC_PROD_WARPS) {
+  } else {
+  tc::setmaxnreg_dec<TC2_AUX_REGS>();
+  if (warp == TC_PROD_WARPS) {
     // =========================================================== MMA issuer
     // The whole warp runs this loop in lock-step (warp-uniform state); one elected lane issues the
     // MMAs / commits (elect.sync inside the asm).  All bulk copies are the loader warp's, so this
@@ -684,10 +562,8 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       tc::mbar_wait(d_empty, (t & 1) ^ 1);
       TR(t, 9);
       tc::fence_after_sync();
-      // one chunk: operand waits, 3 MMAs + 2 commits.  With a compile-time chunk
-      // count the loop below unrolls, so N, idesc, the D / A columns and the A-stage parity are
-      // immediates (the MMA warp shares SM sub-partition 0 with four producer warps: its
-      // instruction count paces the lock-step pipeline)
+      // one chunk: operand waits, 3 MMAs + 2 commits (rolled: unrolling it gained nothing once the
+      // producers' code fit the instruction cache, and it spilled at 48 registers)
       auto mma_chunk = [&](int c) {
         const uint32_t ga = static_cast<uint32_t>(t) * static_cast<uint32_t>(nch) + static_cast<uint32_t>(c);
         const int sa = ga % TC2_NA, sbb = g % TC2_NB;
@@ -712,7 +588,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         ++g;
       };
       if (NCH > 0) {
-#pragma unroll
+#pragma unroll 1
         for (int c = 0; c < (NCH > 0 ? NCH : 1); ++c) mma_chunk(c);
       } else {
         for (int c = 0; c < nch; ++c) mma_chunk(c);
@@ -720,8 +596,8 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       tc::mma_commit_w(d_full);
       TR(t, 10);
       if (trace != nullptr && lane == 0 && t < TC2_TR_TILES) {   // MMA warp: cycles waiting on A / B per tile
-        trace[(static_cast<size_t>(t) * TC2_TR_EV + 12) * 18 + warp] = static_cast<unsigned long long>(wa_acc);
-        trace[(static_cast<size_t>(t) * TC2_TR_EV + 13) * 18 + warp] = static_cast<unsigned long long>(wb_acc);
+        trace[(static_cast<size_t>(t) * TC2_TR_EV + 12) * TC2_TR_W + warp] = static_cast<unsigned long long>(wa_acc);
+        trace[(static_cast<size_t>(t) * TC2_TR_EV + 13) * TC2_TR_W + warp] = static_cast<unsigned long long>(wb_acc);
       }
       wa_acc = wb_acc = 0;
     }
@@ -774,7 +650,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       }
     }
     __syncwarp();
-  } else {
+  } else if (warp == TC_PROD_WARPS + 1) {
     // =========================================================== loader (lane 0)
     // Keeps the three bulk-copy rings full with non-blocking tests: L^-1 chunks (refill of a slot
     // once its MMAs completed), T groups (once their R2 MMAs completed), staged list records (once
@@ -824,6 +700,164 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       }
     }
     __syncwarp();
+  } else {
+    // =========================================================== finalize (warps 20-23)
+    const int pt = tid - FW0 * 32;                       // row of the tile
+    double* scratch = TB.scratch + (static_cast<size_t>(blockIdx.x) * TC_EPI_WARPS + (warp & 3)) * Mp16;
+    // ---- finalize (row = pt): FP32 screen + bound of tile u's rows and lazy admission.  Keys that
+    // lose against tau lower this thread's drop_r instead of a shared atomicMin
+    // per row (min is order-free; reduced once at the end, and tc2_prune lowers ts.drop as before).
+    uint64_t drop_r = KEY_NONE;
+    auto finalize = [&](int u, int n) {
+      const int us = u % TC_TI, ms = u % TC2_TI, vs_slot = u & 1;
+      uint64_t key = KEY_NONE;
+      bool sensitive = false;
+      const int row = pt;
+      float mu32 = 0.f, sb = 0.f, kk = 0.f, vv = 0.f, mu = 0.f, s2 = 0.f, d_mu = 0.f, d_s2 = 0.f;
+      double cm0 = 0.0;
+      bool early = false;
+      if (pt < n) {
+#pragma unroll
+        for (int q = 0; q < TC_JQ; ++q) {
+          const float* mp = m_part + (us * TC_JQ + q) * 3 * TC_ROWS;
+          mu32 += mp[row];
+          sb += mp[TC_ROWS + row];
+          kk += mp[2 * TC_ROWS + row];
+          vv += vpart[(vs_slot * TC_JQ + q) * TC_ROWS + row];
+        }
+        cm0 = m_m0[ms * TC_ROWS + row];
+        TR(u, 13);
+        mu = static_cast<float>(cm0 + G.b) + mu32;
+        const float vs = vv;
+        s2 = static_cast<float>(G.sf2) - vs;
+        // FP32 k + 3xTF32 contraction: error coefficient 8x the SIMT one (DESIGN.md §5.6)
+        const float eps = 8.0f * static_cast<float>(G.eps);
+        d_mu = eps * sb + 2e-7f * (1.0f + fabsf(mu));
+        const float ew = eps * static_cast<float>(G.w_fro);
+        d_s2 = 2.5f * ew * sqrtf(vs * kk) + ew * ew * kk + eps * vs + 8.0f * U32 * G.sf2f;
+        // Early rejection (EI, bench path only): a cheap upper bound of the admission score,
+        //   ln sigma + ln h(z),  h(z) <= phi(z) / (1 + z^2) for z <= 0 (Mills ratio
+        //   Q(x) >= x phi(x) / (1 + x^2)),  h(z) <= z + phi(0) for z > 0,
+        // at the same (mu - d_mu, s2 + d_s2) as the exact screen, plus slack covering twice the
+        // screen's evaluation margin and its own MUFU rounding: its key never exceeds the exact
+        // admission key, so key >= tau rejects exactly the rows the exact screen would reject, and
+        // the (smaller) cheap key is a valid entry for the best-dropped bound.
+        const uint64_t tau = ts.tau;
+        if (A.acq == 0 && !A.d_scores && !A.d_screen && tau != KEY_NONE) {
+          const float s2p = s2 + d_s2;
+          if (s2p > 0.0f) {
+            const float z = (static_cast<float>(G.fstar) - (mu - d_mu) - static_cast<float>(A.xi)) * rsqrtf(s2p);
+            const float lnhb = z > 0.0f ? __logf(z + 0.3989422804014327f)
+                                        : -0.5f * z * z - 0.9189385332046727f - __logf(1.0f + z * z);
+            const float cheap = 0.5f * __logf(s2p) + lnhb;
+            const float cheap_ub = cheap + 2e-5f * (1.0f + fabsf(cheap) + z * z);
+            const uint64_t kc = make_key(cheap_ub, m_cvi[ms * TC_ROWS + row]);
+            if (kc >= tau) {
+              early = true;
+              if (kc < drop_r) drop_r = kc;
+            }
+          }
+        }
+      }
+      const bool warp_early = __all_sync(0xffffffffu, early || pt >= n);
+      if (pt < n && !early && !warp_early) {
+        const float fstar = static_cast<float>(G.fstar), m0f = static_cast<float>(cm0);
+        float m2;
+        float ub = acquisition32(A.acq, mu - d_mu, s2 + d_s2, m0f, fstar, static_cast<float>(A.xi),
+                                 static_cast<float>(A.kappa), m2);
+        ub += m2;
+        if (A.d_screen) {   // parity / debug output of the screen (never on the bench path)
+          float m3;
+          const float scr = acquisition32(A.acq, mu, s2, m0f, fstar, static_cast<float>(A.xi),
+                                          static_cast<float>(A.kappa), m3);
+          *reinterpret_cast<float4*>(A.d_screen + 4ull * m_j[ms * TC_ROWS + row]) = make_float4(mu, s2, scr, ub);
+        }
+        TR(u, 14);
+        if (A.d_scores) {
+          const double mud = cm0 + G.b + static_cast<double>(mu32);
+          const double s2d = G.sf2 - static_cast<double>(vv);
+          if (A.acq == 0) {
+            if (s2d > 0.0) {
+              const double sg = sqrt(s2d), z = (G.fstar - mud - A.xi) / sg;
+              if (z >= -3.2) {
+                const double Phi = 0.5 * erfc(-z * INV_SQRT2);
+                const double h = exp(-0.5 * z * z) * INV_SQRT_2PI + z * Phi;
+                const double uu = static_cast<double>(U32);
+                // R2 from the tensor cores: mu error model 4u(1 + sb) (DESIGN.md §5.9)
+                const double e_s = (1.0 - z * Phi / h) / (2.0 * s2d) * 160.0 * uu * static_cast<double>(vv) +
+                                   Phi / (sg * h) * 4.0 * uu * (1.0 + static_cast<double>(sb));
+                sensitive = e_s > 5e-6;
+              }
+            } else {
+              sensitive = true;
+            }
+          }
+          if (!sensitive)
+            A.d_scores[m_j[ms * TC_ROWS + row]] =
+                static_cast<float>(acquisition(A.acq, mud, s2d, cm0, G.fstar, A.xi, A.kappa));
+        }
+        if (!sensitive && ub > -INFINITY) key = make_key(ub, m_cvi[ms * TC_ROWS + row]);
+      }
+      {
+        unsigned fl = __ballot_sync(0xffffffffu, sensitive);
+        while (fl) {
+          const int src = __ffs(fl) - 1;
+          fl &= fl - 1;
+          const int row = (warp - FW0) * 32 + src;
+          const uint32_t cvi = m_cvi[ms * TC_ROWS + row];
+          DV dv;
+          uint32_t act;
+          uint64_t raw;
+          decode_dev(S, cvi, dv, act, raw);
+          double kalpha, vq;
+          posterior64_warp(S, G, dv, lane, scratch, kalpha, vq);
+          if (lane == src) {
+            const double cm0 = m_m0[ms * TC_ROWS + row];
+            const double sc = acquisition(A.acq, cm0 + G.b + kalpha, G.sf2 - vq, cm0, G.fstar, A.xi, A.kappa);
+            const double ub = sc + 1e-12 * fmax(1.0, fabs(sc));
+            A.d_scores[m_j[ms * TC_ROWS + row]] = static_cast<float>(sc);
+            if (ub > -INFINITY) key = make_key(__double2float_ru(ub), cvi);
+          }
+        }
+      }
+      TR(u, 6);
+      if (key != KEY_NONE) {
+        if (key < ts.tau) {
+          const int pos = atomicAdd(&ts.n_add, 1);
+          arr[ts.n_list + pos] = key;
+        } else if (key < drop_r) {
+          drop_r = key;
+        }
+      }
+      TR(u, 7);
+    };
+
+    for (int t = 0; t < my_tiles; ++t) {
+      // idle most of the tile: poll with back-off (a suspended try_wait loop re-issued ~250 times per
+      // tile on every finalize warp, issue slots taken from the producers of the same sub-partition)
+      tc::mbar_wait_backoff(f_ready + (t & 1), (t >> 1) & 1, 512);
+      const uint64_t r0 = (blockIdx.x + static_cast<uint64_t>(t) * gridDim.x) * TC_ROWS;
+      const int n = static_cast<int>(n_list - r0 < TC_ROWS ? n_list - r0 : TC_ROWS);
+      finalize(t, n);
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(f_free + (t & 1));   // tile t's slots may be reused
+      named_sync(2, TC_ROWS);                              // admissions done: uniform prune decision
+      if (ts.n_list + ts.n_add > out.P - TC_ROWS) tc2_prune(arr, ts, out.KC, pt, TC_ROWS, 2);
+      else named_sync(2, TC_ROWS);                         // decision read before the next tile's admissions
+    }
+    // ---- best dropped key, CTA list (final prune: sorted, at most KC entries)
+    if (drop_r != KEY_NONE)
+      atomicMin(reinterpret_cast<unsigned long long*>(&ts.drop), static_cast<unsigned long long>(drop_r));
+    named_sync(2, TC_ROWS);
+    tc2_prune(arr, ts, out.KC, pt, TC_ROWS, 2);
+    const int n = ts.n_list;
+    uint64_t* dst = out.lists + static_cast<size_t>(blockIdx.x) * out.KC;
+    for (int i = pt; i < n; i += TC_ROWS) dst[i] = arr[i];
+    if (pt == 0) {
+      out.counts[blockIdx.x] = n;
+      out.drop[blockIdx.x] = ts.drop;
+    }
+  }
   }
   // ---- teardown
   tc::fence_before_sync();

@@ -344,5 +344,13 @@ __host__ __device__ __forceinline__ uint32_t kmajor_off(uint32_t row, uint32_t k
   return (row >> 3) * (kcore * 128u) + (k >> 2) * 128u + (row & 7u) * 16u + (k & 3u) * 4u;
 }
 
+
+// Register rebalancing between warpgroups (all four warps of a warpgroup execute the same
+// instruction): the issue / loader / finalize warps give registers back to the producers.
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
+
 }  // namespace tc
 }  // namespace as
