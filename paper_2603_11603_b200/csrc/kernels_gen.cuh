@@ -30,7 +30,10 @@ struct CandList {
 // ENS: GP prior mean from the regression-simulator ensemble (NEXT-1) instead of ln cost_sim; a
 // template parameter so the default instantiation carries no trace of it (register allocation)
 template <bool ENS>
-__global__ void __launch_bounds__(GEN_THREADS, 3)
+#ifndef AS_GEN_OCC
+#define AS_GEN_OCC 3
+#endif
+__global__ void __launch_bounds__(GEN_THREADS, AS_GEN_OCC)
 gen_kernel(DevSpace S, BatchArgs A, uint64_t j0, uint64_t nj, CandList L, int ci_n, unsigned long long* valid_total) {
   extern __shared__ __align__(16) uint64_t gen_cidx[];
   __shared__ unsigned long long blk_valid;

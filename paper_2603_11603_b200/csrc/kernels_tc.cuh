@@ -44,6 +44,7 @@ struct TcB {
 };
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // Top-k' admission among the `nt` threads synchronised by named barrier `id`.
 __device__ __forceinline__ void group_bitonic(uint64_t* arr, int n_el, int t, int nt, int id) {

@@ -23,12 +23,14 @@
 //               tile t+1; epilogue read (|v|^2 of the last column blocks), then tile t is handed to
 //               the finalize warps through an mbarrier (f_ready) -- no CTA barrier.
 //   warp 16     L^-1 MMA issuer (warp-converged, one elected lane issues).
-//   warp 17     loader: bulk copies of the T groups and staged list records, and the zero-fill of
-//               used one-hot buffers.
+//   warp 17     T loader: bulk copies of the T groups and the zero-fill of used one-hot buffers
+//               (blocking waits in ring order).
 //   warp 18     R2 MMA issuer.        warp 19  L^-1 chunk loader.
 //   warps 20-23 finalize (one per SM sub-partition, row = 32 (warp - 20) + lane): FP32 screen +
 //               certified bound, lazy CTA top-k' of tile t while the producers run tile t+1; they
-//               release the tile's slots (partial sums, |v|^2, meta) through f_free.
+//               release the tile's slots (partial sums, |v|^2, meta) through f_free, and lane 0 of
+//               warp 20 stages the list records of tile t + 4.  The T loader waits in ring order
+//               (blocking) instead of polling with back-off.
 // TMEM: D [Mp16] | A ring [8 x 16] | R2 ring [2 groups x 64]  (Mp16 <= 256 -> <= 512 columns).
 #pragma once
 #include "kernels_gen.cuh"
@@ -44,12 +46,21 @@ constexpr int TC2_PF = TC2_NB - 2;           // chunks prefetched ahead of the M
                                              // waits for the MMAs two chunks back, not the previous one
 constexpr int TC2_NT = 2;                    // T group ring stages (refilled early by the loader warp)
 constexpr int TC2_KPMAX = 64;                // one-hot width the host aims for (features beyond go SIMT)
-constexpr int TC2_TI = 3;                    // meta slots (cvi, j, m0): read by finalize() one tile later
-constexpr int TC2_CB = 1;                    // chunks whose math is batched ahead of their A-stage waits (ILP)
+constexpr int TC2_TI = 4;                    // meta slots (cvi, j, m0): read by finalize() up to 3 tiles later
+constexpr int TC2_PS = 3;                    // partial-sum slots (flush_part -> finalize)
+constexpr int TC2_NS = 3;                    // staging slots of list records (tile u staged after hand-off u - 4)
+#ifndef AS_TC2_CB
+#define AS_TC2_CB 1
+#endif
+constexpr int TC2_CB = AS_TC2_CB;                    // chunks whose math is batched ahead of their A-stage waits (ILP)
 constexpr int TC2_XW = 8;                    // non-producer warps (MMA, loader, R2, L^-1 loader, 4 finalize)
 constexpr int TC2_THREADS = 16 * 32 + TC2_XW * 32;
-constexpr int TC2_PROD_REGS = 96;            // setmaxnreg: producers 96, the others 48 (80 at launch)
-constexpr int TC2_AUX_REGS = 48;
+#ifndef AS_TC2_PREGS
+#define AS_TC2_PREGS 96
+#define AS_TC2_AREGS 48
+#endif
+constexpr int TC2_PROD_REGS = AS_TC2_PREGS;            // setmaxnreg: producers 96, the others 48 (80 at launch)
+constexpr int TC2_AUX_REGS = AS_TC2_AREGS;
 
 // Shared-memory carve-out: the fixed-size arrays first (compile-time offsets, so the hot loop
 // addresses them with immediates), then the rings whose size depends on M and Kp.
@@ -59,7 +70,7 @@ constexpr size_t TC2_O_ALPHA = TC2_O_BARS + 64 * 8;
 constexpr size_t TC2_O_OH = TC2_O_ALPHA + 2 * MMAX * 4;
 constexpr size_t TC2_O_MXH = TC2_O_OH + 4 * MMAX * 4;
 constexpr size_t TC2_O_MPART = TC2_O_MXH + 4 * TC_TI * TC_ROWS * 4;
-constexpr size_t TC2_O_VPART = TC2_O_MPART + TC_TI * 4 * 3 * TC_ROWS * 4;   // [TI][jq][3][128]: one slot per thread
+constexpr size_t TC2_O_VPART = TC2_O_MPART + TC2_PS * 4 * 3 * TC_ROWS * 4;   // [PS][jq][3][128]: one slot per thread
 constexpr size_t TC2_O_MCVI = TC2_O_VPART + 2 * 4 * TC_ROWS * 4;   // vpart: [2 slots][jq][128]
 constexpr size_t TC2_O_MJ = TC2_O_MCVI + TC2_TI * TC_ROWS * 4;
 constexpr size_t TC2_O_MM0 = TC2_O_MJ + TC2_TI * TC_ROWS * 4;
@@ -68,7 +79,7 @@ constexpr size_t TC2_O_XH = TC2_O_MM0 + TC2_TI * TC_ROWS * 8;
 constexpr size_t TC2_STG_CVI = 0, TC2_STG_J = 512, TC2_STG_M0 = 1024, TC2_STG_DV0 = 2048, TC2_STG_DV1 = 3072,
                  TC2_STG_DV2 = 4096, TC2_STG_BYTES = 5120;
 constexpr size_t TC2_O_STG = TC2_O_XH + 4 * VMAX * 4;
-constexpr size_t TC2_O_VAR = TC2_O_STG + 2 * TC2_STG_BYTES;
+constexpr size_t TC2_O_VAR = TC2_O_STG + TC2_NS * TC2_STG_BYTES;
 // + NB L^-1 stages (2 Mp16 16 4 B) + NT T stages (2 64 Kp 2 B) + 2 E buffers (128 Kp 2 B) + P keys
 __host__ __device__ constexpr size_t tc2_smem_total(int Mp16, int Kp, int P) {
   return TC2_O_VAR + static_cast<size_t>(TC2_NB) * 2 * Mp16 * 16 * 2 + static_cast<size_t>(TC2_NT) * 2 * 64 * Kp * 2 +
@@ -145,7 +156,11 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       trace[(static_cast<size_t>(u) * TC2_TR_EV + ev) * TC2_TR_W + warp] = clock64();
   };
   const int ng = (nch + TC2_RG - 1) / TC2_RG;                         // R2 groups per tile
-  const uint32_t A0col = static_cast<uint32_t>(Mp16);                 // TMEM column of A stage 0
+  // accumulators: one D (M > 128: 256 columns, the next tile's MMAs wait for the epilogue read) or two
+  // (Mp16 <= 128: tile t's accumulator is read while the MMAs of tile t + 1 run -- "lag" mode)
+  const int ND = NCH > 0 ? (NCH * TC_KCH <= 128 ? 2 : 1) : (Mp16 <= 128 ? 2 : 1);
+  auto dcol = [&](int u) -> uint32_t { return static_cast<uint32_t>((ND == 2 ? (u & 1) : 0) * Mp16); };
+  const uint32_t A0col = static_cast<uint32_t>(ND * Mp16);            // TMEM column of A stage 0
   const uint32_t R0col = A0col + 16u * TC2_NA;                        // TMEM column of R2 stage 0
   const uint32_t b_stage_bytes = 2u * Mp16 * TC_KCH * 2;              // L^-1 FP16 hi + lo at the widest chunk
   const uint32_t t_stage_bytes = 2u * (TC2_RG * TC_KCH) * Kp * 2;     // T: 2 FP16 pieces x 64 points
@@ -175,18 +190,21 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
   uint64_t* a_empty = a_full + TC2_NA;          // [NA] commit
   uint64_t* b_full = a_empty + TC2_NA;          // [NB] 1 + tx
   uint64_t* b_empty = b_full + TC2_NB;         // [NB] commit
-  uint64_t* d_full = b_empty + TC2_NB;         // [1]  commit
-  uint64_t* d_empty = d_full + 1;              // [1]  count PW
-  uint64_t* t_ready = d_empty + 1;             // [TI] count 1 (tile meta + E rows published)
+  uint64_t* d_full = b_empty + TC2_NB;         // [ND] commit
+  uint64_t* d_empty = d_full + 2;              // [ND] count PW
+  uint64_t* t_ready = d_empty + 2;             // [TI] count 1 (tile meta + E rows published)
   uint64_t* r_full = t_ready + TC_TI;          // [RS] commit
   uint64_t* r_empty = r_full + TC2_RS;         // [RS] count PW
   uint64_t* x_full = r_empty + TC2_RS;         // [NT] 1 + tx  (T group loaded)
   uint64_t* x_empty = x_full + TC2_NT;         // [NT] commit
-  uint64_t* s_full = x_empty + TC2_NT;         // [2]  1 + tx  (tile records staged)
-  uint64_t* s_empty = s_full + 2;              // [2]  count PW
-  uint64_t* ez_full = s_empty + 2;             // [2]  1 + tx  (E buffer zeroed again by a bulk copy)
-  uint64_t* f_ready = ez_full + 2;             // [2]  count PW  (tile partial sums + |v|^2 written)
-  uint64_t* f_free = f_ready + 2;              // [2]  count 4   (finalize done with the tile's slots)
+  uint64_t* s_full = x_empty + TC2_NT;         // [NS] 1 + tx  (tile records staged)
+  uint64_t* s_empty = s_full + TC2_NS;         // [NS] count PW
+  uint64_t* ez_full = s_empty + TC2_NS;        // [2]  1 + tx  (E buffer zeroed again by a bulk copy)
+  uint64_t* f_free = ez_full + 2;              // [2]  count 4   (finalize done with the tile's slots)
+  // hand-off of tile t to the finalize warps.  (A pair of named barriers -- producers bar.arrive,
+  // finalize bar.sync -- deadlocked the NEXT launch in lag mode: stray barrier state outlived the
+  // CTA.  mbarriers carry no state across launches.)
+  uint64_t* f_ready = f_free + 2;              // [2]  count PW  (tile partial sums + |v|^2 written)
 
   // ---- setup
   // point-pair layout: [al_2p, al_2p+1, |al_2p|, |al_2p+1|] so one LDS.128 feeds packed f32x2 math
@@ -220,8 +238,10 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       tc::mbar_init(b_full + s, 1);
       tc::mbar_init(b_empty + s, 1);
     }
-    tc::mbar_init(d_full, 1);
-    tc::mbar_init(d_empty, TC_PROD_WARPS);
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(d_full + s, 1);
+      tc::mbar_init(d_empty + s, TC_PROD_WARPS);
+    }
     for (int s = 0; s < TC_TI; ++s) tc::mbar_init(t_ready + s, 1);
     for (int s = 0; s < TC2_RS; ++s) {
       tc::mbar_init(r_full + s, 1);
@@ -232,11 +252,13 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       tc::mbar_init(x_empty + s, 1);
     }
     for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(ez_full + s, 1);
+      tc::mbar_init(f_free + s, TC_EPI_WARPS);
+      tc::mbar_init(f_ready + s, TC_PROD_WARPS);
+    }
+    for (int s = 0; s < TC2_NS; ++s) {
       tc::mbar_init(s_full + s, 1);
       tc::mbar_init(s_empty + s, TC_PROD_WARPS);
-      tc::mbar_init(ez_full + s, 1);
-      tc::mbar_init(f_ready + s, TC_PROD_WARPS);
-      tc::mbar_init(f_free + s, TC_EPI_WARPS);
     }
     tc::mbar_fence_init();
     ts.n_list = 0;
@@ -270,11 +292,11 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     // ---- epilogue, part 1 (all producer warps): the last NA column blocks of D -> |v|^2 partial,
     // release D.
     auto epilogue_read = [&](int u, float vsq_run) {
-      tc::mbar_wait(d_full, u & 1);
+      tc::mbar_wait(d_full + (ND == 2 ? (u & 1) : 0), (ND == 2 ? (u >> 1) : u) & 1);
       TR(u, 4);
       tc::fence_after_sync();
       float vsq = vsq_run;
-      const uint32_t taddr = lane_base + TC_JPT * jq;
+      const uint32_t taddr = lane_base + TC_JPT * jq + dcol(u);
       const int bfirst = nch > TC2_NA ? nch - TC2_NA : 0;
       for (int b0 = bfirst; b0 < nch; b0 += 4) {
         float v[16];
@@ -291,10 +313,8 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       vpart[((u & 1) * TC_JQ + jq) * TC_ROWS + quad * 32 + lane] = vsq * T2.vsq_unscale;
       tc::fence_before_sync();
       __syncwarp();
-      if (lane == 0) {
-        tc::mbar_arrive(d_empty);
-        tc::mbar_arrive(f_ready + (u & 1));   // partial sums (flush_part) + |v|^2 of tile u -> finalize warps
-      }
+      if (lane == 0) tc::mbar_arrive(d_empty + (ND == 2 ? (u & 1) : 0));
+      if (lane == 0) tc::mbar_arrive(f_ready + (u & 1));   // partial sums + |v|^2 of tile u -> finalize
       TR(u, 5);
     };
 
@@ -306,8 +326,9 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       if (u < my_tiles) {
         const uint64_t r0 = (blockIdx.x + static_cast<uint64_t>(u) * gridDim.x) * TC_ROWS;
         n = static_cast<int>(n_list - r0 < TC_ROWS ? n_list - r0 : TC_ROWS);
-        const unsigned char* sg = stg + (u & 1) * TC2_STG_BYTES;
-        tc::mbar_wait(s_full + (u & 1), (u >> 1) & 1);
+        const int ss = u % TC2_NS;
+        const unsigned char* sg = stg + ss * TC2_STG_BYTES;
+        tc::mbar_wait(s_full + ss, (u / TC2_NS) & 1);
         if (pt < n) {
           const int ms = u % TC2_TI;
           m_cvi[ms * TC_ROWS + pt] = reinterpret_cast<const uint32_t*>(sg + TC2_STG_CVI)[pt];
@@ -337,7 +358,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         }
         tc::fence_proxy_async();   // generic-proxy stores -> visible to the tensor core (async proxy)
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(s_empty + (u & 1));   // staged records consumed
+        if (lane == 0) tc::mbar_arrive(s_empty + ss);   // staged records consumed
       }
       named_sync(1, TC_PROD_THREADS);
       if (pt == 0 && n > 0) tc::mbar_arrive(t_ready + us);   // E rows of tile u published (R2 warp)
@@ -353,7 +374,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     // stage / slot / parity folds to a constant
     auto produce = [&](int u, int cb, int ce, unsigned long long& mu2, unsigned long long& sb2,
                        unsigned long long& kk2, float& vsq_run) {
-      const uint32_t dq = lane_base + TC_JPT * jq;
+      const uint32_t dq = lane_base + TC_JPT * jq + dcol(u);
       const uint32_t gbase = static_cast<uint32_t>(u) * static_cast<uint32_t>(nch);
       const uint32_t grbase = static_cast<uint32_t>(u) * static_cast<uint32_t>(ng);
       unsigned long long xb[NH > 0 ? NH : 1];                 // (x_h, x_h): broadcast over a point pair
@@ -503,7 +524,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       const float2 m_ = f2_unpack(mu2), s_ = f2_unpack(sb2), k_ = f2_unpack(kk2);
       const float mu_p = m_.x + m_.y, sb_p = s_.x + s_.y, kk_p = k_.x + k_.y;
       // each thread owns its slot (no atomics: the four quarters of a candidate used to contend)
-      float* mp = m_part + ((u % TC_TI) * TC_JQ + jq) * 3 * TC_ROWS;
+      float* mp = m_part + ((u % TC2_PS) * TC_JQ + jq) * 3 * TC_ROWS;
       mp[cand] = mu_p * T2.k_unscale;
       mp[TC_ROWS + cand] = sb_p * T2.k_unscale;
       mp[2 * TC_ROWS + cand] = kk_p * (T2.k_unscale * T2.k_unscale);
@@ -512,18 +533,46 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     // Tile loop.  Before the epilogue of tile t (which waits for all of t's MMAs) the producers
     // already produce the first NA chunks of tile t+1 into the A ring, so the MMA drain of tile t
     // overlaps useful work and the MMAs of t+1 start as soon as the accumulator is read out.
+    unsigned long long mu_c = 0ull, sb_c = 0ull, kk_c = 0ull;  // tile t's running sums (packed pairs)
+    float vsq_c = 0.f, vsq_t = 0.f;
+    if (ND == 2) {
+      // lag mode (Mp16 <= 128, two accumulators): iteration t publishes t + 1, produces every chunk of
+      // tile t (its R2 groups were issued one iteration earlier) and reads the accumulator of tile
+      // t - 1 (its MMAs completed while tile t was produced): neither MMA round trip is exposed
+      for (int t = 0; t <= my_tiles; ++t) {
+        const bool have = t < my_tiles;
+        // slots of tile t - 3 (meta (t + 1) % 4, partial sums t % 3, |v|^2 (t - 1) & 1) released --
+        // also in the final epilogue-only iteration: its f_ready arrival reuses tile t - 3's phase
+        // slot, and arriving before the finalize warps consumed that phase aliases the parity
+        if (t >= 3) tc::mbar_wait(f_free + ((t - 3) & 1), ((t - 3) >> 1) & 1);
+        if (have) {
+          TR(t, 0);
+          publish(t + 1);
+          TR(t, 1);
+          produce(t, 0, nch, mu_c, sb_c, kk_c, vsq_c);
+          TR(t, 2);
+          flush_part(t, mu_c, sb_c, kk_c);
+          mu_c = sb_c = kk_c = 0ull;
+        }
+        if (t >= 1) {
+          TR(t - 1, 3);
+          epilogue_read(t - 1, vsq_t);          // hands tile t - 1 to the finalize warps
+        }
+        vsq_t = vsq_c;
+        vsq_c = 0.f;
+        if (!have) break;
+      }
+    } else {
     // One instruction copy of each chunk range (the chunk loop is unrolled, and the code must stay
     // small for the instruction cache): iteration t = -1 only produces the head of tile 0.
     constexpr int HEADC = NCH < TC2_NA ? NCH : TC2_NA;
     const int head = NCH > 0 ? HEADC : (nch < TC2_NA ? nch : TC2_NA);   // multiple of the R2 group size, or all of nch
-    unsigned long long mu_c = 0ull, sb_c = 0ull, kk_c = 0ull;  // tile t's running sums (packed pairs)
-    float vsq_c = 0.f, vsq_t = 0.f;
     int n_next = n_cur;                                       // rows of tile t + 1
     n_cur = 0;                                                // rows of tile t
     for (int t = -1; t < 0 || n_cur > 0; ++t) {
       if (t >= 0) {
         TR(t, 0);
-        // slots of tile t - 2 (meta (t + 1) % 3, partial sums and |v|^2 t & 1) released by the finalize warps
+        // slots of tile t - 2 (meta (t + 1) % 4, partial sums t % 3, |v|^2 t & 1) released by the finalize warps
         if (t >= 2) tc::mbar_wait(f_free + (t & 1), ((t >> 1) + 1) & 1);
         n_next = publish(t + 1);
         TR(t, 1);
@@ -541,9 +590,10 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       }
       if (t >= 0) {
         TR(t, 3);
-        epilogue_read(t, vsq_t);              // hands tile t to the finalize warps (f_ready)
+        epilogue_read(t, vsq_t);              // hands tile t to the finalize warps
       }
       n_cur = n_next;
+    }
     }
   } else {
   tc::setmaxnreg_dec<TC2_AUX_REGS>();
@@ -559,7 +609,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     long long wa_acc = 0, wb_acc = 0;
     for (int t = 0; tile_exists(t); ++t) {
       TR(t, 8);
-      tc::mbar_wait(d_empty, (t & 1) ^ 1);
+      tc::mbar_wait(d_empty + (ND == 2 ? (t & 1) : 0), ((ND == 2 ? (t >> 1) : t) & 1) ^ 1);
       TR(t, 9);
       tc::fence_after_sync();
       // one chunk: operand waits, 3 MMAs + 2 commits (rolled: unrolling it gained nothing once the
@@ -582,7 +632,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
         const uint32_t a_h = tmem + A0col + 16u * sa, a_l = a_h + 8;
         const uint64_t bh = dB + ((sbb * b_stage_bytes) >> 4);
         const uint64_t bl = bh + ((N * TC_KCH * 2) >> 4);
-        const uint32_t d = tmem + c * TC_KCH;
+        const uint32_t d = tmem + dcol(t) + c * TC_KCH;
         // 3-term FP16 split: hi.hi + hi.lo + lo.hi (one K = 16 step each), then release A and B
         tc::mma3_f16_ts_commit2_w(d, a_h, a_l, bh, bl, idesc, c > 0 ? 1u : 0u, a_empty + sa, b_empty + sbb);
         ++g;
@@ -593,7 +643,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       } else {
         for (int c = 0; c < nch; ++c) mma_chunk(c);
       }
-      tc::mma_commit_w(d_full);
+      tc::mma_commit_w(d_full + (ND == 2 ? (t & 1) : 0));
       TR(t, 10);
       if (trace != nullptr && lane == 0 && t < TC2_TR_TILES) {   // MMA warp: cycles waiting on A / B per tile
         trace[(static_cast<size_t>(t) * TC2_TR_EV + 12) * TC2_TR_W + warp] = static_cast<unsigned long long>(wa_acc);
@@ -652,51 +702,29 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     __syncwarp();
   } else if (warp == TC_PROD_WARPS + 1) {
     // =========================================================== loader (lane 0)
-    // Keeps the three bulk-copy rings full with non-blocking tests: L^-1 chunks (refill of a slot
-    // once its MMAs completed), T groups (once their R2 MMAs completed), staged list records (once
-    // published).  Exactly the CTA's totals are loaded, so nothing is left in flight at exit.
+    // T groups in ring order with blocking waits: refill a stage once its R2 MMAs completed, and
+    // zero a tile's one-hot buffer once the last R2 group of that tile completed.  Exactly the CTA's
+    // totals are loaded, so nothing is left in flight at exit.
     if (lane == 0) {
       const uint32_t tot_T = static_cast<uint32_t>(my_tiles) * ng;
-      uint32_t xl = 0;
-      int xc = 0, sl = 0;
-      while (xl < tot_T || sl < my_tiles) {
-        bool prog = false;
-        if (sl < my_tiles && tc::mbar_test(s_empty + (sl & 1), ((sl >> 1) & 1u) ^ 1u)) {
-          const uint64_t r0 = (blockIdx.x + static_cast<uint64_t>(sl) * gridDim.x) * TC_ROWS;
-          const uint32_t n = static_cast<uint32_t>(n_list - r0 < TC_ROWS ? n_list - r0 : TC_ROWS);
-          const uint32_t b4 = (n * 4 + 15) & ~15u, b8 = (n * 8 + 15) & ~15u;   // bulk sizes: multiples of 16 B
-          unsigned char* sg = stg + (sl & 1) * TC2_STG_BYTES;
-          uint64_t* bar = s_full + (sl & 1);
-          tc::mbar_arrive_expect_tx(bar, 2 * b4 + 4 * b8);
-          tc::bulk_g2s(sg + TC2_STG_CVI, L.cvi + r0, b4, bar);
-          tc::bulk_g2s(sg + TC2_STG_J, L.j + r0, b4, bar);
-          tc::bulk_g2s(sg + TC2_STG_M0, L.m0 + r0, b8, bar);
-          tc::bulk_g2s(sg + TC2_STG_DV0, L.dv0 + r0, b8, bar);
-          tc::bulk_g2s(sg + TC2_STG_DV1, L.dv1 + r0, b8, bar);
-          tc::bulk_g2s(sg + TC2_STG_DV2, L.dv2 + r0, b8, bar);
-          ++sl;
-          prog = true;
-        }
-        if (xl < tot_T && tc::mbar_test(x_empty + (xl % TC2_NT), ((xl / TC2_NT) & 1u) ^ 1u)) {
-          const int s_ = xl % TC2_NT;
-          if (xl >= TC2_NT) {
-            // R2 group xl - NT has completed; if it was the last group of its tile u, the one-hot
-            // buffer E[u & 1] is free: zero it for tile u + 2 (every u + 2 < my_tiles gets here)
-            const uint32_t xg = xl - TC2_NT;
-            const int u = static_cast<int>(xg / ng);
-            if (xg % ng == static_cast<uint32_t>(ng - 1) && u + 2 < my_tiles) {
-              tc::mbar_arrive_expect_tx(ez_full + (u & 1), e_bytes);
-              tc::bulk_g2s(E0 + (u & 1) * e_bytes, T2.ezero, e_bytes, ez_full + (u & 1));
-            }
+      int xc = 0;
+      for (uint32_t xl = 0; xl < tot_T; ++xl) {
+        const int s_ = xl % TC2_NT;
+        tc::mbar_wait(x_empty + s_, ((xl / TC2_NT) & 1u) ^ 1u);
+        if (xl >= TC2_NT) {
+          // R2 group xl - NT has completed; if it was the last group of its tile u, the one-hot
+          // buffer E[u & 1] is free: zero it for tile u + 2 (every u + 2 < my_tiles gets here)
+          const uint32_t xg = xl - TC2_NT;
+          const int u = static_cast<int>(xg / ng);
+          if (xg % ng == static_cast<uint32_t>(ng - 1) && u + 2 < my_tiles) {
+            tc::mbar_arrive_expect_tx(ez_full + (u & 1), e_bytes);
+            tc::bulk_g2s(E0 + (u & 1) * e_bytes, T2.ezero, e_bytes, ez_full + (u & 1));
           }
-          tc::mbar_arrive_expect_tx(x_full + s_, t_stage_bytes);
-          tc::bulk_g2s(T0 + static_cast<size_t>(s_) * t_stage_bytes,
-                       T2.tch + static_cast<size_t>(xc) * (t_stage_bytes / 2), t_stage_bytes, x_full + s_);
-          ++xl;
-          if (++xc == ng) xc = 0;
-          prog = true;
         }
-        if (!prog) __nanosleep(100);
+        tc::mbar_arrive_expect_tx(x_full + s_, t_stage_bytes);
+        tc::bulk_g2s(T0 + static_cast<size_t>(s_) * t_stage_bytes,
+                     T2.tch + static_cast<size_t>(xc) * (t_stage_bytes / 2), t_stage_bytes, x_full + s_);
+        if (++xc == ng) xc = 0;
       }
     }
     __syncwarp();
@@ -708,8 +736,27 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     // lose against tau lower this thread's drop_r instead of a shared atomicMin
     // per row (min is order-free; reduced once at the end, and tc2_prune lowers ts.drop as before).
     uint64_t drop_r = KEY_NONE;
+    // list records of tile sl into staging slot sl & 1 once publish(sl - 2) consumed it (lane 0 of
+    // the first finalize warp; publish(sl) waits on s_full)
+    auto stage = [&](int sl) {
+      const int ss = sl % TC2_NS;
+      tc::mbar_wait(s_empty + ss, ((sl / TC2_NS) & 1u) ^ 1u);
+      const uint64_t r0 = (blockIdx.x + static_cast<uint64_t>(sl) * gridDim.x) * TC_ROWS;
+      const uint32_t n = static_cast<uint32_t>(n_list - r0 < TC_ROWS ? n_list - r0 : TC_ROWS);
+      const uint32_t b4 = (n * 4 + 15) & ~15u, b8 = (n * 8 + 15) & ~15u;   // bulk sizes: multiples of 16 B
+      unsigned char* sg = stg + ss * TC2_STG_BYTES;
+      uint64_t* bar = s_full + ss;
+      tc::mbar_arrive_expect_tx(bar, 2 * b4 + 4 * b8);
+      tc::bulk_g2s(sg + TC2_STG_CVI, L.cvi + r0, b4, bar);
+      tc::bulk_g2s(sg + TC2_STG_J, L.j + r0, b4, bar);
+      tc::bulk_g2s(sg + TC2_STG_M0, L.m0 + r0, b8, bar);
+      tc::bulk_g2s(sg + TC2_STG_DV0, L.dv0 + r0, b8, bar);
+      tc::bulk_g2s(sg + TC2_STG_DV1, L.dv1 + r0, b8, bar);
+      tc::bulk_g2s(sg + TC2_STG_DV2, L.dv2 + r0, b8, bar);
+    };
+    const bool stager = warp == FW0 && lane == 0;
     auto finalize = [&](int u, int n) {
-      const int us = u % TC_TI, ms = u % TC2_TI, vs_slot = u & 1;
+      const int us = u % TC2_PS, ms = u % TC2_TI, vs_slot = u & 1;
       uint64_t key = KEY_NONE;
       bool sensitive = false;
       const int row = pt;
@@ -832,10 +879,13 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       TR(u, 7);
     };
 
+    if (stager)
+      for (int sl = 0; sl < 4 && sl < my_tiles; ++sl) stage(sl);   // tile 3 waits for publish(0)
+    __syncwarp();
     for (int t = 0; t < my_tiles; ++t) {
-      // idle most of the tile: poll with back-off (a suspended try_wait loop re-issued ~250 times per
-      // tile on every finalize warp, issue slots taken from the producers of the same sub-partition)
-      tc::mbar_wait_backoff(f_ready + (t & 1), (t >> 1) & 1, 512);
+      tc::mbar_wait(f_ready + (t & 1), (t >> 1) & 1);      // tile t handed over
+      if (stager && t + 4 < my_tiles) stage(t + 4);         // publish(t + 1) is done: its slot is free
+      __syncwarp();
       const uint64_t r0 = (blockIdx.x + static_cast<uint64_t>(t) * gridDim.x) * TC_ROWS;
       const int n = static_cast<int>(n_list - r0 < TC_ROWS ? n_list - r0 : TC_ROWS);
       finalize(t, n);

@@ -29,7 +29,34 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 // Blocking wait for the phase with parity `parity`.  The suspend-time hint lets the hardware park
 // the warp until the phase completes instead of re-polling (spinning warps steal issue slots from
 // the producer warps on the same SM sub-partition).
+#ifdef AS_DEBUG_HANG
+// development aid: report a wait that does not complete within ~2 s and trap
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity);
+__device__ __noinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  long long t0 = clock64() & ~1ll;
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(0x100000u)
+        : "memory");
+    if (ok) return;
+    const long long dt = clock64() - t0;
+    if (dt > 2000000000ll && !(t0 & 1)) {
+      if ((threadIdx.x & 31) == 0)
+        printf("HANG block %d warp %d bar smem 0x%x parity %u\n", blockIdx.x, threadIdx.x >> 5, smem_u32(bar), parity);
+      t0 |= 1;
+    }
+    if (dt > 8000000000ll) __trap();
+  }
+}
+__device__ __forceinline__ void mbar_wait_hw(uint64_t* bar, uint32_t parity) {
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#endif
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
