@@ -90,7 +90,7 @@ size_t tc_smem_bytes(int Mp16, int DP, int d, int P) {
 }
 
 // one-hot R2 kernel (kernels_tc2.cuh): fixed arrays + B ring + T ring + E (2) + top-k' keys
-size_t tc2_smem_bytes(int Mp16, int Kp, int /*nh*/, int P) { return tc2_smem_total(Mp16, Kp, P); }
+size_t tc2_smem_bytes(int Mp16, int Kp, int P, bool big) { return tc2_smem_total(Mp16, Kp, P, big); }
 using Tc2KernelFn = void (*)(DevSpace, DevGP, BatchArgs, CtaOut, TcB, Tc2B, CandList);
 template <int KT, int NCH>
 Tc2KernelFn tc2_kernel_kt(int nh) {
@@ -656,7 +656,7 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
   const bool gp = (a.acq != AS_ACQ_SIM) && s->G.M > 0;
   int P = next_pow2_h(s->KC + SCORE_THREADS);
   const int P_tc2 = next_pow2_h(s->KC + 4 * TC_ROWS);   // lazy admission: room for >= 3 tiles before a prune
-  const bool tc2_fits = tc2_smem_bytes(s->tb.Mp16, s->t2.Kp, s->t2.nh, P_tc2) <= static_cast<size_t>(s->smem_optin);
+  const bool tc2_fits = tc2_smem_bytes(s->tb.Mp16, s->t2.Kp, P_tc2, s->G.kernel == 0 && s->tb.nch == 16) <= static_cast<size_t>(s->smem_optin);
   // auto: the one-hot tensor-core kernel for M >= 64, and below that for large batches too (its
   // generation split beats the fused SIMT kernel there: C4, M = 48, 10^8 candidates 38.5 -> 15.3 ms;
   // small batches keep the single-launch SIMT kernel for latency)
@@ -666,7 +666,7 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
   size_t smem = 0;
   if (use_tc2) {
     P = P_tc2;
-    smem = tc2_smem_bytes(s->tb.Mp16, s->t2.Kp, s->t2.nh, P);
+    smem = tc2_smem_bytes(s->tb.Mp16, s->t2.Kp, P, s->G.kernel == 0 && s->tb.nch == 16);
   } else if (use_tc) {
     smem = tc_smem_bytes(s->tb.Mp16, s->G.DP, s->H.d, P);
   } else {
@@ -865,6 +865,9 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
       K -= s->H.feat[best].n;
     }
     t2.nh = nh == 0 ? 0 : (nh <= 2 ? 2 : 4);
+#ifdef AS_EXP_NH0
+    t2.nh = 0;   // timing experiment only: SIMT features dropped (wrong scores)
+#endif
     K = 0;
     for (int f = 0; f < DMAX; ++f) {
       t2.eoff[f] = (f < d && simt[f]) ? -1 : K;

@@ -46,9 +46,6 @@ constexpr int TC2_PF = TC2_NB - 2;           // chunks prefetched ahead of the M
                                              // waits for the MMAs two chunks back, not the previous one
 constexpr int TC2_NT = 2;                    // T group ring stages (refilled early by the loader warp)
 constexpr int TC2_KPMAX = 64;                // one-hot width the host aims for (features beyond go SIMT)
-constexpr int TC2_TI = 4;                    // meta slots (cvi, j, m0): read by finalize() up to 3 tiles later
-constexpr int TC2_PS = 3;                    // partial-sum slots (flush_part -> finalize)
-constexpr int TC2_NS = 3;                    // staging slots of list records (tile u staged after hand-off u - 4)
 #ifndef AS_TC2_CB
 #define AS_TC2_CB 1
 #endif
@@ -65,25 +62,34 @@ constexpr int TC2_AUX_REGS = AS_TC2_AREGS;
 // Shared-memory carve-out: the fixed-size arrays first (compile-time offsets, so the hot loop
 // addresses them with immediates), then the rings whose size depends on M and Kp.
 constexpr size_t tc2_r128(size_t b) { return (b + 127) & ~size_t(127); }
-constexpr size_t TC2_O_BARS = 0;
-constexpr size_t TC2_O_ALPHA = TC2_O_BARS + 64 * 8;
-constexpr size_t TC2_O_OH = TC2_O_ALPHA + 2 * MMAX * 4;
-constexpr size_t TC2_O_MXH = TC2_O_OH + 4 * MMAX * 4;
-constexpr size_t TC2_O_MPART = TC2_O_MXH + 4 * TC_TI * TC_ROWS * 4;
-constexpr size_t TC2_O_VPART = TC2_O_MPART + TC2_PS * 4 * 3 * TC_ROWS * 4;   // [PS][jq][3][128]: one slot per thread
-constexpr size_t TC2_O_MCVI = TC2_O_VPART + 2 * 4 * TC_ROWS * 4;   // vpart: [2 slots][jq][128]
-constexpr size_t TC2_O_MJ = TC2_O_MCVI + TC2_TI * TC_ROWS * 4;
-constexpr size_t TC2_O_MM0 = TC2_O_MJ + TC2_TI * TC_ROWS * 4;
-constexpr size_t TC2_O_XH = TC2_O_MM0 + TC2_TI * TC_ROWS * 8;
-// staging of one tile of list records (bulk-copied by the loader): cvi | j | m0 | dv0 | dv1 | dv2
+// Slot counts: the M = 256 instance (BIG, one accumulator) needs 3 meta / 2 partial-sum / 2 staging
+// slots with records staged 3 tiles ahead; lag mode (two accumulators, the epilogue one tile later)
+// needs one more of each and stages 4 ahead.  The M = 256 layout is the one shared memory is tight for.
 constexpr size_t TC2_STG_CVI = 0, TC2_STG_J = 512, TC2_STG_M0 = 1024, TC2_STG_DV0 = 2048, TC2_STG_DV1 = 3072,
                  TC2_STG_DV2 = 4096, TC2_STG_BYTES = 5120;
-constexpr size_t TC2_O_STG = TC2_O_XH + 4 * VMAX * 4;
-constexpr size_t TC2_O_VAR = TC2_O_STG + TC2_NS * TC2_STG_BYTES;
+template <bool BIG>
+struct Tc2L {
+  static constexpr int TI = BIG ? 3 : 4;       // meta slots (cvi, j, m0): publish -> finalize
+  static constexpr int PS = BIG ? 2 : 3;       // partial-sum slots (flush_part -> finalize)
+  static constexpr int NS = BIG ? 2 : 3;       // staging slots of list records
+  static constexpr int AHEAD = BIG ? 3 : 4;    // records of tile t + AHEAD staged after hand-off t
+  static constexpr size_t BARS = 0;
+  static constexpr size_t ALPHA = BARS + 64 * 8;
+  static constexpr size_t OH = ALPHA + 2 * MMAX * 4;
+  static constexpr size_t MXH = OH + 4 * MMAX * 4;
+  static constexpr size_t MPART = MXH + 4 * TC_TI * TC_ROWS * 4;
+  static constexpr size_t VPART = MPART + PS * 4 * 3 * TC_ROWS * 4;   // [PS][jq][3][128]: one slot per thread
+  static constexpr size_t MCVI = VPART + 2 * 4 * TC_ROWS * 4;         // vpart: [2 slots][jq][128]
+  static constexpr size_t MJ = MCVI + TI * TC_ROWS * 4;
+  static constexpr size_t MM0 = MJ + TI * TC_ROWS * 4;
+  static constexpr size_t XH = MM0 + TI * TC_ROWS * 8;
+  static constexpr size_t STG = XH + 4 * VMAX * 4;                    // staged records: cvi | j | m0 | dv0-2
+  static constexpr size_t VAR = tc2_r128(STG + NS * TC2_STG_BYTES);
+};
 // + NB L^-1 stages (2 Mp16 16 4 B) + NT T stages (2 64 Kp 2 B) + 2 E buffers (128 Kp 2 B) + P keys
-__host__ __device__ constexpr size_t tc2_smem_total(int Mp16, int Kp, int P) {
-  return TC2_O_VAR + static_cast<size_t>(TC2_NB) * 2 * Mp16 * 16 * 2 + static_cast<size_t>(TC2_NT) * 2 * 64 * Kp * 2 +
-         2ull * 128 * Kp * 2 + static_cast<size_t>(P) * 8;
+__host__ __device__ constexpr size_t tc2_smem_total(int Mp16, int Kp, int P, bool big) {
+  return (big ? Tc2L<true>::VAR : Tc2L<false>::VAR) + static_cast<size_t>(TC2_NB) * 2 * Mp16 * 16 * 2 +
+         static_cast<size_t>(TC2_NT) * 2 * 64 * Kp * 2 + 2ull * 128 * Kp * 2 + static_cast<size_t>(P) * 8;
 }
 
 // Phase timeline of CTA 0 (development aid, off unless the host sets AS_TC2_TRACE): clock64 per
@@ -140,6 +146,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
   constexpr int TC_PROD_THREADS = PW * 32;
   constexpr int TC_THREADS = TC_PROD_THREADS + TC2_XW * 32;  // + MMA, loader, R2, L^-1 loader, 4 finalize warps
   constexpr int FW0 = PW + 4;                                // first finalize warp
+  using LY = Tc2L<NCH == 16>;
   constexpr int TC_JQ = TC_PROD_THREADS / TC_ROWS;   // producer threads per candidate
   constexpr int TC_JPT = TC_KCH / TC_JQ;             // observed points per thread per chunk
   static_assert(TC_JQ == 4 && TC_JPT == 4, "R2 group columns are laid out for 16 producer warps");
@@ -166,22 +173,22 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
   const uint32_t t_stage_bytes = 2u * (TC2_RG * TC_KCH) * Kp * 2;     // T: 2 FP16 pieces x 64 points
   const uint32_t e_bytes = static_cast<uint32_t>(TC_ROWS) * Kp * 2;   // E: 128 rows x Kp FP16
   unsigned char* const sm0 = smem_raw;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm0 + TC2_O_BARS);
-  float* alpha_s = reinterpret_cast<float*>(sm0 + TC2_O_ALPHA);   // (alpha_j, |alpha_j|) pairs
-  float* oh_s = reinterpret_cast<float*>(sm0 + TC2_O_OH);         // [Mp16][NH]
-  float* m_xh = reinterpret_cast<float*>(sm0 + TC2_O_MXH);        // [TI][128][NH]
-  float* m_part = reinterpret_cast<float*>(sm0 + TC2_O_MPART);
-  float* vpart = reinterpret_cast<float*>(sm0 + TC2_O_VPART);
-  uint32_t* m_cvi = reinterpret_cast<uint32_t*>(sm0 + TC2_O_MCVI);
-  uint32_t* m_j = reinterpret_cast<uint32_t*>(sm0 + TC2_O_MJ);
-  double* m_m0 = reinterpret_cast<double*>(sm0 + TC2_O_MM0);
-  float* xh_s = reinterpret_cast<float*>(sm0 + TC2_O_XH);         // [NH][VMAX]
-  unsigned char* stg = sm0 + TC2_O_STG;                           // [2][TC2_STG_BYTES]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm0 + LY::BARS);
+  float* alpha_s = reinterpret_cast<float*>(sm0 + LY::ALPHA);   // (alpha_j, |alpha_j|) pairs
+  float* oh_s = reinterpret_cast<float*>(sm0 + LY::OH);         // [Mp16][NH]
+  float* m_xh = reinterpret_cast<float*>(sm0 + LY::MXH);        // [TI][128][NH]
+  float* m_part = reinterpret_cast<float*>(sm0 + LY::MPART);
+  float* vpart = reinterpret_cast<float*>(sm0 + LY::VPART);
+  uint32_t* m_cvi = reinterpret_cast<uint32_t*>(sm0 + LY::MCVI);
+  uint32_t* m_j = reinterpret_cast<uint32_t*>(sm0 + LY::MJ);
+  double* m_m0 = reinterpret_cast<double*>(sm0 + LY::MM0);
+  float* xh_s = reinterpret_cast<float*>(sm0 + LY::XH);         // [NH][VMAX]
+  unsigned char* stg = sm0 + LY::STG;                           // [2][TC2_STG_BYTES]
   // this CTA's tiles of the candidate list: blockIdx.x, blockIdx.x + gridDim.x, ...
   const uint64_t n_list = *L.count;
   const uint64_t n_tiles = (n_list + TC_ROWS - 1) / TC_ROWS;
   const int my_tiles = blockIdx.x < n_tiles ? static_cast<int>((n_tiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
-  unsigned char* B0 = sm0 + TC2_O_VAR;
+  unsigned char* B0 = sm0 + LY::VAR;
   unsigned char* T0 = B0 + static_cast<size_t>(TC2_NB) * b_stage_bytes;
   unsigned char* E0 = T0 + static_cast<size_t>(TC2_NT) * t_stage_bytes;
   uint64_t* arr = reinterpret_cast<uint64_t*>(E0 + 2ull * e_bytes);
@@ -198,8 +205,8 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
   uint64_t* x_full = r_empty + TC2_RS;         // [NT] 1 + tx  (T group loaded)
   uint64_t* x_empty = x_full + TC2_NT;         // [NT] commit
   uint64_t* s_full = x_empty + TC2_NT;         // [NS] 1 + tx  (tile records staged)
-  uint64_t* s_empty = s_full + TC2_NS;         // [NS] count PW
-  uint64_t* ez_full = s_empty + TC2_NS;        // [2]  1 + tx  (E buffer zeroed again by a bulk copy)
+  uint64_t* s_empty = s_full + LY::NS;         // [NS] count PW
+  uint64_t* ez_full = s_empty + LY::NS;        // [2]  1 + tx  (E buffer zeroed again by a bulk copy)
   uint64_t* f_free = ez_full + 2;              // [2]  count 4   (finalize done with the tile's slots)
   // hand-off of tile t to the finalize warps.  (A pair of named barriers -- producers bar.arrive,
   // finalize bar.sync -- deadlocked the NEXT launch in lag mode: stray barrier state outlived the
@@ -223,7 +230,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
   {
     // both one-hot buffers start zeroed; afterwards the loader re-zeroes a buffer with a bulk copy
     // as soon as the last R2 MMAs of its tile have completed (no zeroing pass, no barrier in publish)
-    unsigned char* E0z = sm0 + TC2_O_VAR + static_cast<size_t>(TC2_NB) * 2u * TB.Mp16 * TC_KCH * 2 +
+    unsigned char* E0z = sm0 + LY::VAR + static_cast<size_t>(TC2_NB) * 2u * TB.Mp16 * TC_KCH * 2 +
                          static_cast<size_t>(TC2_NT) * 2u * (TC2_RG * TC_KCH) * T2.Kp * 2;
     for (uint32_t i = tid; i < 2u * TC_ROWS * T2.Kp * 2 / 16; i += TC_THREADS)
       *reinterpret_cast<uint4*>(E0z + 16 * i) = make_uint4(0u, 0u, 0u, 0u);
@@ -256,7 +263,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       tc::mbar_init(f_free + s, TC_EPI_WARPS);
       tc::mbar_init(f_ready + s, TC_PROD_WARPS);
     }
-    for (int s = 0; s < TC2_NS; ++s) {
+    for (int s = 0; s < LY::NS; ++s) {
       tc::mbar_init(s_full + s, 1);
       tc::mbar_init(s_empty + s, TC_PROD_WARPS);
     }
@@ -326,11 +333,11 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       if (u < my_tiles) {
         const uint64_t r0 = (blockIdx.x + static_cast<uint64_t>(u) * gridDim.x) * TC_ROWS;
         n = static_cast<int>(n_list - r0 < TC_ROWS ? n_list - r0 : TC_ROWS);
-        const int ss = u % TC2_NS;
+        const int ss = u % LY::NS;
         const unsigned char* sg = stg + ss * TC2_STG_BYTES;
-        tc::mbar_wait(s_full + ss, (u / TC2_NS) & 1);
+        tc::mbar_wait(s_full + ss, (u / LY::NS) & 1);
         if (pt < n) {
-          const int ms = u % TC2_TI;
+          const int ms = u % LY::TI;
           m_cvi[ms * TC_ROWS + pt] = reinterpret_cast<const uint32_t*>(sg + TC2_STG_CVI)[pt];
           m_j[ms * TC_ROWS + pt] = reinterpret_cast<const uint32_t*>(sg + TC2_STG_J)[pt];
           m_m0[ms * TC_ROWS + pt] = reinterpret_cast<const double*>(sg + TC2_STG_M0)[pt];
@@ -524,7 +531,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
       const float2 m_ = f2_unpack(mu2), s_ = f2_unpack(sb2), k_ = f2_unpack(kk2);
       const float mu_p = m_.x + m_.y, sb_p = s_.x + s_.y, kk_p = k_.x + k_.y;
       // each thread owns its slot (no atomics: the four quarters of a candidate used to contend)
-      float* mp = m_part + ((u % TC2_PS) * TC_JQ + jq) * 3 * TC_ROWS;
+      float* mp = m_part + ((u % LY::PS) * TC_JQ + jq) * 3 * TC_ROWS;
       mp[cand] = mu_p * T2.k_unscale;
       mp[TC_ROWS + cand] = sb_p * T2.k_unscale;
       mp[2 * TC_ROWS + cand] = kk_p * (T2.k_unscale * T2.k_unscale);
@@ -739,8 +746,8 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     // list records of tile sl into staging slot sl & 1 once publish(sl - 2) consumed it (lane 0 of
     // the first finalize warp; publish(sl) waits on s_full)
     auto stage = [&](int sl) {
-      const int ss = sl % TC2_NS;
-      tc::mbar_wait(s_empty + ss, ((sl / TC2_NS) & 1u) ^ 1u);
+      const int ss = sl % LY::NS;
+      tc::mbar_wait(s_empty + ss, ((sl / LY::NS) & 1u) ^ 1u);
       const uint64_t r0 = (blockIdx.x + static_cast<uint64_t>(sl) * gridDim.x) * TC_ROWS;
       const uint32_t n = static_cast<uint32_t>(n_list - r0 < TC_ROWS ? n_list - r0 : TC_ROWS);
       const uint32_t b4 = (n * 4 + 15) & ~15u, b8 = (n * 8 + 15) & ~15u;   // bulk sizes: multiples of 16 B
@@ -756,7 +763,7 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     };
     const bool stager = warp == FW0 && lane == 0;
     auto finalize = [&](int u, int n) {
-      const int us = u % TC2_PS, ms = u % TC2_TI, vs_slot = u & 1;
+      const int us = u % LY::PS, ms = u % LY::TI, vs_slot = u & 1;
       uint64_t key = KEY_NONE;
       bool sensitive = false;
       const int row = pt;
@@ -880,11 +887,11 @@ score_tc2_kernel(DevSpace S, DevGP G, BatchArgs A, CtaOut out, TcB TB, Tc2B T2, 
     };
 
     if (stager)
-      for (int sl = 0; sl < 4 && sl < my_tiles; ++sl) stage(sl);   // tile 3 waits for publish(0)
+      for (int sl = 0; sl < LY::AHEAD && sl < my_tiles; ++sl) stage(sl);   // the last waits for publish(0)
     __syncwarp();
     for (int t = 0; t < my_tiles; ++t) {
       tc::mbar_wait(f_ready + (t & 1), (t >> 1) & 1);      // tile t handed over
-      if (stager && t + 4 < my_tiles) stage(t + 4);         // publish(t + 1) is done: its slot is free
+      if (stager && t + LY::AHEAD < my_tiles) stage(t + LY::AHEAD);   // publish(t + 1) done: slot free
       __syncwarp();
       const uint64_t r0 = (blockIdx.x + static_cast<uint64_t>(t) * gridDim.x) * TC_ROWS;
       const int n = static_cast<int>(n_list - r0 < TC_ROWS ? n_list - r0 : TC_ROWS);
