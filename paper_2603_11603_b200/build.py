@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES_CU = ["engine.cu"]
 SOURCES_CPP = ["space.cpp"]
-HEADERS = ["common.cuh", "kernels.cuh", "kernels_gen.cuh", "kernels_lml.cuh", "kernels_pool.cuh", "kernels_tc.cuh", "kernels_tc2.cuh", "tc_ptx.cuh", "space.hpp", "json.hpp", "../../include/autoscout.h"]
+HEADERS = ["common.cuh", "kernels.cuh", "kernels_gen.cuh", "kernels_lml.cuh", "kernels_pool.cuh", "kernels_tc.cuh", "kernels_tc2.cuh", "tc_ptx.cuh", "host_pool.hpp", "space.hpp", "json.hpp", "../../include/autoscout.h"]
 
 
 def _run(cmd, verbose):

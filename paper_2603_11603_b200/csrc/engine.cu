@@ -15,6 +15,7 @@
 #include "kernels.cuh"
 #include "kernels_tc.cuh"
 #include "kernels_tc2.cuh"
+#include "host_pool.hpp"
 #include "kernels_lml.cuh"
 #include "kernels_pool.cuh"
 #include "space.hpp"
@@ -276,11 +277,19 @@ as_status upload_gp(as_space* s, cudaStream_t st) {
     while (cols < need) cols <<= 1;
     s->tb.tmem_cols = cols;
   }
-  for (int c = 0; c < nch; ++c) {
+  // chunk offsets first, then the chunks in parallel on the host pool (each writes its own range)
+  HostPool& pool = HostPool::get();
+  {
+    size_t tot = 0;
+    for (int c = 0; c < nch; ++c) {
+      s->tb.off[c] = static_cast<uint32_t>(tot);
+      tot += 2ull * (Mp16 - c * TC_KCH) * TC_KCH;
+    }
+    s->h_Bch.assign(tot, 0.f);
+  }
+  pool.run(nch, [&](int c) {
     const int N = Mp16 - c * TC_KCH;
-    s->tb.off[c] = static_cast<uint32_t>(s->h_Bch.size());
-    const size_t base = s->h_Bch.size();
-    s->h_Bch.resize(base + 2ull * N * TC_KCH, 0.f);
+    const size_t base = s->tb.off[c];
     for (int n = 0; n < N; ++n)
       for (int k = 0; k < TC_KCH; ++k) {
         const int i = c * TC_KCH + n, j = c * TC_KCH + k;
@@ -291,7 +300,7 @@ as_status upload_gp(as_space* s, cudaStream_t st) {
         s->h_Bch[base + off] = hi;
         s->h_Bch[base + static_cast<size_t>(N) * TC_KCH + off] = lo;
       }
-  }
+  });
   // T operand of the one-hot R2 contraction (kernels_tc2.cuh): group g = observed points
   // [64g, 64g+64) x one-hot columns (f, v); T = 2^s (xt_f[v] - o_jf)^2 in FP64, split hi + lo FP16.
   // SIMT features: 2^(s/2) xt and 2^(s/2) o in FP32.
@@ -327,11 +336,12 @@ as_status upload_gp(as_space* s, cudaStream_t st) {
       std::memcpy(&h, &u, 2);
       return static_cast<double>(__half2float(h));
     };
-    for (int gi = 0; gi < ngr; ++gi) {
+    pool.run(ngr * GR, [&](int task) {     // one observed point per task
+      const int gi = task / GR, n = task % GR;
       uint16_t* base = s->h_Tch.data() + static_cast<size_t>(gi) * 2 * GR * Kp;
-      for (int n = 0; n < GR; ++n) {
+      {
         const int j = gi * GR + n;
-        if (j >= M) continue;
+        if (j >= M) return;
         for (int f = 0; f < d; ++f) {
           if (t2.eoff[f] < 0) continue;
           for (int v = 0; v < H.feat[f].n; ++v) {
@@ -347,7 +357,7 @@ as_status upload_gp(as_space* s, cudaStream_t st) {
           }
         }
       }
-    }
+    });
     // L^-1^T chunks for the FP16 contraction: chunk c = rows i in [16c, Mp16) x columns j in
     // [16c, 16c+16), 2^ew L^-1[i][j] split hi + lo FP16 (kmajor_off16); k is scaled by 2^ek in-kernel
     {
@@ -364,12 +374,17 @@ as_status upload_gp(as_space* s, cudaStream_t st) {
       t2.ek = ek;
       t2.k_unscale = static_cast<float>(std::ldexp(1.0, -ek));
       t2.vsq_unscale = static_cast<float>(std::ldexp(1.0, -2 * (ek + ew)));
-      s->h_Wch.clear();
-      for (int c = 0; c < nch; ++c) {
+      {
+        size_t tot = 0;
+        for (int c = 0; c < nch; ++c) {
+          t2.woff[c] = static_cast<uint32_t>(tot);
+          tot += 2ull * (Mp16 - c * TC_KCH) * TC_KCH;
+        }
+        s->h_Wch.assign(tot, 0);
+      }
+      pool.run(nch, [&](int c) {
         const int N = Mp16 - c * TC_KCH;
-        t2.woff[c] = static_cast<uint32_t>(s->h_Wch.size());
-        const size_t base = s->h_Wch.size();
-        s->h_Wch.resize(base + 2ull * N * TC_KCH, 0);
+        const size_t base = t2.woff[c];
         for (int n = 0; n < N; ++n)
           for (int k = 0; k < TC_KCH; ++k) {
             const int i = c * TC_KCH + n, j = c * TC_KCH + k;
@@ -380,7 +395,7 @@ as_status upload_gp(as_space* s, cudaStream_t st) {
             s->h_Wch[base + o] = hi;
             s->h_Wch[base + static_cast<size_t>(N) * TC_KCH + o] = h16(w - v16(hi));
           }
-      }
+      });
     }
     const double hs = std::ldexp(1.0, sc / 2);
     s->h_xh.assign(static_cast<size_t>(4) * VMAX, 0.f);

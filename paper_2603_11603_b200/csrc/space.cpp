@@ -2,6 +2,7 @@
 // Compiled with -ffp-contract=off so the host FP64 resource check is bit-identical to the
 // oracle's numpy evaluation and to the device's __dmul_rn/__dadd_rn path (R7).
 #include "space.hpp"
+#include "host_pool.hpp"
 
 #include <algorithm>
 #include <cmath>
@@ -924,9 +925,12 @@ Status gp_fit(const HostSpace& S, const std::vector<DV>& obs_dv, const std::vect
     fit.fstar = std::fmin(fit.fstar, y[i]);
   }
   fit.r = r;
-  // K = k(o_i, o_j) + sn2 I ; Cholesky K = L L^T
+  // K = k(o_i, o_j) + sn2 I ; Cholesky K = L L^T.  Host threads (host_pool.hpp): every element is
+  // computed by one task with the operations and order of the sequential loops, so the fit does not
+  // depend on the thread count.
+  HostPool& pool = HostPool::get();
   std::vector<double> L(static_cast<size_t>(M) * M, 0.0);
-  for (int i = 0; i < M; ++i)
+  pool.run(M, [&](int i) {
     for (int j = 0; j <= i; ++j) {
       double r2 = 0.0;
       for (int q = 0; q < d; ++q) {
@@ -935,27 +939,60 @@ Status gp_fit(const HostSpace& S, const std::vector<DV>& obs_dv, const std::vect
       }
       L[i * M + j] = kernel64(S.kernel, S.sf2, r2) + (i == j ? S.sn2 : 0.0);
     }
-  // Right-looking Cholesky: after column q is final, A[i][j] -= L[i][q] L[j][q] for q < j <= i.
-  // Each element still receives its updates in ascending q (the textbook left-looking order), so
-  // the result is identical; the update of row i runs unit-stride over j through Lt = L^T.
+  });
+  // Right-looking Cholesky in column blocks of CB: factor the diagonal block, then the panel below
+  // it (rows in parallel), then the trailing update A[i][j] -= L[i][q] L[j][q] for the block's q
+  // (rows in parallel).  Each element still receives its updates in ascending q (the textbook
+  // left-looking order), so the factor is identical to the unblocked loop; rows run unit-stride over
+  // j through Lt = L^T.
   std::vector<double> Lt(static_cast<size_t>(M) * M, 0.0);
-  for (int q = 0; q < M; ++q) {
-    const double s = L[q * M + q];
-    if (!(s > 0.0)) return err(E_NUM, "Cholesky of the GP covariance failed (not positive definite)");
-    const double lqq = std::sqrt(s);
-    L[q * M + q] = lqq;
-    Lt[static_cast<size_t>(q) * M + q] = lqq;
-    for (int i = q + 1; i < M; ++i) {
-      L[i * M + q] /= lqq;
-      Lt[static_cast<size_t>(q) * M + i] = L[i * M + q];
+  constexpr int CB = 32;
+  bool pd = true;
+  for (int k0 = 0; k0 < M && pd; k0 += CB) {
+    const int k1 = std::min(M, k0 + CB);
+    for (int q = k0; q < k1; ++q) {          // diagonal block, sequential
+      const double sq = L[q * M + q];
+      if (!(sq > 0.0)) {
+        pd = false;
+        break;
+      }
+      const double lqq = std::sqrt(sq);
+      L[q * M + q] = lqq;
+      Lt[static_cast<size_t>(q) * M + q] = lqq;
+      for (int i = q + 1; i < k1; ++i) {
+        L[i * M + q] /= lqq;
+        Lt[static_cast<size_t>(q) * M + i] = L[i * M + q];
+      }
+      const double* lq = Lt.data() + static_cast<size_t>(q) * M;
+      for (int i = q + 1; i < k1; ++i) {
+        const double liq = L[i * M + q];
+        double* ai = L.data() + static_cast<size_t>(i) * M;
+        for (int j = q + 1; j <= i; ++j) ai[j] -= liq * lq[j];
+      }
     }
-    const double* lq = Lt.data() + static_cast<size_t>(q) * M;
-    for (int i = q + 1; i < M; ++i) {
-      const double liq = L[i * M + q];
+    if (!pd || k1 == M) break;
+    pool.run(M - k1, [&](int t) {           // panel rows i >= k1: columns [k0, k1)
+      const int i = k1 + t;
       double* ai = L.data() + static_cast<size_t>(i) * M;
-      for (int j = q + 1; j <= i; ++j) ai[j] -= liq * lq[j];
-    }
+      for (int q = k0; q < k1; ++q) {
+        ai[q] /= L[q * M + q];
+        Lt[static_cast<size_t>(q) * M + i] = ai[q];
+        const double liq = ai[q];
+        const double* lq = Lt.data() + static_cast<size_t>(q) * M;
+        for (int j = q + 1; j < k1; ++j) ai[j] -= liq * lq[j];
+      }
+    });
+    pool.run(M - k1, [&](int t) {           // trailing update of row i: columns [k1, i]
+      const int i = M - 1 - t;                // longest rows first
+      double* ai = L.data() + static_cast<size_t>(i) * M;
+      for (int q = k0; q < k1; ++q) {
+        const double liq = ai[q];
+        const double* lq = Lt.data() + static_cast<size_t>(q) * M;
+        for (int j = k1; j <= i; ++j) ai[j] -= liq * lq[j];
+      }
+    });
   }
+  if (!pd) return err(E_NUM, "Cholesky of the GP covariance failed (not positive definite)");
   // alpha = L^-T L^-1 r
   std::vector<double> z(M);
   for (int i = 0; i < M; ++i) {
@@ -973,18 +1010,39 @@ Status gp_fit(const HostSpace& S, const std::vector<DV>& obs_dv, const std::vect
   // The sum is accumulated for all c of the row at once (axpy over the contiguous row W[q][0..q],
   // q ascending): the same operations in the same order per element as the column-by-column
   // form, but unit-stride and vectorisable.
+  // Column ranges [c0, c1) in parallel, cut so that each holds about the same work ((M - c)^2 / 2
+  // multiply-adds per column); inside a range the row-by-row axpy form, unit-stride in c.
   fit.Wl.assign(static_cast<size_t>(M) * M, 0.0);
-  std::vector<double> t(M);
-  for (int i = 0; i < M; ++i) {
-    for (int c = 0; c <= i; ++c) t[c] = (c == i) ? 1.0 : 0.0;
-    for (int q = 0; q < i; ++q) {
-      const double liq = L[i * M + q];
-      const double* wq = fit.Wl.data() + static_cast<size_t>(q) * M;
-      for (int c = 0; c <= q; ++c) t[c] -= liq * wq[c];
+  const int nr = std::min(M, 4 * pool.threads());
+  std::vector<int> cut(nr + 1, M);
+  {
+    const double tot = static_cast<double>(M) * M * M / 6.0;
+    double acc = 0.0;
+    int r = 0;
+    cut[0] = 0;
+    for (int c = 0; c < M && r + 1 < nr; ++c) {
+      acc += 0.5 * static_cast<double>(M - c) * (M - c);
+      if (acc >= tot * (r + 1) / nr) cut[++r] = c + 1;
     }
-    const double lii = L[i * M + i];
-    for (int c = 0; c <= i; ++c) fit.Wl[static_cast<size_t>(i) * M + c] = t[c] / lii;
+    for (int q = r + 1; q <= nr; ++q) cut[q] = M;
   }
+  pool.run(nr, [&](int rg) {
+    const int c0 = cut[rg], c1 = cut[rg + 1];
+    if (c0 >= c1) return;
+    std::vector<double> t(static_cast<size_t>(c1 - c0));
+    for (int i = c0; i < M; ++i) {
+      const int ce = std::min(c1, i + 1);
+      for (int c = c0; c < ce; ++c) t[c - c0] = (c == i) ? 1.0 : 0.0;
+      for (int q = c0; q < i; ++q) {
+        const double liq = L[i * M + q];
+        const double* wq = fit.Wl.data() + static_cast<size_t>(q) * M;
+        const int cq = std::min(c1, q + 1);
+        for (int c = c0; c < cq; ++c) t[c - c0] -= liq * wq[c];
+      }
+      const double lii = L[i * M + i];
+      for (int c = c0; c < ce; ++c) fit.Wl[static_cast<size_t>(i) * M + c] = t[c - c0] / lii;
+    }
+  });
   double fro = 0.0;
   for (double w : fit.Wl) fro += w * w;
   fit.w_fro = std::sqrt(fro);

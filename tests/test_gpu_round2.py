@@ -241,3 +241,24 @@ def test_two_process_exchange_one_gpu(tmp_path):
     ref, _ = OP.topk(o, fit, "range", 0, o.n_cvi(), 16, acq="ei")
     assert [int(r) for r in res[:-1, 0]] == [r for r, _ in ref]
     assert np.allclose(res[:-1, 1], [s for _, s in ref], rtol=1e-12, atol=1e-12)
+
+
+# ---------------------------------------------------------------- repeated launches (lag mode)
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("name,M,mode,count", [("C5", 128, "range", None), ("C4", 48, "sample", 3_000_000),
+                                               ("C4", 256, "sample", 3_000_000)])
+def test_repeated_launches_same_result(name, M, mode, count):
+    """Five back-to-back scoring passes of the one-hot kernel (lag mode for Mp16 <= 128: two
+    accumulators, hand-off of tile t - 1 to the finalize warps): identical certified top-32 every
+    time.  Regression for a hand-off that left barrier state behind and deadlocked the NEXT launch."""
+    o, fit, sp = setup(name, M)
+    count = o.n_cvi() if count is None else count
+    first = None
+    for _ in range(5):
+        sp.score_batch(mode=mode, begin=0, count=count, seed=3, acq="ei", k=32)
+        top = sp.topk(32)
+        torch.cuda.synchronize()
+        if first is None:
+            first = top
+        else:
+            assert top == first
