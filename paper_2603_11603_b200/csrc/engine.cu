@@ -605,7 +605,10 @@ as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, b
   const int ci_n = by_bucket ? -1 : std::min(s->H.n_struct, GEN_CI_MAX);
   const size_t gen_smem = by_bucket ? (static_cast<size_t>(s->H.n_struct) + 1) * 8 + (s->D.n_bucket + 1) * 4
                                     : static_cast<size_t>(ci_n) * 8;
-  auto gen_k = s->D.ens_on ? gen_kernel<true> : gen_kernel<false>;
+  // tail-group count 5 (C2, C4, C5) as a compile-time constant: all group records loaded up front
+  const bool nc5 = s->D.n_comp == 5;
+  auto gen_k = s->D.ens_on ? (nc5 ? gen_kernel<true, 5> : gen_kernel<true, 0>)
+                           : (nc5 ? gen_kernel<false, 5> : gen_kernel<false, 0>);
   CUDA_TRY(cudaFuncSetAttribute(gen_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gen_smem)));
   int occ = 1;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gen_k, GEN_THREADS, gen_smem));

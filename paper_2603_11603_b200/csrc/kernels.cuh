@@ -214,6 +214,52 @@ __device__ __forceinline__ void decode_dev_bucket(const DevSpace& S, const uint6
   if (sidx) *sidx = lo;
   decode_tail(S, lo, static_cast<uint32_t>(p - pre[lo]), dv, act, raw);
 }
+// Generation kernel variant with a compile-time component count NC: the (offset, count, magic,
+// shift) records of all NC tail groups are loaded as soon as the structure is known, so the
+// mixed-radix chain and the tuple loads no longer wait for one record load per group in turn.
+template <int NC>
+__device__ __forceinline__ void decode_tail_nc(const DevSpace& S, int lo, uint32_t t, DV& dv, uint32_t& act, uint64_t& raw) {
+  if (NC == 0) {
+    decode_tail(S, lo, t, dv, act, raw);
+    return;
+  }
+  uint4 oc[NC > 0 ? NC : 1];
+  const uint4* ob = S.s_oc + static_cast<size_t>(lo) * (NC > 0 ? NC : 1);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) oc[c] = __ldg(ob + c);
+  const DV* sd = S.s_dv + lo;
+  dv.w[0] = __ldg(&sd->w[0]);
+  dv.w[1] = __ldg(&sd->w[1]);
+  dv.w[2] = __ldg(&sd->w[2]);
+  act = __ldg(S.s_act + lo);
+  raw = __ldg(S.s_raw + lo);
+#pragma unroll
+  for (int c = NC - 1; c >= 0; --c) {
+    const uint32_t hi = __umulhi(oc[c].z, t);
+    const uint32_t q = (hi + ((t - hi) >> (oc[c].w & 0xFFu))) >> (oc[c].w >> 8);
+    const uint32_t r = t - q * oc[c].y;
+    t = q;
+    const Tuple* tu = S.tuples + oc[c].x + r;
+    dv.w[0] |= __ldg(&tu->dv.w[0]);
+    dv.w[1] |= __ldg(&tu->dv.w[1]);
+    dv.w[2] |= __ldg(&tu->dv.w[2]);
+    act |= __ldg(&tu->act);
+    raw += __ldg(&tu->raw);
+  }
+}
+template <int NC>
+__device__ __forceinline__ void decode_dev_bucket_nc(const DevSpace& S, const uint64_t* pre, const uint32_t* bkt,
+                                                     uint64_t p, DV& dv, uint32_t& act, uint64_t& raw, int* sidx) {
+  const int b = static_cast<int>(p >> S.bshift);
+  int lo = static_cast<int>(bkt[b]), hi = static_cast<int>(bkt[b + 1]) + 1;
+  if (hi > S.n_struct) hi = S.n_struct;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (pre[mid] <= p) lo = mid; else hi = mid;
+  }
+  *sidx = lo;
+  decode_tail_nc<NC>(S, lo, static_cast<uint32_t>(p - pre[lo]), dv, act, raw);
+}
 __device__ __forceinline__ void decode_dev_idx(const DevSpace& S, const uint64_t* cidx, uint64_t p, DV& dv,
                                                uint32_t& act, uint64_t& raw) {
   decode_dev_ci(S, cidx, S.n_struct < CI ? S.n_struct : CI, p, dv, act, raw);

@@ -28,8 +28,9 @@ struct CandList {
 };
 
 // ENS: GP prior mean from the regression-simulator ensemble (NEXT-1) instead of ln cost_sim; a
-// template parameter so the default instantiation carries no trace of it (register allocation)
-template <bool ENS>
+// template parameter so the default instantiation carries no trace of it (register allocation).
+// NC: tail-group count as a compile-time constant (decode_tail_nc; 0 = any count, runtime loop)
+template <bool ENS, int NC>
 #ifndef AS_GEN_OCC
 #define AS_GEN_OCC 3
 #endif
@@ -65,7 +66,7 @@ gen_kernel(DevSpace S, BatchArgs A, uint64_t j0, uint64_t nj, CandList L, int ci
       bool pin;
       pcvi = assign_pos(A, j, pin);
       int sidx = 0;
-      if (by_bucket) decode_dev_bucket(S, gen_cidx, gen_bkt, pcvi, dv, act, raw, &sidx);
+      if (by_bucket) decode_dev_bucket_nc<NC>(S, gen_cidx, gen_bkt, pcvi, dv, act, raw, &sidx);
       else decode_dev_ci(S, gen_cidx, ci_n, pcvi, dv, act, raw, &sidx);
       if (S.srec != nullptr) {
         // per-structure products + tabulated resource check (derived mode)
