@@ -247,6 +247,17 @@ __device__ __forceinline__ void decode_tail_nc(const DevSpace& S, int lo, uint32
     raw += __ldg(&tu->raw);
   }
 }
+// structure of CVI position p from the SMEM prefix table + bucket index
+__device__ __forceinline__ int find_struct_bucket(const DevSpace& S, const uint64_t* pre, const uint32_t* bkt, uint64_t p) {
+  const int b = static_cast<int>(p >> S.bshift);
+  int lo = static_cast<int>(bkt[b]), hi = static_cast<int>(bkt[b + 1]) + 1;
+  if (hi > S.n_struct) hi = S.n_struct;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (pre[mid] <= p) lo = mid; else hi = mid;
+  }
+  return lo;
+}
 template <int NC>
 __device__ __forceinline__ void decode_dev_bucket_nc(const DevSpace& S, const uint64_t* pre, const uint32_t* bkt,
                                                      uint64_t p, DV& dv, uint32_t& act, uint64_t& raw, int* sidx) {

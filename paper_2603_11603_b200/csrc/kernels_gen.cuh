@@ -37,7 +37,7 @@ template <bool ENS, int NC>
 __global__ void __launch_bounds__(GEN_THREADS, AS_GEN_OCC)
 gen_kernel(DevSpace S, BatchArgs A, uint64_t j0, uint64_t nj, CandList L, int ci_n, unsigned long long* valid_total) {
   extern __shared__ __align__(16) uint64_t gen_cidx[];
-  __shared__ unsigned long long blk_valid;
+  __shared__ unsigned int blk_valid;         // this block's valid candidates (< 2^32 per slice)
   const int tid = threadIdx.x, lane = tid & 31;
   // ci_n < 0: SMEM copies of the whole prefix table (n_struct + 1) and the bucket index (decode by
   // bucket); else a coarse index of ci_n entries
@@ -51,7 +51,6 @@ gen_kernel(DevSpace S, BatchArgs A, uint64_t j0, uint64_t nj, CandList L, int ci
     load_cidx_n(S, gen_cidx, ci_n, tid, GEN_THREADS);
   }
   __syncthreads();
-  unsigned long long my_valid = 0;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * GEN_THREADS;
   for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * GEN_THREADS; base < nj; base += stride) {
     const uint64_t jj = base + tid;
@@ -66,17 +65,25 @@ gen_kernel(DevSpace S, BatchArgs A, uint64_t j0, uint64_t nj, CandList L, int ci
       bool pin;
       pcvi = assign_pos(A, j, pin);
       int sidx = 0;
-      if (by_bucket) decode_dev_bucket_nc<NC>(S, gen_cidx, gen_bkt, pcvi, dv, act, raw, &sidx);
-      else decode_dev_ci(S, gen_cidx, ci_n, pcvi, dv, act, raw, &sidx);
+      uint64_t memok = 0;
+      if (by_bucket) {
+        // the structure's resource-check bits are requested before the tail decode (its loads
+        // would otherwise queue behind the tuple loads and the check would wait a second L2 trip)
+        sidx = find_struct_bucket(S, gen_cidx, gen_bkt, pcvi);
+        if (S.srec != nullptr) memok = __ldg(&S.srec[sidx].memok);
+        decode_tail_nc<NC>(S, sidx, static_cast<uint32_t>(pcvi - gen_cidx[sidx]), dv, act, raw);
+      } else {
+        decode_dev_ci(S, gen_cidx, ci_n, pcvi, dv, act, raw, &sidx);
+        if (S.srec != nullptr) memok = __ldg(&S.srec[sidx].memok);
+      }
       if (S.srec != nullptr) {
         // per-structure products + tabulated resource check (derived mode)
         SimRec r;
         const double2* rp = reinterpret_cast<const double2*>(S.srec + sidx);
         const double2 a = __ldg(rp), b = __ldg(rp + 1), c = __ldg(rp + 2), e = __ldg(rp + 3);
-        const ulonglong2 f = __ldg(reinterpret_cast<const ulonglong2*>(rp + 4));
         r.comp = a.x; r.bub = a.y; r.tp = b.x; r.dp = b.y; r.ep = c.x; r.cp = c.y; r.vi_tp = e.x;
         r.tpgt1 = static_cast<uint32_t>(__double_as_longlong(e.y));
-        r.memok = f.x;
+        r.memok = memok;
         sim_fast(S.sim, S.sf, S.val, S.lg2, r, dv, act, cost, ok);
       } else {
         sim_dev(S, dv, act, cost, ok);
@@ -103,14 +110,15 @@ gen_kernel(DevSpace S, BatchArgs A, uint64_t j0, uint64_t nj, CandList L, int ci
         L.dv1[slot] = dv.w[1];
         L.dv2[slot] = dv.w[2];
       }
-      if (lane == 0) my_valid += __popc(vb);
+      // valid count straight into shared memory (a RED, no return value): a per-lane 64-bit
+      // counter live across the loop was spilled, and its reload cost ~7 % of the kernel's samples
+      if (lane == 0) atomicAdd(&blk_valid, static_cast<unsigned int>(__popc(vb)));
     }
   }
-  if (lane == 0 && my_valid) atomicAdd(&blk_valid, my_valid);
   __syncthreads();
   if (tid == 0 && blk_valid) {
-    atomicAdd(valid_total, blk_valid);
-    if (A.d_valid_count) atomicAdd(reinterpret_cast<unsigned long long*>(A.d_valid_count), blk_valid);
+    atomicAdd(valid_total, static_cast<unsigned long long>(blk_valid));
+    if (A.d_valid_count) atomicAdd(reinterpret_cast<unsigned long long*>(A.d_valid_count), static_cast<unsigned long long>(blk_valid));
   }
 }
 
