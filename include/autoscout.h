@@ -284,6 +284,17 @@ as_status autoscout_set_path(as_space* s, int32_t path);
  * AS_ERR_INVALID_ARG outside [128, 2^31]. */
 as_status autoscout_set_slice(as_space* s, uint64_t max_candidates);
 
+/* Asynchronous observe (enable != 0; spaces with the simulator prior, gp.prior = "sim"): observe()
+ * validates and decodes the new observations synchronously (its argument errors are reported as
+ * before), then returns while a host thread computes the GP fit and the device-layout operand
+ * tables (P:263-265's "profiled set" update).  Every later call that reads the
+ * fit waits for it first; score_batch launches the fit-independent candidate generation of its
+ * first slice (decode, mask, simulator) before waiting, so the host fit overlaps GPU work.  An
+ * error of the deferred fit (AS_ERR_NUMERIC: covariance not positive definite) is returned by that
+ * next call, once; the handle then keeps the previous observed set.  Results are identical to the
+ * synchronous mode.  Off by default; with enable = 0 any pending fit is completed first. */
+as_status autoscout_set_async_observe(as_space* s, int32_t enable);
+
 /* Device-time of the last score kernel launch in ms (CUDA events on the launching stream,
  * recorded when `timing` was enabled), for the roofline report in bench.py. */
 as_status autoscout_set_timing(as_space* s, int32_t enable);

@@ -38,7 +38,7 @@ EXPORTS = ["autoscout_space_create", "autoscout_space_destroy", "autoscout_space
            "autoscout_set_timing", "autoscout_raw_to_cvi", "autoscout_subtree_range", "autoscout_neighbors",
            "autoscout_prior", "autoscout_ensemble_info", "autoscout_gp_lml", "autoscout_set_gp_hyper",
            "autoscout_ml2", "autoscout_set_slice", "autoscout_topk_pool_device", "autoscout_topk_merge_device",
-           "autoscout_activity",
+           "autoscout_activity", "autoscout_set_async_observe",
            "autoscout_last_kernel_ms", "autoscout_last_phase_ms", "autoscout_last_error"]
 
 
@@ -100,6 +100,7 @@ def _load():
         "autoscout_mask_range": ([P, U64, U64, P, P, P], I32),
         "autoscout_set_path": ([P, I32], I32),
         "autoscout_set_timing": ([P, I32], I32),
+        "autoscout_set_async_observe": ([P, I32], I32),
         "autoscout_set_slice": ([P, U64], I32),
         "autoscout_last_kernel_ms": ([P, pD, pD], I32),
         "autoscout_last_phase_ms": ([P, pD, pD], I32),
@@ -280,11 +281,11 @@ class Space:
         _check(_LIB.autoscout_observe(self.h, raws.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
                                       costs.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(raws),
                                       _stream_ptr(stream)))
-        self.info = self.space_info()
+        # (no space_info() refresh here: it would wait for an asynchronous fit; self.info only
+        # caches the space's constants)
 
     def observe_clear(self):
         _check(_LIB.autoscout_observe_clear(self.h))
-        self.info = self.space_info()
 
     def observe_info(self):
         m, b, f = ctypes.c_int32(), ctypes.c_double(), ctypes.c_double()
@@ -358,6 +359,10 @@ class Space:
     def set_slice(self, max_candidates):
         """Candidates per generate + score slice of the one-hot path (list memory 40 B each)."""
         _check(_LIB.autoscout_set_slice(self.h, int(max_candidates)))
+
+    def set_async_observe(self, enable=True):
+        """observe() returns before the GP fit; score_batch overlaps it with candidate generation."""
+        _check(_LIB.autoscout_set_async_observe(self.h, 1 if enable else 0))
 
     def set_timing(self, enable=True):
         _check(_LIB.autoscout_set_timing(self.h, 1 if enable else 0))
@@ -455,3 +460,7 @@ def autoscout_ml2(space, n_set=1024, seed=0, apply=True, stream=None):
 
 def autoscout_set_slice(space, max_candidates):
     return space.set_slice(max_candidates)
+
+
+def autoscout_set_async_observe(space, enable=True):
+    return space.set_async_observe(enable)

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/autoscout.h"
@@ -224,6 +225,16 @@ struct as_space {
   bool scored = false;
   uint64_t n_launches = 0;
   uint64_t fit_upload_bytes = 0;   // H2D bytes of the last GP upload (bench e2e accounting)
+  // asynchronous observe (autoscout_set_async_observe, prior "sim" only): the host GP fit and the
+  // operand tables run on a worker thread; every call that reads the fit joins it first, and
+  // score_batch launches the fit-independent candidate generation of its first slice before joining
+  bool async_observe = false;
+  std::thread fit_thr;
+  bool fit_pending = false;
+  as_status fit_status = AS_OK;
+  std::string fit_msg;
+  int pending_M = 0;
+  bool gen0_launched = false;      // slice 0 of the next one-hot launch was generated before the join
   // timing
   bool timing = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -232,7 +243,9 @@ struct as_space {
 
 namespace {
 
-as_status upload_gp(as_space* s, cudaStream_t st) {
+// host half of the GP upload: device-layout operands staged in host vectors (no CUDA calls; runs
+// on the async-observe worker thread)
+as_status build_gp_host(as_space* s) {
   const HostSpace& H = s->H;
   const GPFit& F = s->fit;
   const int M = F.M, d = H.d;
@@ -418,7 +431,13 @@ as_status upload_gp(as_space* s, cudaStream_t st) {
   G.fstar = M > 0 ? F.fstar : INFINITY;
   G.eps = 2.0 * (d + 8 + M) * std::ldexp(1.0, -24);
   G.w_fro = F.w_fro;
+  return AS_OK;
+}
+
+// device half of the GP upload: H2D of the staged operands on stream st
+as_status upload_gp_device(as_space* s, cudaStream_t st) {
   if (s->device < 0) return AS_OK;
+  DevGP& G = s->G;
   auto cp = [&](void* dst, const void* src, size_t bytes) -> as_status {
     if (bytes) CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
     s->fit_upload_bytes += bytes;
@@ -452,6 +471,25 @@ as_status upload_gp(as_space* s, cudaStream_t st) {
   G.alpha64 = s->d_alpha64;
   G.W64 = s->d_W64;
   return AS_OK;
+}
+
+as_status upload_gp(as_space* s, cudaStream_t st) {
+  as_status r = build_gp_host(s);
+  return r == AS_OK ? upload_gp_device(s, st) : r;
+}
+
+// wait for an asynchronous observe(): commit its fit (or report its deferred error) and upload it
+as_status join_fit(const as_space* cs, cudaStream_t st) {
+  as_space* s = const_cast<as_space*>(cs);
+  if (!s->fit_pending) return AS_OK;
+  s->fit_thr.join();
+  s->fit_pending = false;
+  if (s->fit_status != AS_OK) {
+    const as_status r = s->fit_status;
+    s->fit_status = AS_OK;
+    return fail(r, "deferred observe(): " + s->fit_msg);
+  }
+  return upload_gp_device(s, st);
 }
 
 as_status ensure_lists(as_space* s, int grid) {
@@ -586,6 +624,63 @@ bool build_simrec(const HostSpace& H, std::vector<SimRec>& rec, SimFast& F) {
   return true;
 }
 
+struct GenCfg {
+  void (*k)(DevSpace, BatchArgs, uint64_t, uint64_t, CandList, int, unsigned long long*);
+  int ci_n;
+  size_t smem;
+  int grid;
+};
+
+// generation kernel configuration (independent of the GP fit)
+GenCfg gen_config(as_space* s) {
+  GenCfg g{};
+  // whole prefix table + bucket index in SMEM when they fit, else a coarse index of GEN_CI_MAX entries
+  const bool by_bucket = s->H.n_struct + 1 <= GEN_CI_MAX;
+  const int ci_n = by_bucket ? -1 : std::min(s->H.n_struct, GEN_CI_MAX);
+  const size_t gen_smem = by_bucket ? (static_cast<size_t>(s->H.n_struct) + 1) * 8 + (s->D.n_bucket + 1) * 4
+                                    : static_cast<size_t>(ci_n) * 8;
+  // tail-group count 5 (C2, C4, C5) as a compile-time constant: all group records loaded up front
+  const bool nc5 = s->D.n_comp == 5;
+  auto gen_k = s->D.ens_on ? (nc5 ? gen_kernel<true, 5> : gen_kernel<true, 0>)
+                           : (nc5 ? gen_kernel<false, 5> : gen_kernel<false, 0>);
+  int occ = 1;
+  if (cudaFuncSetAttribute(gen_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gen_smem)) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gen_k, GEN_THREADS, gen_smem) != cudaSuccess)
+    occ = 1;
+  g.k = gen_k;
+  g.ci_n = ci_n;
+  g.smem = gen_smem;
+  g.grid = s->n_sm * std::max(occ, 1);
+  return g;
+}
+
+// candidates [j0, j0 + nj) of the batch into the compact list (count reset first)
+as_status gen_launch(as_space* s, const GenCfg& g, const BatchArgs& A, uint64_t j0, uint64_t nj, cudaStream_t st) {
+  CUDA_TRY(cudaMemsetAsync(s->list.count, 0, sizeof(unsigned long long), st));
+  g.k<<<g.grid, GEN_THREADS, g.smem, st>>>(s->D, A, j0, nj, s->list, g.ci_n, reinterpret_cast<unsigned long long*>(s->d_valid));
+  CUDA_TRY(cudaGetLastError());
+  ++s->n_launches;
+  return AS_OK;
+}
+
+BatchArgs batch_args(const as_space* s, const as_score_args& a) {
+  BatchArgs A{};
+  A.mode = a.mode;
+  A.acq = a.acq;
+  A.begin = a.begin;
+  A.count = a.count;
+  A.fk = feistel_make(s->H.n_cvi, a.seed);
+  A.list = a.mode == AS_MODE_LIST ? a.d_positions : nullptr;
+  A.n_cvi = s->H.n_cvi;
+  A.kappa = a.kappa;
+  A.xi = a.xi;
+  A.d_scores = a.d_scores;
+  A.d_screen = a.d_screen;
+  A.d_raw = a.d_raw;
+  A.d_valid_count = a.d_valid_count;
+  return A;
+}
+
 as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, bool reset, cudaStream_t st) {
   s->sev_used = 0;
   if (s->timing) CUDA_TRY(cudaEventRecord(s->ev[0], st));
@@ -600,19 +695,7 @@ as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, b
     r = ensure_cand_list(s, static_cast<size_t>(std::min<uint64_t>(count, s->slice)));
     if (r != AS_OK) return r;
   }
-  // whole prefix table + bucket index in SMEM when they fit, else a coarse index of GEN_CI_MAX entries
-  const bool by_bucket = s->H.n_struct + 1 <= GEN_CI_MAX;
-  const int ci_n = by_bucket ? -1 : std::min(s->H.n_struct, GEN_CI_MAX);
-  const size_t gen_smem = by_bucket ? (static_cast<size_t>(s->H.n_struct) + 1) * 8 + (s->D.n_bucket + 1) * 4
-                                    : static_cast<size_t>(ci_n) * 8;
-  // tail-group count 5 (C2, C4, C5) as a compile-time constant: all group records loaded up front
-  const bool nc5 = s->D.n_comp == 5;
-  auto gen_k = s->D.ens_on ? (nc5 ? gen_kernel<true, 5> : gen_kernel<true, 0>)
-                           : (nc5 ? gen_kernel<false, 5> : gen_kernel<false, 0>);
-  CUDA_TRY(cudaFuncSetAttribute(gen_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gen_smem)));
-  int occ = 1;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gen_k, GEN_THREADS, gen_smem));
-  const int grid_gen = s->n_sm * std::max(occ, 1);
+  const GenCfg gc = gen_config(s);
   auto k2 = tc2_kernel_for(s->G.kernel, s->t2.nh, s->tb.nch);
   CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   TcB tb = s->tb;
@@ -625,12 +708,13 @@ as_status launch_tc2(as_space* s, const BatchArgs& A, CtaOut out, size_t smem, b
     const uint64_t j0 = sl * SL, nj = std::min<uint64_t>(SL, count - j0);
     const bool ev = s->timing && s->sev_used + 3 <= static_cast<int>(s->sev.size());
     if (nj > 0) {
-      CUDA_TRY(cudaMemsetAsync(s->list.count, 0, sizeof(unsigned long long), st));
       if (ev) CUDA_TRY(cudaEventRecord(s->sev[s->sev_used], st));
-      gen_k<<<grid_gen, GEN_THREADS, gen_smem, st>>>(s->D, A, j0, nj, s->list, ci_n,
-                                                           reinterpret_cast<unsigned long long*>(s->d_valid));
-      CUDA_TRY(cudaGetLastError());
-      ++s->n_launches;
+      if (sl == 0 && s->gen0_launched) {
+        s->gen0_launched = false;              // generated before the observe() join (score_batch)
+      } else {
+        r = gen_launch(s, gc, A, j0, nj, st);
+        if (r != AS_OK) return r;
+      }
       if (ev) CUDA_TRY(cudaEventRecord(s->sev[s->sev_used + 1], st));
       static unsigned long long* tr_buf = nullptr;
       const char* tr_path = std::getenv("AS_TC2_TRACE");   // development aid: CTA-0 phase timeline
@@ -726,20 +810,8 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
       s->scratch_cap = need;
     }
   }
-  BatchArgs A{};
-  A.mode = a.mode;
-  A.acq = a.acq;
-  A.begin = a.begin;
-  A.count = a.count;
-  A.fk = feistel_make(s->H.n_cvi, a.seed);
-  A.list = a.mode == AS_MODE_LIST ? a.d_positions : nullptr;
-  A.n_cvi = s->H.n_cvi;
-  A.kappa = a.kappa;
-  A.xi = a.xi;
-  A.d_scores = a.d_scores;
-  A.d_screen = a.d_screen;
-  A.d_raw = a.d_raw;
-  A.d_valid_count = a.d_valid_count;
+  const BatchArgs A = batch_args(s, a);
+  if (!use_tc2) s->gen0_launched = false;   // an early slice-0 generation is simply unused
   CtaOut out{s->d_lists, s->d_counts, s->d_drops, s->d_valid, s->KC, P};
   DevGP G = s->G;
   if (use_tc2) return launch_tc2(s, A, out, smem, reset, st);
@@ -1048,6 +1120,10 @@ as_status autoscout_space_create(const char* space_json, int32_t cuda_device, as
 
 void autoscout_space_destroy(as_space* s) {
   if (!s) return;
+  if (s->fit_pending) {   // a pending asynchronous fit finishes before the handle goes away
+    s->fit_thr.join();
+    s->fit_pending = false;
+  }
   if (s->device >= 0) {
     cudaSetDevice(s->device);
     for (void* p : s->owned) cudaFree(p);
@@ -1073,6 +1149,7 @@ void autoscout_space_destroy(as_space* s) {
 
 as_status autoscout_space_info(const as_space* s, as_space_info* out) {
   if (!s || !out) return fail(AS_ERR_INVALID_ARG, "null argument");
+  if (const as_status jr = join_fit(s, nullptr)) return jr;
   out->n_raw = s->H.n_raw;
   out->n_cvi = s->H.n_cvi;
   out->n_features = s->H.d;
@@ -1088,6 +1165,10 @@ as_status autoscout_space_info(const as_space* s, as_space_info* out) {
 
 as_status autoscout_observe(as_space* s, const uint64_t* raw_idx, const double* cost, int64_t n, void* cuda_stream) {
   if (!s || n < 0 || (n > 0 && (!raw_idx || !cost))) return fail(AS_ERR_INVALID_ARG, "bad arguments");
+  {
+    const as_status jr = join_fit(s, static_cast<cudaStream_t>(cuda_stream));
+    if (jr != AS_OK) return jr;
+  }
   if (static_cast<int64_t>(s->obs_raw.size()) + n > MMAX)
     return fail(AS_ERR_CAPACITY, "more than " + std::to_string(MMAX) + " observed configurations");
   std::vector<DV> ndv;
@@ -1116,17 +1197,43 @@ as_status autoscout_observe(as_space* s, const uint64_t* raw_idx, const double* 
   all_act.insert(all_act.end(), nact.begin(), nact.end());
   all_cost.insert(all_cost.end(), cost, cost + n);
   all_sim.insert(all_sim.end(), nsim.begin(), nsim.end());
-  GPFit fit;
-  EnsembleFit ens;
-  std::vector<double> m0_ens;
-  if (s->H.prior == 1) {
-    ensemble_fit(s->H, all_dv, all_cost, ens);
-    if (ens.on)
-      for (const DV& dv : all_dv) m0_ens.push_back(ensemble_m0(s->H, ens, dv));
+  // the numeric fit (+ the device-layout operand tables): inline, or on a worker thread
+  auto fit_work = [s, all_dv = std::move(all_dv), all_act = std::move(all_act), all_cost = std::move(all_cost),
+                   all_sim = std::move(all_sim), raws = std::vector<uint64_t>(raw_idx, raw_idx + n)]() mutable
+      -> std::pair<as_status, std::string> {
+    GPFit fit;
+    EnsembleFit ens;
+    std::vector<double> m0_ens;
+    if (s->H.prior == 1) {
+      ensemble_fit(s->H, all_dv, all_cost, ens);
+      if (ens.on)
+        for (const DV& dv : all_dv) m0_ens.push_back(ensemble_m0(s->H, ens, dv));
+    }
+    Status st = gp_fit(s->H, all_dv, all_act, all_cost, all_sim, fit, ens.on ? &m0_ens : nullptr);
+    if (!st.ok()) return {static_cast<as_status>(st.code), st.msg};
+    s->ens = std::move(ens);
+    s->obs_raw.insert(s->obs_raw.end(), raws.begin(), raws.end());
+    s->obs_dv = std::move(all_dv);
+    s->obs_act = std::move(all_act);
+    s->obs_cost = std::move(all_cost);
+    s->obs_sim = std::move(all_sim);
+    s->fit = std::move(fit);
+    return {build_gp_host(s), std::string()};
+  };
+  if (s->async_observe && s->H.prior != 1 && s->device >= 0) {
+    invalidate_pool(s);   // the running pool was screened under the previous fit
+    s->pending_M = static_cast<int>(s->obs_dv.size() + ndv.size());
+    s->fit_pending = true;
+    s->fit_thr = std::thread([s, w = std::move(fit_work)]() mutable {
+      const auto r = w();
+      s->fit_status = r.first;
+      s->fit_msg = r.second;
+    });
+    return AS_OK;
   }
-  Status st = gp_fit(s->H, all_dv, all_act, all_cost, all_sim, fit, ens.on ? &m0_ens : nullptr);
-  if (!st.ok()) return fail(static_cast<as_status>(st.code), st.msg);
-  s->ens = std::move(ens);
+  const auto r = fit_work();
+  if (r.first != AS_OK) return fail(r.first, r.second);
+  invalidate_pool(s);     // the running pool was screened under the previous fit
   if (s->device >= 0) {
     if (s->ens.on) {
       CUDA_TRY(cudaMemcpy(s->d_ens_tab, s->ens.tab.data(), s->ens.tab.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -1134,20 +1241,14 @@ as_status autoscout_observe(as_space* s, const uint64_t* raw_idx, const double* 
     s->D.ens_on = s->ens.on ? 1 : 0;
     s->D.ens_c0 = s->ens.c0;
   }
-  s->obs_raw.insert(s->obs_raw.end(), raw_idx, raw_idx + n);
-  s->obs_dv = std::move(all_dv);
-  s->obs_act = std::move(all_act);
-  s->obs_cost = std::move(all_cost);
-  s->obs_sim = std::move(all_sim);
-  s->fit = std::move(fit);
-  invalidate_pool(s);   // the running pool was screened under the previous fit
-  const as_status ur = upload_gp(s, static_cast<cudaStream_t>(cuda_stream));
+  const as_status ur = upload_gp_device(s, static_cast<cudaStream_t>(cuda_stream));
   if (ur == AS_OK && s->ens.on) s->fit_upload_bytes += s->ens.tab.size() * sizeof(double);
   return ur;
 }
 
 as_status autoscout_observe_clear(as_space* s) {
   if (!s) return fail(AS_ERR_INVALID_ARG, "null argument");
+  join_fit(s, nullptr);   // a pending fit is superseded (a deferred error no longer matters)
   s->obs_raw.clear();
   s->obs_dv.clear();
   s->obs_act.clear();
@@ -1162,6 +1263,7 @@ as_status autoscout_observe_clear(as_space* s) {
 
 as_status autoscout_observe_info(const as_space* s, int32_t* m_out, double* b_out, double* fstar_out) {
   if (!s) return fail(AS_ERR_INVALID_ARG, "null argument");
+  if (const as_status jr = join_fit(s, nullptr)) return jr;
   if (m_out) *m_out = s->fit.M;
   if (b_out) *b_out = s->fit.b;
   if (fstar_out) *fstar_out = s->fit.M > 0 ? s->fit.fstar : INFINITY;
@@ -1185,7 +1287,8 @@ as_status autoscout_score_batch(as_space* s, const as_score_args* a, void* cuda_
     return fail(AS_ERR_INVALID_ARG, "kappa must be finite and >= 0, xi finite");
   if (a->mode != AS_MODE_LIST && (a->begin > s->H.n_cvi || a->count > s->H.n_cvi - a->begin))
     return fail(AS_ERR_INDEX_RANGE, "batch exceeds [0, n_cvi)");
-  if (a->acq == AS_ACQ_EI && s->G.M == 0) return fail(AS_ERR_NO_OBSERVATIONS, "EI needs at least one observation");
+  if (a->acq == AS_ACQ_EI && (s->fit_pending ? s->pending_M : s->G.M) == 0)
+    return fail(AS_ERR_NO_OBSERVATIONS, "EI needs at least one observation");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   CUDA_TRY(cudaSetDevice(s->device));
   const bool reset = !a->accumulate || !s->scored;
@@ -1194,10 +1297,26 @@ as_status autoscout_score_batch(as_space* s, const as_score_args* a, void* cuda_
     if (a->acq != b0.acq || a->kappa != b0.kappa || a->xi != b0.xi)
       return fail(AS_ERR_INVALID_ARG, "accumulate = 1 needs the acquisition, kappa and xi of the pool's first batch");
   }
+  if (reset) CUDA_TRY(cudaMemsetAsync(s->d_valid, 0, sizeof(uint64_t), st));
+  if (s->fit_pending) {
+    // asynchronous observe(): the candidate generation of the first slice does not depend on the
+    // fit, so it runs on the GPU while the host thread finishes the fit (one-hot path only)
+    if (reset && a->acq != AS_ACQ_SIM && a->count > 0 && (s->path == 0 || s->path == 3)) {
+      const uint64_t nj = std::min<uint64_t>(a->count, s->slice);
+      as_status r = ensure_cand_list(s, static_cast<size_t>(nj));
+      if (r == AS_OK) r = gen_launch(s, gen_config(s), batch_args(s, *a), 0, nj, st);
+      if (r != AS_OK) return r;
+      s->gen0_launched = true;
+    }
+    const as_status jr = join_fit(s, st);
+    if (jr != AS_OK) {
+      s->gen0_launched = false;
+      return jr;
+    }
+  }
   if (reset) {
     s->batches.clear();
     s->KC = std::min(a->k + std::max(a->k, 64), s->KC_max);
-    CUDA_TRY(cudaMemsetAsync(s->d_valid, 0, sizeof(uint64_t), st));
   }
   as_score_args rec = *a;
   rec.d_scores = nullptr;
@@ -1214,6 +1333,7 @@ as_status autoscout_score_batch(as_space* s, const as_score_args* a, void* cuda_
 as_status autoscout_topk(as_space* s, int32_t k, uint64_t* raw_out, double* score_out, int32_t* n_out,
                          void* cuda_stream) {
   if (!s || !raw_out || !score_out || !n_out || k < 1) return fail(AS_ERR_INVALID_ARG, "bad arguments");
+  if (const as_status jr = join_fit(s, static_cast<cudaStream_t>(cuda_stream))) return jr;
   if (!s->scored || s->batches.empty()) return fail(AS_ERR_STATE, "nothing scored");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   CUDA_TRY(cudaSetDevice(s->device));
@@ -1235,6 +1355,7 @@ as_status autoscout_topk(as_space* s, int32_t k, uint64_t* raw_out, double* scor
 as_status autoscout_topk_pool(as_space* s, int32_t k, void* pool_out, int32_t cap, int32_t* n_out, void* cut_out,
                               void* cuda_stream) {
   if (!s || !pool_out || !n_out || !cut_out || cap < 1 || k < 1) return fail(AS_ERR_INVALID_ARG, "bad arguments");
+  if (const as_status jr = join_fit(s, static_cast<cudaStream_t>(cuda_stream))) return jr;
   if (!s->scored || s->batches.empty()) return fail(AS_ERR_STATE, "nothing scored");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   CUDA_TRY(cudaSetDevice(s->device));
@@ -1288,6 +1409,7 @@ as_status autoscout_topk_merge(const as_space* s, const void* pools, const int32
 
 as_status autoscout_topk_pool_device(as_space* s, int32_t k, void* d_pool_out, int32_t cap, void* cuda_stream) {
   if (!s || !d_pool_out || cap < 1 || k < 1) return fail(AS_ERR_INVALID_ARG, "bad arguments");
+  if (const as_status jr = join_fit(s, static_cast<cudaStream_t>(cuda_stream))) return jr;
   if (s->device < 0) return fail(AS_ERR_STATE, "host-only handle");
   if (!s->scored || s->batches.empty()) return fail(AS_ERR_STATE, "nothing scored");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
@@ -1387,6 +1509,7 @@ as_status autoscout_cvi_to_raw(const as_space* s, uint64_t cvi, uint64_t* raw_ou
 // ---------------------------------------------------------------- NEXT-4: ML-II evidence on the device
 as_status autoscout_gp_lml(as_space* s, const double* hyp, int32_t n_set, double* lml_out, void* cuda_stream) {
   if (!s || (n_set > 0 && (!hyp || !lml_out)) || n_set < 0) return fail(AS_ERR_INVALID_ARG, "bad arguments");
+  if (const as_status jr = join_fit(s, static_cast<cudaStream_t>(cuda_stream))) return jr;
   if (s->device < 0) return fail(AS_ERR_STATE, "host-only handle cannot launch (no CUDA device)");
   const int M = s->fit.M, d = s->H.d;
   if (M == 0) return fail(AS_ERR_NO_OBSERVATIONS, "the evidence needs observations");
@@ -1450,6 +1573,7 @@ as_status apply_gp_hyper(as_space* s, const double* lengthscale, double sf2, dou
 
 as_status autoscout_set_gp_hyper(as_space* s, const double* lengthscale, double sf2, double sn2) {
   if (!s || !lengthscale) return fail(AS_ERR_INVALID_ARG, "null argument");
+  if (const as_status jr = join_fit(s, nullptr)) return jr;
   for (int j = 0; j < s->H.d; ++j)
     if (!(lengthscale[j] > 0.0) || !std::isfinite(lengthscale[j])) return fail(AS_ERR_INVALID_ARG, "lengthscale must be > 0");
   if (!(sf2 > 0.0) || !(sn2 > 0.0) || !std::isfinite(sf2) || !std::isfinite(sn2))
@@ -1458,6 +1582,8 @@ as_status autoscout_set_gp_hyper(as_space* s, const double* lengthscale, double 
   const double old_sf2 = s->H.sf2, old_sn2 = s->H.sn2;
   const std::vector<uint64_t> raws = s->obs_raw;
   const std::vector<double> costs = s->obs_cost;
+  const bool async0 = s->async_observe;   // the refit below must report its error here (synchronous)
+  s->async_observe = false;
   as_status r = apply_gp_hyper(s, lengthscale, sf2, sn2);
   // refit the current observed set under the new hyper-parameters (observe_clear + observe)
   if (r == AS_OK) r = autoscout_observe_clear(s);
@@ -1472,6 +1598,7 @@ as_status autoscout_set_gp_hyper(as_space* s, const double* lengthscale, double 
     if (!raws.empty()) autoscout_observe(s, raws.data(), costs.data(), static_cast<int64_t>(raws.size()), nullptr);
     g_err = why;
   }
+  s->async_observe = async0;
   return r;
 }
 
@@ -1500,6 +1627,7 @@ void ml2_candidate(const HostSpace& H, uint64_t seed, int h, double* out) {
 as_status autoscout_ml2(as_space* s, int32_t n_set, uint64_t seed, int32_t apply, double* best_hyp_out,
                         double* best_lml_out, int32_t* best_index_out, void* cuda_stream) {
   if (!s || n_set < 1) return fail(AS_ERR_INVALID_ARG, "n_set must be >= 1");
+  if (const as_status jr = join_fit(s, static_cast<cudaStream_t>(cuda_stream))) return jr;
   const int d = s->H.d;
   std::vector<double> hyp(static_cast<size_t>(n_set) * (d + 2)), lml(n_set);
   for (int h = 0; h < n_set; ++h) ml2_candidate(s->H, seed, h, hyp.data() + static_cast<size_t>(h) * (d + 2));
@@ -1520,6 +1648,7 @@ as_status autoscout_ml2(as_space* s, int32_t n_set, uint64_t seed, int32_t apply
 
 as_status autoscout_prior(const as_space* s, uint64_t raw, double* m0_out, int32_t* source_out) {
   if (!s || !m0_out) return fail(AS_ERR_INVALID_ARG, "null argument");
+  if (const as_status jr = join_fit(s, nullptr)) return jr;
   int dig[DMAX];
   DV dv;
   uint32_t act;
@@ -1539,6 +1668,7 @@ as_status autoscout_prior(const as_space* s, uint64_t raw, double* m0_out, int32
 
 as_status autoscout_ensemble_info(const as_space* s, double* r2_out, double* w_out, int32_t* available_out) {
   if (!s) return fail(AS_ERR_INVALID_ARG, "null argument");
+  if (const as_status jr = join_fit(s, nullptr)) return jr;
   for (int m = 0; m < 4; ++m) {
     if (r2_out) r2_out[m] = s->ens.r2[m];
     if (w_out) w_out[m] = s->ens.w[m];
@@ -1652,6 +1782,13 @@ as_status autoscout_set_slice(as_space* s, uint64_t max_candidates) {
   if (!s || max_candidates < TC_ROWS || max_candidates > (1ull << 31))
     return fail(AS_ERR_INVALID_ARG, "slice must be in [128, 2^31] candidates");
   s->slice = max_candidates;
+  return AS_OK;
+}
+
+as_status autoscout_set_async_observe(as_space* s, int32_t enable) {
+  if (!s) return fail(AS_ERR_INVALID_ARG, "null argument");
+  if (const as_status jr = join_fit(s, nullptr)) return jr;
+  s->async_observe = enable != 0;
   return AS_OK;
 }
 

@@ -24,6 +24,7 @@ class HostPool {
   // fn(task) for every task in [0, n); the caller takes part and returns when all tasks are done
   void run(int n, const std::function<void(int)>& fn) {
     if (n <= 0) return;
+    std::lock_guard<std::mutex> caller(run_mu_);   // one fork-join at a time (e.g. two spaces' fits)
     if (n == 1 || workers_.empty()) {
       for (int i = 0; i < n; ++i) fn(i);
       return;
@@ -92,7 +93,7 @@ class HostPool {
     }
   }
   std::vector<std::thread> workers_;
-  std::mutex mu_;
+  std::mutex mu_, run_mu_;
   std::condition_variable cv_, done_cv_;
   const std::function<void(int)>* fn_ = nullptr;
   int n_ = 0;

@@ -262,3 +262,46 @@ def test_repeated_launches_same_result(name, M, mode, count):
             first = top
         else:
             assert top == first
+
+
+# ---------------------------------------------------------------- asynchronous observe
+@pytest.mark.parametrize("name,M,mode,count", [("C4", 256, "sample", 3_000_000), ("C2", 64, "range", None),
+                                               ("C5", 128, "range", None)])
+def test_async_observe_same_results(name, M, mode, count):
+    """set_async_observe: observe() returns before the fit, score_batch generates slice 0 while the
+    host thread fits; certified top-k, scores and the fit summary equal the synchronous handle's,
+    over repeated observe_clear / observe / score / topk cycles (the bench's e2e loop)."""
+    o = oracle_space(name)
+    raws, costs = observed(o, M, 0)
+    count = o.n_cvi() if count is None else count
+    ref = A.Space(space_path(name), 0)
+    ref.observe(raws, costs)
+    ref.score_batch(mode=mode, begin=0, count=count, seed=1, acq="ei", k=32)
+    want = ref.topk(32)
+    sp = A.Space(space_path(name), 0)
+    sp.set_async_observe(True)
+    for _ in range(3):
+        sp.observe_clear()
+        sp.observe(raws, costs)
+        sp.score_batch(mode=mode, begin=0, count=count, seed=1, acq="ei", k=32)
+        assert sp.topk(32) == want
+        assert sp.observe_info() == ref.observe_info()
+    torch.cuda.synchronize()
+
+
+def test_async_observe_deferred_error():
+    """A fit that fails on the worker thread (duplicated observation, sn2 ~ 0: K singular) is
+    reported by the next call, once; the handle keeps the previous observed set."""
+    o = oracle_space("C1")
+    raws, costs = observed(o, 8, 0)
+    sp = A.Space(space_path("C1"), 0)
+    sp.set_gp_hyper([0.5] * len(o.features), 0.1, 1e-300)
+    sp.observe(raws, costs)
+    before = sp.observe_info()
+    sp.set_async_observe(True)
+    sp.observe(raws[:1], costs[:1])                   # returns: the fit runs on the worker thread
+    with pytest.raises(A.AutoscoutError):
+        sp.score_batch(mode="range", begin=0, count=o.n_cvi(), acq="ei", k=8)
+    assert sp.observe_info() == before
+    sp.score_batch(mode="range", begin=0, count=o.n_cvi(), acq="ei", k=8)
+    assert len(sp.topk(8)) == 8
