@@ -847,9 +847,8 @@ as_status launch_batch(as_space* s, const as_score_args& a, bool reset, cudaStre
 // Refine the running pool in FP64 and bring it to the host, sorted (score desc, raw asc).
 as_status refine_pool(as_space* s, int acq, double kappa, double xi, cudaStream_t st, std::vector<Entry>& ent,
                       uint64_t& cut, int& n_pool) {
-  const int blocks = (s->KC + REFINE_WARPS - 1) / REFINE_WARPS;
-  const size_t smem = static_cast<size_t>(REFINE_WARPS) * std::max(s->G.M, 1) * sizeof(double);
-  refine_kernel<<<blocks, REFINE_WARPS * 32, smem, st>>>(s->D, s->G, s->d_pool, s->d_pool_n, acq, kappa, xi,
+  const size_t smem = static_cast<size_t>(std::max(s->G.M, 1)) * sizeof(double);
+  refine_kernel<<<s->KC, REFINE_CTA, smem, st>>>(s->D, s->G, s->d_pool, s->d_pool_n, acq, kappa, xi,
                                                          s->d_ref_score, s->d_ref_raw);
   CUDA_TRY(cudaGetLastError());
   ++s->n_launches;
@@ -1417,9 +1416,8 @@ as_status autoscout_topk_pool_device(as_space* s, int32_t k, void* d_pool_out, i
   const as_score_args& a0 = s->batches.front();
   int* h_flag = reinterpret_cast<int*>(s->h_stage);   // pinned; refine_pool is not running concurrently
   for (;;) {
-    const int blocks = (s->KC + REFINE_WARPS - 1) / REFINE_WARPS;
-    const size_t rsm = static_cast<size_t>(REFINE_WARPS) * std::max(s->G.M, 1) * sizeof(double);
-    refine_kernel<<<blocks, REFINE_WARPS * 32, rsm, st>>>(s->D, s->G, s->d_pool, s->d_pool_n, a0.acq, a0.kappa,
+    const size_t rsm = static_cast<size_t>(std::max(s->G.M, 1)) * sizeof(double);
+    refine_kernel<<<s->KC, REFINE_CTA, rsm, st>>>(s->D, s->G, s->d_pool, s->d_pool_n, a0.acq, a0.kappa,
                                                           a0.xi, s->d_ref_score, s->d_ref_raw);
     CUDA_TRY(cudaGetLastError());
     ++s->n_launches;
