@@ -292,6 +292,7 @@ as_status build_gp_host(as_space* s) {
   }
   // chunk offsets first, then the chunks in parallel on the host pool (each writes its own range)
   HostPool& pool = HostPool::get();
+  const bool par = M >= 128;  // small fits: inline (the pool wake-ups would dominate)
   {
     size_t tot = 0;
     for (int c = 0; c < nch; ++c) {
@@ -313,7 +314,7 @@ as_status build_gp_host(as_space* s) {
         s->h_Bch[base + off] = hi;
         s->h_Bch[base + static_cast<size_t>(N) * TC_KCH + off] = lo;
       }
-  });
+  }, par);
   // T operand of the one-hot R2 contraction (kernels_tc2.cuh): group g = observed points
   // [64g, 64g+64) x one-hot columns (f, v); T = 2^s (xt_f[v] - o_jf)^2 in FP64, split hi + lo FP16.
   // SIMT features: 2^(s/2) xt and 2^(s/2) o in FP32.
@@ -370,7 +371,7 @@ as_status build_gp_host(as_space* s) {
           }
         }
       }
-    });
+    }, par);
     // L^-1^T chunks for the FP16 contraction: chunk c = rows i in [16c, Mp16) x columns j in
     // [16c, 16c+16), 2^ew L^-1[i][j] split hi + lo FP16 (kmajor_off16); k is scaled by 2^ek in-kernel
     {
@@ -408,7 +409,7 @@ as_status build_gp_host(as_space* s) {
             s->h_Wch[base + o] = hi;
             s->h_Wch[base + static_cast<size_t>(N) * TC_KCH + o] = h16(w - v16(hi));
           }
-      });
+      }, par);
     }
     const double hs = std::ldexp(1.0, sc / 2);
     s->h_xh.assign(static_cast<size_t>(4) * VMAX, 0.f);
@@ -1219,7 +1220,8 @@ as_status autoscout_observe(as_space* s, const uint64_t* raw_idx, const double* 
     s->fit = std::move(fit);
     return {build_gp_host(s), std::string()};
   };
-  if (s->async_observe && s->H.prior != 1 && s->device >= 0) {
+  // asynchronous only where the fit is worth a thread (M >= 128: ~1 ms of host work at M = 256)
+  if (s->async_observe && s->H.prior != 1 && s->device >= 0 && s->obs_dv.size() + ndv.size() >= 128) {
     invalidate_pool(s);   // the running pool was screened under the previous fit
     s->pending_M = static_cast<int>(s->obs_dv.size() + ndv.size());
     s->fit_pending = true;

@@ -22,8 +22,13 @@ class HostPool {
   }
   int threads() const { return static_cast<int>(workers_.size()) + 1; }
   // fn(task) for every task in [0, n); the caller takes part and returns when all tasks are done
-  void run(int n, const std::function<void(int)>& fn) {
+  // parallel = false: inline on the caller (small fits, where waking the pool costs more than it saves)
+  void run(int n, const std::function<void(int)>& fn, bool parallel = true) {
     if (n <= 0) return;
+    if (!parallel) {
+      for (int i = 0; i < n; ++i) fn(i);
+      return;
+    }
     std::lock_guard<std::mutex> caller(run_mu_);   // one fork-join at a time (e.g. two spaces' fits)
     if (n == 1 || workers_.empty()) {
       for (int i = 0; i < n; ++i) fn(i);

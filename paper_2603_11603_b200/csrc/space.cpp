@@ -929,6 +929,7 @@ Status gp_fit(const HostSpace& S, const std::vector<DV>& obs_dv, const std::vect
   // computed by one task with the operations and order of the sequential loops, so the fit does not
   // depend on the thread count.
   HostPool& pool = HostPool::get();
+  const bool par = M >= 128;  // below, the whole fit takes tens of microseconds: no thread wake-ups
   std::vector<double> L(static_cast<size_t>(M) * M, 0.0);
   pool.run(M, [&](int i) {
     for (int j = 0; j <= i; ++j) {
@@ -939,7 +940,7 @@ Status gp_fit(const HostSpace& S, const std::vector<DV>& obs_dv, const std::vect
       }
       L[i * M + j] = kernel64(S.kernel, S.sf2, r2) + (i == j ? S.sn2 : 0.0);
     }
-  });
+  }, par);
   // Right-looking Cholesky in column blocks of CB: factor the diagonal block, then the panel below
   // it (rows in parallel), then the trailing update A[i][j] -= L[i][q] L[j][q] for the block's q
   // (rows in parallel).  Each element still receives its updates in ascending q (the textbook
@@ -981,7 +982,7 @@ Status gp_fit(const HostSpace& S, const std::vector<DV>& obs_dv, const std::vect
         const double* lq = Lt.data() + static_cast<size_t>(q) * M;
         for (int j = q + 1; j < k1; ++j) ai[j] -= liq * lq[j];
       }
-    });
+    }, par);
     pool.run(M - k1, [&](int t) {           // trailing update of row i: columns [k1, i]
       const int i = M - 1 - t;                // longest rows first
       double* ai = L.data() + static_cast<size_t>(i) * M;
@@ -990,7 +991,7 @@ Status gp_fit(const HostSpace& S, const std::vector<DV>& obs_dv, const std::vect
         const double* lq = Lt.data() + static_cast<size_t>(q) * M;
         for (int j = k1; j <= i; ++j) ai[j] -= liq * lq[j];
       }
-    });
+    }, par);
   }
   if (!pd) return err(E_NUM, "Cholesky of the GP covariance failed (not positive definite)");
   // alpha = L^-T L^-1 r
@@ -1042,7 +1043,7 @@ Status gp_fit(const HostSpace& S, const std::vector<DV>& obs_dv, const std::vect
       const double lii = L[i * M + i];
       for (int c = c0; c < ce; ++c) fit.Wl[static_cast<size_t>(i) * M + c] = t[c - c0] / lii;
     }
-  });
+  }, par);
   double fro = 0.0;
   for (double w : fit.Wl) fro += w * w;
   fit.w_fro = std::sqrt(fro);

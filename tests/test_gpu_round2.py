@@ -291,17 +291,18 @@ def test_async_observe_same_results(name, M, mode, count):
 
 def test_async_observe_deferred_error():
     """A fit that fails on the worker thread (duplicated observation, sn2 ~ 0: K singular) is
-    reported by the next call, once; the handle keeps the previous observed set."""
-    o = oracle_space("C1")
-    raws, costs = observed(o, 8, 0)
-    sp = A.Space(space_path("C1"), 0)
+    reported by the next call, once; the handle keeps the previous observed set.  (Asynchronous
+    only from 128 observations: C5 with 128 + 1.)"""
+    o = oracle_space("C5")
+    raws, costs = observed(o, 128, 0)
+    sp = A.Space(space_path("C5"), 0)
     sp.set_gp_hyper([0.5] * len(o.features), 0.1, 1e-300)
     sp.observe(raws, costs)
     before = sp.observe_info()
     sp.set_async_observe(True)
     sp.observe(raws[:1], costs[:1])                   # returns: the fit runs on the worker thread
     with pytest.raises(A.AutoscoutError):
-        sp.score_batch(mode="range", begin=0, count=o.n_cvi(), acq="ei", k=8)
+        sp.score_batch(mode="range", begin=0, count=1 << 20, acq="ei", k=8)
     assert sp.observe_info() == before
-    sp.score_batch(mode="range", begin=0, count=o.n_cvi(), acq="ei", k=8)
+    sp.score_batch(mode="range", begin=0, count=1 << 20, acq="ei", k=8)
     assert len(sp.topk(8)) == 8
