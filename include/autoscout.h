@@ -292,7 +292,9 @@ as_status autoscout_set_slice(as_space* s, uint64_t max_candidates);
  * first slice (decode, mask, simulator) before waiting, so the host fit overlaps GPU work.  An
  * error of the deferred fit (AS_ERR_NUMERIC: covariance not positive definite) is returned by that
  * next call, once; the handle then keeps the previous observed set.  Results are identical to the
- * synchronous mode.  Off by default; with enable = 0 any pending fit is completed first. */
+ * synchronous mode.  Only observed sets of >= 128 points are fitted asynchronously (smaller fits
+ * take tens of microseconds and stay inline).  Off by default; with enable = 0 any pending fit is
+ * completed first. */
 as_status autoscout_set_async_observe(as_space* s, int32_t enable);
 
 /* Device-time of the last score kernel launch in ms (CUDA events on the launching stream,
