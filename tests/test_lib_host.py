@@ -102,6 +102,23 @@ def test_host_gp_fit_matches_oracle(oracle_spaces, name, M):
     assert fstar == pytest.approx(fit.fstar, rel=1e-15)
 
 
+def test_async_observe_flag_on_host_only_handle(oracle_spaces):
+    """set_async_observe on a host-only handle: accepted, observe() stays synchronous (the
+    asynchronous fit exists for the device path), and the fit equals the oracle's."""
+    o = oracle_spaces["C2"]
+    sp = A.Space(space_path("C2"), -1)
+    sp.set_async_observe(True)
+    raws, costs = observed(o, 130)
+    fit = run.observed_fit(o, raws, costs)
+    sp.observe(raws, costs)
+    m, b, fstar = sp.observe_info()
+    assert m == 130
+    assert b == pytest.approx(fit.b, rel=1e-13, abs=1e-15)
+    sp.set_async_observe(False)
+    sp.observe_clear()
+    assert sp.observe_info()[0] == 0
+
+
 def observed(o, M, seed=0):
     def unrank(p):
         dg = o.cvi_unrank(p)
