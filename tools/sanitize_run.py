@@ -14,6 +14,7 @@ from bench import observed_with_library  # noqa: E402
 
 n4 = int(os.environ.get("AS_SAN_N", 1 << 14))
 for cfg, M, mode, count, path in [("C2", 64, "range", None, "tc2"), ("C4", 256, "sample", n4, "auto"),
+                                  ("C5", 128, "range", n4, "auto"),   # lag mode (two accumulators)
                                   ("C2", 64, "range", 20000, "tc"), ("C1", 16, "range", None, "simt")]:
     sp = Space(os.path.join(ROOT, "spaces", f"{cfg}.json"), 0)
     raws, costs = observed_with_library(sp, M, 0)
@@ -27,6 +28,12 @@ for cfg, M, mode, count, path in [("C2", 64, "range", None, "tc2"), ("C4", 256, 
     pool = sp.topk_pool_device(16, 80)
     merged, cert = sp.topk_merge_device(torch.cat([pool, pool]), 2, 80, 16)
     print(cfg, path, "top1", top[0], "merged", merged[0], cert, flush=True)
+    # the bench configuration: no per-candidate outputs (early rejection on), asynchronous observe
+    sp.set_async_observe(True)
+    sp.observe_clear()
+    sp.observe(raws, costs)
+    sp.score_batch(mode=mode, begin=0, count=n, acq="ei", k=16)
+    assert sp.topk(16) == top
 sp = Space(os.path.join(ROOT, "spaces", "C2.json"), 0)
 raws, costs = observed_with_library(sp, 64, 0)
 sp.observe(raws, costs)
