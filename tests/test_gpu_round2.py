@@ -306,3 +306,28 @@ def test_async_observe_deferred_error():
     assert sp.observe_info() == before
     sp.score_batch(mode="range", begin=0, count=1 << 20, acq="ei", k=8)
     assert len(sp.topk(8)) == 8
+
+
+def test_async_observe_list_mode_and_slices():
+    """Asynchronous observe with the early slice-0 generation: a LIST batch and a SAMPLE batch cut
+    into several generation slices (set_slice) give the synchronous handle's certified top-k."""
+    o = oracle_space("C4")
+    raws, costs = observed(o, 256, 0)
+    rng = np.random.default_rng(5)
+    pos = np.unique(rng.integers(0, o.n_cvi(), 300_000, dtype=np.int64))
+    d_pos = torch.tensor(pos, device="cuda")
+    results = []
+    for async_on in (False, True):
+        sp = A.Space(space_path("C4"), 0)
+        sp.set_async_observe(async_on)
+        sp.set_slice(1 << 20)                            # 3e6 SAMPLE candidates -> 3 slices
+        sp.observe(raws, costs)
+        sp.score_batch(mode="list", begin=0, count=len(pos), acq="ei", k=32, d_positions=d_pos)
+        top_l = sp.topk(32)
+        sp.observe_clear()
+        sp.observe(raws, costs)
+        sp.score_batch(mode="sample", begin=0, count=3_000_000, seed=9, acq="ei", k=32)
+        top_s = sp.topk(32)
+        results.append((top_l, top_s))
+    torch.cuda.synchronize()
+    assert results[0] == results[1]
